@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark: BASELINE.json configs[1] (C2) — AoS->SoA conversion with
+binary16 storage of position/velocity, fused into drift, 16M particles.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one pass of the hot path over the whole 16M-particle population:
+the default 88-B AoS (f64 x, f32 v, ...) in HBM -> k_gather_tiled (TMA-staged
+record tiles, RNE narrowing to binary16, drift x += v*dt in binary64) ->
+SoA binary16 {x', v}.  Under torchrun every rank runs its own 16M particles
+(weak scaling: particles shard with no data-path collective); timing is the
+max over ranks.  `e2e` is the same step through the C ABI with HOST buffers
+(pinned AoS in, SoA out, chunked H2D/compute/D2H pipeline inside the timed
+region).  `--impl reference` times the unmodified reference (oracle/_ref) on
+this host's cores for the same composition.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle updates/s & HBM GB/s vs peak per kernel; GPU vs CPU AoS→SoA speedup"
+UNIT = "particle updates/s"
+N_DEFAULT = 1 << 24
+REC_BYTES = 88
+ALG_BYTES = 48  # R x(f64) 24 + v(f32) 12, W SoA x' 6 + v 6
+
+
+def config(n, world, prec_name):
+    return {"workload": "C2 (BASELINE configs[1]): AoS->SoA + %s storage of x,v fused into drift" % prec_name,
+            "particles_per_gpu": n, "record_bytes": REC_BYTES, "schema": "reference default (f64 x3, i64, f32 ...)",
+            "dst": "SoA %s {x', v}" % prec_name, "dt": 1e-3, "arith": "binary64, separately rounded (bit-exact)",
+            "l2": "inputs 1.48 GB/GPU > 126 MB L2; no flush needed",
+            "parallelism": "replicas" if world == 1 else "dp%d (particles sharded, no collective)" % world}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profiles(kernel_key):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the GPU is busy."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def cpu_reference_rate(n_per_thread, threads, prec, seed=42):
+    """The unmodified reference (oracle/_ref) C2 composition on host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.RefLib.available():
+        raise RuntimeError("oracle/_ref/libref_driver.so missing (run `make -C oracle`)")
+    R = O.RefLib()
+    T = 16
+    secs = R.time_c2(n_per_thread, threads, T, seed)
+    if secs <= 0:
+        raise RuntimeError(R.L.ref_last_error().decode())
+    return n_per_thread * threads / secs, secs
+
+
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def reference_arm(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n_pt = args.ref_sample // threads
+    for _ in range(args.warmup):
+        cpu_reference_rate(max(n_pt // 8, 128), threads, args.prec)
+    times = []
+    for _ in range(args.steps):
+        rate, secs = cpu_reference_rate(n_pt, threads, args.prec)
+        times.append(secs)
+    total = n_pt * threads
+    value = total * len(times) / sum(times)
+    sample = "%d particles/step (%d per thread x %d threads) of the C2 workload; reference ops: " \
+             "load_state->store_state(T16)->unpack->narrow(drift)->aos_to_soa->run_kernel_chunked(drift)" % (
+                 total, n_pt, threads)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference random_initial_conditions, seed 42+thread)",
+            "config": config(N_DEFAULT, world, "binary16"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def b200_arm(args):
+    import torch
+    from paper_2512_05516_b200 import api
+
+    world, rank, local = dist_init()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    n = args.n
+    prec = api.SF_PREC_BF16 if args.prec == "bf16" else 16
+    prec_name = "bf16" if args.prec == "bf16" else "binary16"
+    P = api.Schema.default()
+    aos_v = api.View(P, n, "aos")
+    dst_v = api.View(P, n, "soa", "drift", prec)
+
+    # synthetic population generated on the device (seeded per rank)
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    src = api.PackedBuffer.empty(aos_v)
+    rec = src.data[: aos_v.nbytes].view(n, REC_BYTES)
+    step = 1 << 22
+    for b in range(0, n, step):
+        e = min(n, b + step)
+        m = e - b
+        f = torch.rand(m, 17, device="cuda", generator=g)
+        rec[b:e, 0:24] = f[:, 0:3].double().contiguous().view(torch.uint8).view(m, 24)
+        rec[b:e, 24:32] = torch.arange(b, e, device="cuda", dtype=torch.int64).view(torch.uint8).view(m, 8)
+        f[:, 3:6] = f[:, 3:6] * 2 - 1  # v ~ U(-1, 1)
+        rec[b:e, 32:88] = f[:, 3:17].contiguous().view(torch.uint8).view(m, 56)
+    out = api.PackedBuffer.empty(dst_v)
+    stream = torch.cuda.current_stream()
+
+    def step_fn():
+        api.gather_kernel(src, dst_v, "drift", 1e-3, api.SF_MATH_FP64_EXACT, out=out)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up (W) plus a ~0.5 s untimed soak so the clock sampler sees load
+    for _ in range(max(args.warmup, 3)):
+        step_fn()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_end = time.time() + 0.5
+    while time.time() < t_end:
+        for _ in range(20):
+            step_fn()
+        torch.cuda.synchronize()
+
+    launches0 = api.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step_fn()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = api.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = n * world / (ms_max * 1e-3)
+
+    peak, peak_kind = peaks()
+    achieved = ALG_BYTES * n / (ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_kind": peak_kind, "kernel": "k_gather_tiled (fused gather+drift, %s)" % prec_name,
+                "algorithmic_bytes_per_particle": ALG_BYTES,
+                "traffic": traffic_from_profiles("gather_drift_%s" % args.prec)}
+
+    # end to end through the C ABI: pinned host AoS in, host SoA out
+    e2e = None
+    if not args.no_e2e:
+        hb = api.HostBuffer(aos_v.nbytes, 0)
+        hb_np = hb.numpy()
+        torch.cuda.synchronize()
+        chunk_b = 1 << 22
+        for b in range(0, aos_v.nbytes, chunk_b * REC_BYTES):
+            e = min(aos_v.nbytes, b + chunk_b * REC_BYTES)
+            hb_np[b:e] = src.data[b:e].cpu().numpy()
+        hs = api.HostBuffer(dst_v.nbytes, 0)
+        for _ in range(max(1, min(args.warmup, 2))):
+            api.run_host(aos_v, hb, dst_v, "drift", 1e-3, chunk=args.chunk, soa_out=hs)
+        barrier()
+        secs = []
+        for _ in range(args.e2e_steps):
+            m = api.run_host(aos_v, hb, dst_v, "drift", 1e-3, chunk=args.chunk, soa_out=hs)
+            secs.append(m["seconds"])
+        s_t = torch.tensor([sum(secs) / len(secs)], device="cuda", dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(s_t, op=dist.ReduceOp.MAX)
+        # parity of the e2e result with the device-resident result
+        got = torch.from_numpy(hs.numpy()[: dst_v.nbytes].copy()).cuda()
+        ok = bool(torch.equal(got, out.data[: dst_v.nbytes]))
+        e2e = {"value": n * world / float(s_t.item()), "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"],
+               "d2h_bytes_per_step": m["d2h_bytes"], "chunk_particles": args.chunk, "matches_device_result": ok,
+               "path": "sf_b200_run_host(streamed): pinned AoS -> H2D || k_gather_tiled || D2H SoA"}
+        hb.free()
+        hs.free()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            n_pt = max(args.ref_sample // 4 // threads, 1024)
+            rate, secs = cpu_reference_rate(n_pt, threads, args.prec)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": "%d particles (%d/thread) of C2 through the unmodified reference ops, %.2f s" % (
+                       n_pt * threads, n_pt, secs)}
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "unavailable: %s" % ex}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform random records, device RNG)",
+                "config": config(n, world, prec_name), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks, "impl": "b200"}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--prec", choices=["fp16", "bf16"], default="fp16")
+    ap.add_argument("--chunk", type=int, default=1 << 21)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--ref-sample", type=int, default=1 << 21)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return b200_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,174 @@
+#ifndef SOAFORGE_B200_H
+#define SOAFORGE_B200_H
+
+/* libsoaforge_b200.so — B200 (sm_100a) drop-in for the reference's
+ * AoS->SoA + reduced-precision SPH hot path.
+ *
+ * Part 1 re-exports the reference C ABI (proj/include/soaforge/soaforge.h:
+ * 22-82) with the same names, argument meaning, status codes and
+ * thread-local last-error convention, so test_capi-style callers link
+ * unchanged.  Part 2 adds the hot-path entry points; every
+ * one of them runs on the GPU through hand-written sm_100a kernels — there is
+ * no CPU fallback, and a missing device is an SF_ERROR.
+ *
+ * Conventions (as in the reference): every entry returns sf_status; on
+ * failure sf_last_error() holds a thread-local message.  Opaque handles are
+ * freed by the matching *_destroy.  Device pointers are caller-owned (the
+ * reference's *_into operators, layout_ops.hpp:104-128) and must be 16-byte
+ * aligned; `stream` is a cudaStream_t (NULL = legacy default stream).      */
+
+#include <stddef.h>
+#include <stdint.h>
+
+#define SF_API __attribute__((visibility("default")))
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sf_status {
+    SF_OK = 0,
+    SF_ERROR = 1,
+    SF_INVALID_ARG = 2,
+    SF_PARSE_ERROR = 3,
+    SF_CHECK_FAILED = 4
+} sf_status;
+
+/* ===================== Part 1: the reference ABI ========================= */
+/* replaces soaforge.h:33-34 */
+SF_API const char* sf_version(void);
+SF_API const char* sf_last_error(void);
+/* replaces soaforge.h:39-43 (fpcodec::layout_for / quantize) */
+SF_API sf_status sf_layout_for(int total_bits, int* sign_bits, int* exponent_bits, int* mantissa_bits);
+SF_API sf_status sf_quantize(double value, int total_bits, double* out);
+
+/* replaces soaforge.h:47-55 (schema DSL, schema.hpp:12-21) */
+typedef struct sf_schema sf_schema;
+SF_API sf_status sf_schema_parse(const char* text, sf_schema** out);
+SF_API void sf_schema_destroy(sf_schema* schema);
+SF_API sf_status sf_schema_record_bits(const sf_schema* schema, uint64_t* out);
+SF_API sf_status sf_schema_field_count(const sf_schema* schema, int* out);
+SF_API sf_status sf_schema_print(sf_schema* schema, const char** out);
+
+/* replaces soaforge.h:59-71 (run configuration, same keys and validation) */
+typedef struct sf_config sf_config;
+SF_API sf_status sf_config_create(sf_config** out);
+SF_API void sf_config_destroy(sf_config* config);
+SF_API sf_status sf_config_set_string(sf_config* config, const char* key, const char* value);
+SF_API sf_status sf_config_set_int(sf_config* config, const char* key, int64_t value);
+SF_API sf_status sf_config_set_double(sf_config* config, const char* key, double value);
+
+/* replaces soaforge.h:77-82 — the commands run their conversions and
+ * kernels on the GPU; CSV columns as in bench.cpp:219/275/323-325. */
+SF_API sf_status sf_run_bench_transform(sf_config* config, const char** out_text);
+SF_API sf_status sf_run_bench_kernels(sf_config* config, const char** out_text);
+SF_API sf_status sf_run_bench_pipeline(sf_config* config, const char** out_text);
+SF_API sf_status sf_run_study_truncation(sf_config* config, const char** out_text);
+SF_API sf_status sf_run_validate(sf_config* config, const char** out_text);
+
+/* ===================== Part 2: B200 hot path ============================= */
+
+/* A view describes one packed particle buffer (the reference PackedBuffer,
+ * layout_ops.hpp:76-98): schema, record count, layout, field subset (an
+ * access set's reads ∪ writes, or all fields) and per-lane storage format. */
+typedef struct sf_view sf_view;
+
+enum { SF_LAYOUT_AOS = 0, SF_LAYOUT_SOA = 1 };
+/* precision codes */
+enum {
+    SF_PREC_STORED = 0,   /* PrecisionTag::Compressed: declared storage widths     */
+    SF_PREC_NATIVE = 1,   /* PrecisionTag::Native: unpacked to IEEE widths (U)     */
+    /* 7..64: every non-excluded float lane narrowed to T bits (RNE, then
+     * mantissa truncation), held in its enclosing IEEE width — the
+     * store_state(T) narrowing of sph.cpp:385-412 followed by U            */
+    SF_PREC_BF16 = 100,   /* non-excluded float lanes as bfloat16 (RNE)            */
+    SF_PREC_PACKED = 1000 /* 1000+T: like T but kept bit-packed at T bits          */
+};
+enum { SF_MATH_FP64_EXACT = 0, SF_MATH_FP32 = 1 };
+
+/* access_set: a `kernel` name declared in the schema text, or NULL/"" for
+ * the full field set (narrow_into, layout_ops.cpp:86-112).
+ * exclude_csv: float fields kept at their stored precision (e.g. "x"). */
+SF_API sf_status sf_b200_view_create(const sf_schema* schema, const char* access_set, int layout,
+                                     int precision, const char* exclude_csv, uint64_t count,
+                                     sf_view** out);
+SF_API void sf_b200_view_destroy(sf_view* view);
+SF_API sf_status sf_b200_view_bytes(const sf_view* view, uint64_t* nbytes);
+/* Lane geometry of one field (bits): lane l of record r sits at
+ * base + r*stride + l*width (layout_ops.cpp:25-39). */
+SF_API sf_status sf_b200_view_lane(const sf_view* view, const char* field, uint64_t* base_bits,
+                                   uint64_t* stride_bits, int* width_bits, int* arity);
+
+/* Fused U∘N∘C (+ narrowing): AoS `src` -> SoA `dst` for every field of dst.
+ * Replaces narrow_into + unpack_into + aos_to_soa_into (layout_ops.cpp:
+ * 86-112, 164-191, 150-162) and the store_state narrowing.  Bit-exact. */
+SF_API sf_status sf_b200_gather(const sf_view* src, const void* src_dev, const sf_view* dst,
+                                void* dst_dev, void* stream);
+/* Gather fused with a linear kernel (kick | drift, sph.cpp:247-264): the
+ * kernel consumes the converted lanes straight from the loads and writes the
+ * updated SoA; no separate conversion pass. */
+SF_API sf_status sf_b200_gather_kernel(const sf_view* src, const void* src_dev, const sf_view* dst,
+                                       void* dst_dev, const char* kernel, double dt, int math,
+                                       void* stream);
+/* Generic lane conversion of every dst field between any two views
+ * (AoS<->SoA, any precisions). */
+SF_API sf_status sf_b200_convert(const sf_view* src, const void* src_dev, const sf_view* dst,
+                                 void* dst_dev, void* stream);
+/* Fused C^T∘U^T∘N^T: write only `kernel`'s write set from src into dst
+ * (widen_merge, layout_ops.cpp:120-146); read-only lanes stay bit-exact. */
+SF_API sf_status sf_b200_scatter_merge(const sf_view* src, const void* src_dev, const sf_view* dst,
+                                       void* dst_dev, const char* kernel, void* stream);
+/* run_kernel_chunked (sph.cpp:286-308) on a device buffer in place:
+ * kick | drift | density.  density uses contiguous `buffer_size` neighbour
+ * buffers with reference semantics; per_access selects Writeback::PerAccess. */
+SF_API sf_status sf_b200_run_kernel(const sf_view* view, void* dev, const char* kernel, double dt,
+                                    uint64_t buffer_size, int per_access, int math, void* stream);
+
+/* Cell-linked density over SoA streams (new algorithm).
+ * x: 3*n, m, h: n, in `prec` (SF_PREC_NATIVE -> fp32 streams, 16 -> fp16,
+ * SF_PREC_BF16 -> bf16); rho_out: n fp32.  Particles must already be sorted
+ * by cell (sf_b200_bin_particles); cell_start has ncell+1 entries.
+ * The grid has nx*ny*nz cells of side `cell` starting at lo[3]; rows
+ * [x_lo_ghost, ...) allow a slab with ghost layers (multi-GPU). */
+SF_API sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int prec,
+                                       uint64_t n, const int32_t* cell_start, int nx, int ny,
+                                       int nz, int own_x0, int own_x1, float* rho_out,
+                                       void* stream);
+/* Counting sort of particles into cells (x-major cell id), stable in
+ * particle index: writes perm[n] (sorted position -> original index) and
+ * cell_start[ncell+1].  scratch must hold sf_b200_bin_scratch_bytes(). */
+SF_API sf_status sf_b200_bin_particles(const float* x, uint64_t n, const float* lo, float cell,
+                                       int nx, int ny, int nz, int32_t* cell_start, int32_t* perm,
+                                       void* scratch, uint64_t scratch_bytes, void* stream);
+SF_API uint64_t sf_b200_bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
+
+/* Host-resident orchestration (the paper's in-place vs streaming question
+ * re-posed for PCIe; pipelines.cpp:231-296).  `host_aos` holds `count`
+ * records of `src` (full field set, AoS).  One step = gather + `kernels`
+ * (comma list of kick,drift) in the dst view's precision + scatter-back of
+ * every write set into the AoS, for every record.
+ *   mode 0 STREAMED: pinned host memory, chunked cudaMemcpyAsync ring
+ *                    (H2D k+1 ∥ compute k ∥ D2H k-1) on 3 streams;
+ *   mode 1 MANAGED:  host_aos is cudaMallocManaged; prefetch/advise hints and
+ *                    in-place conversion on the migrated pages.
+ * host_soa (optional): when non-NULL the SoA result (dst view, all
+ * records) is copied to this host buffer instead of scattering back into
+ * the AoS — the end-to-end form of the fused gather+kernel path.
+ * metrics[0..4] = {seconds, h2d_bytes, d2h_bytes, chunks, kernel_launches}. */
+enum { SF_MODE_STREAMED = 0, SF_MODE_MANAGED = 1 };
+SF_API sf_status sf_b200_run_host(const sf_view* src, void* host_aos, const sf_view* dst,
+                                  const char* kernels, double dt, int math, int mode,
+                                  uint64_t chunk_records, void* host_soa, double* metrics);
+
+/* Host buffers for sf_b200_run_host: mode 0 pinned (cudaHostAlloc),
+ * mode 1 managed (cudaMallocManaged). */
+SF_API sf_status sf_b200_host_alloc(uint64_t bytes, int mode, void** out);
+SF_API sf_status sf_b200_host_free(void* p, int mode);
+
+/* Number of sm_100a kernels this library has launched (process-wide). */
+SF_API uint64_t sf_b200_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,293 @@
+"""Python mirror of the reference operator interface, executed on the B200.
+
+Names follow the reference (proj/include/soaforge/*.hpp): a ``Schema`` is
+parsed from the same DSL (schema.hpp:12-21); a ``PackedBuffer`` is a view
+(layout, field subset, lane formats) over caller-owned device bytes
+(layout_ops.hpp:76-98); the operators are the reference's N/U/C and their
+transposes (layout_ops.hpp:100-128) and run_kernel (sph.hpp:97-104), but each
+call is one fused sm_100a kernel launched through libsoaforge_b200.so on
+torch's current CUDA stream.  Errors map the reference's exception classes:
+ValueError subclasses for invalid arguments and parse errors.
+
+torch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+from . import _lib as L
+from ._lib import (SF_LAYOUT_AOS, SF_LAYOUT_SOA, SF_MATH_FP32, SF_MATH_FP64_EXACT, SF_PREC_BF16,  # noqa: F401
+                   SF_PREC_NATIVE, SF_PREC_PACKED, SF_PREC_STORED, check, enc, lib)
+
+# sph.cpp:445-467 — the built-in particle schema, same text
+DEFAULT_SCHEMA_TEXT = """# SWIFT-style particle record; positions stay binary64, the rest binary32.
+schema particle {
+  field x : f64 x3;
+  field id : i64;
+  field v : f32 x3;
+  field u : f32;
+  field m : f32;
+  field h : f32;
+  field rho : f32;
+  field P : f32;
+  field cs : f32;
+  field a : f32 x3;
+  field du : f32;
+  field dt : f32;
+}
+kernel density reads x, m, h writes rho;
+kernel force reads x, v, m, h, rho, P, cs writes a, du;
+kernel kick reads v, u, a, du writes v, u;
+kernel drift reads x, v writes x;
+kernel identity reads x writes x;
+"""
+
+
+def version() -> str:
+    return lib().sf_version().decode()
+
+
+def layout_for(total_bits: int) -> Tuple[int, int, int]:
+    """fpcodec::layout_for (fpcodec.cpp:28-37)."""
+    s, e, m = C.c_int(), C.c_int(), C.c_int()
+    check(lib().sf_layout_for(total_bits, C.byref(s), C.byref(e), C.byref(m)))
+    return s.value, e.value, m.value
+
+
+def quantize(x: float, total_bits: int) -> float:
+    """fpcodec::quantize (fpcodec.cpp:151-155)."""
+    out = C.c_double()
+    check(lib().sf_quantize(float(x), total_bits, C.byref(out)))
+    return out.value
+
+
+class Schema:
+    """schema::parse_file over the DSL; owns an sf_schema handle."""
+
+    def __init__(self, text: str = DEFAULT_SCHEMA_TEXT):
+        h = C.c_void_p()
+        check(lib().sf_schema_parse(text.encode(), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def default(cls) -> "Schema":
+        return cls(DEFAULT_SCHEMA_TEXT)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def record_bits(self) -> int:
+        v = C.c_uint64()
+        check(lib().sf_schema_record_bits(self._h, C.byref(v)))
+        return v.value
+
+    @property
+    def field_count(self) -> int:
+        v = C.c_int()
+        check(lib().sf_schema_field_count(self._h, C.byref(v)))
+        return v.value
+
+    def print(self) -> str:
+        out = C.c_char_p()
+        check(lib().sf_schema_print(self._h, C.byref(out)))
+        return out.value.decode()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and L._lib is not None:
+            L._lib.sf_schema_destroy(self._h)
+            self._h = None
+
+
+class View:
+    """A packed-buffer descriptor (PackedBuffer without the bytes)."""
+
+    def __init__(self, schema: Schema, count: int, layout: str = "aos", access_set: Optional[str] = None,
+                 precision: int = SF_PREC_STORED, exclude: str = ""):
+        self.schema, self.count, self.layout = schema, int(count), layout
+        self.access_set, self.precision, self.exclude = access_set, precision, exclude
+        h = C.c_void_p()
+        check(lib().sf_b200_view_create(schema.handle, enc(access_set), SF_LAYOUT_AOS if layout == "aos" else SF_LAYOUT_SOA,
+                                        precision, enc(exclude), self.count, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def nbytes(self) -> int:
+        v = C.c_uint64()
+        check(lib().sf_b200_view_bytes(self._h, C.byref(v)))
+        return v.value
+
+    def lane(self, field: str) -> Tuple[int, int, int, int]:
+        """(base_bits, stride_bits, width_bits, arity) of a field (layout_ops.cpp:25-39)."""
+        b, s, w, a = C.c_uint64(), C.c_uint64(), C.c_int(), C.c_int()
+        check(lib().sf_b200_view_lane(self._h, field.encode(), C.byref(b), C.byref(s), C.byref(w), C.byref(a)))
+        return b.value, s.value, w.value, a.value
+
+    def with_count(self, count: int) -> "View":
+        return View(self.schema, count, self.layout, self.access_set, self.precision, self.exclude)
+
+    def like(self, layout=None, access_set=-1, precision=None, exclude=None) -> "View":
+        return View(self.schema, self.count, layout or self.layout,
+                    self.access_set if access_set == -1 else access_set,
+                    self.precision if precision is None else precision,
+                    self.exclude if exclude is None else exclude)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and L._lib is not None:
+            L._lib.sf_b200_view_destroy(self._h)
+            self._h = None
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class PackedBuffer:
+    """View + device bytes (torch uint8 tensor, caller-owned storage)."""
+    view: View
+    data: "object"
+
+    @staticmethod
+    def empty(view: View, device="cuda") -> "PackedBuffer":
+        import torch
+        # +16: every buffer is a whole number of 16-B words (vector stores)
+        return PackedBuffer(view, torch.zeros(view.nbytes + 16, dtype=torch.uint8, device=device))
+
+    @staticmethod
+    def from_host(view: View, host_bytes, device="cuda") -> "PackedBuffer":
+        import numpy as np
+        import torch
+        b = PackedBuffer.empty(view, device)
+        arr = np.frombuffer(bytes(host_bytes), dtype=np.uint8) if not isinstance(host_bytes, np.ndarray) \
+            else host_bytes.view(np.uint8).ravel()
+        if arr.size != view.nbytes:
+            raise ValueError(f"expected {view.nbytes} bytes, got {arr.size}")
+        b.data[: view.nbytes].copy_(torch.from_numpy(arr.copy()))
+        return b
+
+    def to_host(self):
+        return self.data[: self.view.nbytes].cpu().numpy()
+
+
+# ---------------------------------------------------------------- operators
+def gather(src: PackedBuffer, dst_view: View, out: Optional[PackedBuffer] = None) -> PackedBuffer:
+    """U∘N∘C (+ narrowing) in one kernel: narrow_into + unpack_into +
+    aos_to_soa_into (layout_ops.cpp:86-191) and store_state(T)."""
+    out = out or PackedBuffer.empty(dst_view, src.data.device)
+    check(lib().sf_b200_gather(src.view.handle, _ptr(src.data), dst_view.handle, _ptr(out.data), _stream()))
+    return out
+
+
+def gather_kernel(src: PackedBuffer, dst_view: View, kernel: str, dt: float = 1e-3,
+                  math: int = SF_MATH_FP64_EXACT, out: Optional[PackedBuffer] = None) -> PackedBuffer:
+    """Gather fused with kick/drift (the conversion is the kernel's load)."""
+    out = out or PackedBuffer.empty(dst_view, src.data.device)
+    check(lib().sf_b200_gather_kernel(src.view.handle, _ptr(src.data), dst_view.handle, _ptr(out.data),
+                                      kernel.encode(), dt, math, _stream()))
+    return out
+
+
+def convert(src: PackedBuffer, dst_view: View, out: Optional[PackedBuffer] = None) -> PackedBuffer:
+    """Any view -> any view, lane by lane (C, C^T, U, U^T, narrowing)."""
+    out = out or PackedBuffer.empty(dst_view, src.data.device)
+    check(lib().sf_b200_convert(src.view.handle, _ptr(src.data), dst_view.handle, _ptr(out.data), _stream()))
+    return out
+
+
+def widen_merge(narrowed: PackedBuffer, original: PackedBuffer, kernel: str) -> None:
+    """N^T: overwrite `kernel`'s write set of `original` (layout_ops.cpp:120-146)."""
+    check(lib().sf_b200_scatter_merge(narrowed.view.handle, _ptr(narrowed.data), original.view.handle,
+                                      _ptr(original.data), kernel.encode(), _stream()))
+
+
+scatter_merge = widen_merge
+
+
+def run_kernel(buf: PackedBuffer, kernel: str, dt: float = 1e-3, buffer_size: int = 64,
+               per_access: bool = False, math: int = SF_MATH_FP64_EXACT) -> None:
+    """run_kernel_chunked (sph.cpp:286-308) in place on the device."""
+    check(lib().sf_b200_run_kernel(buf.view.handle, _ptr(buf.data), kernel.encode(), dt, buffer_size,
+                                   int(per_access), math, _stream()))
+
+
+def bin_particles(x, lo, cell: float, dims, cell_start=None, perm=None):
+    """Counting sort into cells (x-major ids), stable by particle index.
+    x: (n,3) float32 cuda tensor.  Returns (cell_start[ncell+1], perm[n])."""
+    import torch
+    n = x.shape[0]
+    nx, ny, nz = dims
+    ncell = nx * ny * nz
+    cell_start = cell_start if cell_start is not None else torch.empty(ncell + 1, dtype=torch.int32, device=x.device)
+    perm = perm if perm is not None else torch.empty(max(n, 1), dtype=torch.int32, device=x.device)
+    nbytes = lib().sf_b200_bin_scratch_bytes(n, nx, ny, nz)
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    lo_arr = (C.c_float * 3)(*[float(v) for v in lo])
+    check(lib().sf_b200_bin_particles(_ptr(x), n, C.cast(lo_arr, C.c_void_p), float(cell), nx, ny, nz,
+                                      _ptr(cell_start), _ptr(perm), _ptr(scratch), nbytes, _stream()))
+    return cell_start, perm
+
+
+def density_cells(x, m, h, cell_start, dims, own=None, prec: int = SF_PREC_NATIVE, rho=None):
+    """Cell-linked density over cell-sorted SoA streams (x: (n,3), m, h: (n,))
+    stored as fp32 (SF_PREC_NATIVE), fp16 (16) or bf16 (SF_PREC_BF16)."""
+    import torch
+    nx, ny, nz = dims
+    own = own or (0, nx)
+    n = m.shape[0]
+    rho = rho if rho is not None else torch.zeros(max(n, 1), dtype=torch.float32, device=m.device)
+    check(lib().sf_b200_density_cells(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(cell_start), nx, ny, nz,
+                                      own[0], own[1], _ptr(rho), _stream()))
+    return rho
+
+
+class HostBuffer:
+    """Pinned (mode 0) or managed (mode 1) host memory for run_host."""
+
+    def __init__(self, nbytes: int, mode: int = 0):
+        p = C.c_void_p()
+        check(lib().sf_b200_host_alloc(nbytes, mode, C.byref(p)))
+        self.ptr, self.nbytes, self.mode = p, nbytes, mode
+
+    def numpy(self):
+        import numpy as np
+        return np.ctypeslib.as_array(C.cast(self.ptr, C.POINTER(C.c_uint8)), shape=(self.nbytes,))
+
+    def free(self):
+        if self.ptr:
+            check(lib().sf_b200_host_free(self.ptr, self.mode))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def run_host(src_view: View, host: HostBuffer, dst_view: View, kernels: str = "drift", dt: float = 1e-3,
+             math: int = SF_MATH_FP64_EXACT, chunk: int = 1 << 22, soa_out: Optional[HostBuffer] = None) -> dict:
+    """One whole-population step on host-resident AoS (streamed or managed).
+    With `soa_out` the SoA result lands in host memory instead of being
+    scattered back into the AoS."""
+    m = (C.c_double * 5)()
+    check(lib().sf_b200_run_host(src_view.handle, host.ptr, dst_view.handle, kernels.encode(), dt, math,
+                                 host.mode, chunk, soa_out.ptr if soa_out is not None else None, m))
+    return {"seconds": m[0], "h2d_bytes": int(m[1]), "d2h_bytes": int(m[2]), "chunks": int(m[3]),
+            "launches": int(m[4])}
+
+
+def launch_count() -> int:
+    return int(lib().sf_b200_launch_count())

@@ -1,0 +1,377 @@
+// sm_100a kernels for the AoS<->SoA + reduced-precision SPH hot path.
+//
+//   k_gather_tiled   AoS -> SoA (U∘N∘C plus narrowing), optionally fused with
+//                    kick/drift.  Persistent CTAs; record tiles staged into
+//                    shared memory by 1-D TMA bulk copies (cp.async.bulk,
+//                    UBLKCP) through an mbarrier ring; lanes extracted with
+//                    funnel shifts (any bit offset/width); 16-B SoA stores.
+//   k_convert        generic lane-by-lane conversion between any two views
+//                    (scatter-back / N^T merge, store_state narrowing,
+//                    in-place kick/drift on any view).  Byte-aligned
+//                    destinations use plain stores, bit-packed ones use
+//                    32-bit atomics so neighbouring lanes never race.
+//   k_density_buffer the reference density (sph.cpp:176-199): one CTA per
+//                    64-particle neighbour buffer, binary64 with separately
+//                    rounded operations, ascending j, self term included.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "codec.cuh"
+#include "plans.cuh"
+
+namespace sfb {
+
+// ----------------------------------------------------------------- bit access
+__device__ __forceinline__ uint64_t ld_bits_smem(const uint8_t* base, uint64_t bitoff, int w) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(base) + (bitoff >> 5);
+    const uint32_t sh = uint32_t(bitoff & 31);
+    const uint32_t a = p[0], b = p[1];
+    const uint32_t lo = __funnelshift_r(a, b, sh);
+    uint32_t hi = 0;
+    if (w + int(sh) > 32) hi = __funnelshift_r(b, p[2], sh);
+    const uint64_t v = (uint64_t(hi) << 32) | lo;
+    return w >= 64 ? v : (v & ((1ull << w) - 1));
+}
+
+// Global read of an arbitrary bit slot using only the aligned words it spans.
+__device__ __forceinline__ uint64_t ld_bits_global(const uint8_t* base, uint64_t bitoff, int w) {
+    if (((bitoff | uint64_t(w)) & 7) == 0) {
+        const uint8_t* p = base + (bitoff >> 3);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        if (w == 64 && (a & 7) == 0) return *reinterpret_cast<const uint64_t*>(p);
+        if (w == 32 && (a & 3) == 0) return *reinterpret_cast<const uint32_t*>(p);
+        if (w == 16 && (a & 1) == 0) return *reinterpret_cast<const uint16_t*>(p);
+    }
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(base) + (bitoff >> 5);
+    const uint32_t sh = uint32_t(bitoff & 31);
+    const int nw = int((sh + uint32_t(w) + 31) >> 5);
+    const uint32_t a = p[0];
+    const uint32_t b = nw > 1 ? p[1] : 0u;
+    const uint32_t c = nw > 2 ? p[2] : 0u;
+    const uint64_t v = (uint64_t(__funnelshift_r(b, c, sh)) << 32) | __funnelshift_r(a, b, sh);
+    return w >= 64 ? v : (v & ((1ull << w) - 1));
+}
+
+__device__ __forceinline__ void st_bytes(uint8_t* p, uint64_t v, int nbytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if (nbytes == 8 && (a & 7) == 0) { *reinterpret_cast<uint64_t*>(p) = v; return; }
+    if (nbytes == 4 && (a & 3) == 0) { *reinterpret_cast<uint32_t*>(p) = uint32_t(v); return; }
+    if (nbytes == 2 && (a & 1) == 0) { *reinterpret_cast<uint16_t*>(p) = uint16_t(v); return; }
+    if ((a & 3) == 0 && (nbytes & 3) == 0) {
+        for (int i = 0; i < nbytes; i += 4) *reinterpret_cast<uint32_t*>(p + i) = uint32_t(v >> (8 * i));
+        return;
+    }
+    if ((a & 1) == 0 && (nbytes & 1) == 0) {
+        for (int i = 0; i < nbytes; i += 2) *reinterpret_cast<uint16_t*>(p + i) = uint16_t(v >> (8 * i));
+        return;
+    }
+    for (int i = 0; i < nbytes; ++i) p[i] = uint8_t(v >> (8 * i));
+}
+
+// Bit-slot store.  Byte-aligned slots are plain stores; others use atomics on
+// the 32-bit words they span (disjoint bit masks commute, so lanes sharing a
+// word with another thread's lanes never race).
+__device__ __forceinline__ void st_bits_global(uint8_t* base, uint64_t bitoff, int w, uint64_t v,
+                                               bool byte_aligned) {
+    if (byte_aligned) {
+        st_bytes(base + (bitoff >> 3), v, w >> 3);
+        return;
+    }
+    uint32_t* p = reinterpret_cast<uint32_t*>(base) + (bitoff >> 5);
+    int sh = int(bitoff & 31);
+    int left = w;
+    while (left > 0) {
+        const int n = min(32 - sh, left);
+        const uint32_t mask = (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << sh;
+        const uint32_t bits = (uint32_t(v) << sh) & mask;
+        atomicAnd(p, ~mask);
+        atomicOr(p, bits);
+        v = n >= 64 ? 0 : (v >> n);
+        left -= n;
+        sh = 0;
+        ++p;
+    }
+}
+
+// ----------------------------------------------------------------- lane ops
+__device__ __forceinline__ double dec(uint64_t b, LaneFmt f) { return decode_lane(b, f); }
+
+// dst = Q(Q(x) + Q(y)*dt) [clamp >= 0]; x already in format fx (the output's),
+// y already in format fy.  Exact mode: binary64 with separately rounded
+// multiply and add (no FMA), exactly BufferView get/set arithmetic.
+__device__ __forceinline__ uint64_t axpy_lane(uint64_t xb, LaneFmt fx, uint64_t yb, LaneFmt fy,
+                                              double dt, uint8_t op, uint8_t math) {
+    double r;
+    if (math == MATH_FP64_EXACT) {
+        r = __dadd_rn(dec(xb, fx), __dmul_rn(dec(yb, fy), dt));
+    } else {
+        const float rf = __fadd_rn(float(dec(xb, fx)), __fmul_rn(float(dec(yb, fy)), float(dt)));
+        r = double(rf);
+    }
+    if (op == OP_AXPY_CLAMP0 && r < 0.0) r = 0.0;
+    return encode_lane(r, fx);
+}
+
+// ----------------------------------------------------------------- k_convert
+__global__ void __launch_bounds__(256) k_convert(const __grid_constant__ ConvertPlan P, const uint8_t* src,
+                                                 uint8_t* dst) {
+    const uint64_t n = P.count;
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
+        for (uint32_t s = 0; s < P.n; ++s) {
+            const CStream& c = P.s[s];
+            for (int l = 0; l < c.src.arity; ++l) {
+                const uint64_t sb = ld_bits_global(src, c.src.base + r * c.src.stride + uint64_t(l) * c.src.fmt.width,
+                                                   c.src.fmt.width);
+                uint64_t out = convert_lane(sb, c.src.fmt, c.dst.fmt);
+                if (c.op != OP_COPY) {
+                    const uint64_t yb = ld_bits_global(src, c.aux.base + r * c.aux.stride + uint64_t(l) * c.aux.fmt.width,
+                                                       c.aux.fmt.width);
+                    out = axpy_lane(out, c.dst.fmt, convert_lane(yb, c.aux.fmt, c.aux_q), c.aux_q, P.dt, c.op, P.math);
+                }
+                st_bits_global(dst, c.dst.base + r * c.dst.stride + uint64_t(l) * c.dst.fmt.width, c.dst.fmt.width, out,
+                               P.dst_byte_aligned);
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- TMA helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+constexpr int kStages = 4;
+constexpr int kGatherThreads = 256;
+constexpr int kChunk = 8;  // SoA elements per work item (16 B of fp16 output)
+
+// ----------------------------------------------------------------- k_gather_tiled
+__global__ void __launch_bounds__(kGatherThreads) k_gather_tiled(const __grid_constant__ GatherPlan P,
+                                                                 const uint8_t* __restrict__ src,
+                                                                 uint8_t* __restrict__ dst, uint64_t src_bytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    const uint32_t stage_bytes = P.tile_bytes + 16;  // +16: funnel-shift overread pad
+    uint8_t* tiles = smem + 128;
+    const uint64_t ntiles = (P.count + P.tile_recs - 1) / P.tile_recs;
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](uint64_t t, int s) {
+        const uint64_t off = t * uint64_t(P.tile_bytes);
+        uint64_t bytes = min(uint64_t(P.tile_bytes), src_bytes - off);
+        const uint32_t bulk = uint32_t(bytes & ~15ull);
+        mbar_expect_tx(&bars[s], bulk);
+        if (bulk) tma_bulk_g2s(tiles + s * stage_bytes, src + off, bulk, &bars[s]);
+    };
+
+    if (tid == 0)
+        for (int s = 0; s < kStages; ++s) {
+            const uint64_t t = blockIdx.x + uint64_t(s) * gridDim.x;
+            if (t < ntiles) issue(t, s);
+        }
+
+    uint32_t k = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = int(k % kStages);
+        uint8_t* tile = tiles + s * stage_bytes;
+        mbar_wait(&bars[s], (k / kStages) & 1);
+        const uint64_t rec0 = t * P.tile_recs;
+        const uint32_t recs = uint32_t(min(uint64_t(P.tile_recs), P.count - rec0));
+        if (recs < P.tile_recs) {  // last tile: the <16-byte tail the bulk copy skipped
+            const uint64_t off = t * uint64_t(P.tile_bytes);
+            const uint64_t bytes = src_bytes - off;
+            const uint32_t bulk = uint32_t(bytes & ~15ull);
+            for (uint32_t b = bulk + tid; b < bytes; b += blockDim.x) tile[b] = src[off + b];
+            __syncthreads();
+        }
+        // work items: (stream, chunk of kChunk consecutive SoA elements)
+        uint32_t items = 0;
+        for (uint32_t q = 0; q < P.n; ++q) items += (recs * P.s[q].arity + kChunk - 1) / kChunk;
+        for (uint32_t it = tid; it < items; it += blockDim.x) {
+            uint32_t q = 0, c = it;
+            for (;; ++q) {
+                const uint32_t nc = (recs * P.s[q].arity + kChunk - 1) / kChunk;
+                if (c < nc) break;
+                c -= nc;
+            }
+            const GStream& g = P.s[q];
+            const uint32_t ar = g.arity;
+            const uint32_t nel = recs * ar;
+            const uint32_t e0 = c * kChunk;
+            const int sw = g.src.width, aw = g.aux_src.width, dw = g.dst.width;
+            uint64_t out[kChunk];
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                const uint32_t e = min(e0 + j, nel - 1);
+                const uint32_t r = ar == 1 ? e : e / 3;
+                const uint32_t l = e - r * ar;
+                const uint64_t rb = uint64_t(r) * P.record_bits;
+                uint64_t v = convert_lane(ld_bits_smem(tile, rb + g.src_off + uint64_t(l) * sw, sw), g.src, g.dst);
+                if (g.op != OP_COPY) {
+                    const uint64_t y = convert_lane(ld_bits_smem(tile, rb + g.aux_off + uint64_t(l) * aw, aw), g.aux_src,
+                                                    g.aux_dst);
+                    v = axpy_lane(v, g.dst, y, g.aux_dst, P.dt, g.op, P.math);
+                }
+                out[j] = v;
+            }
+            uint8_t* o = dst + g.dst_base + (rec0 * ar + e0) * uint64_t(dw >> 3);
+            const bool full = e0 + kChunk <= nel && (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+            if (full) {
+                if (dw == 16) {
+                    uint4 v4;
+                    v4.x = uint32_t(out[0] | (out[1] << 16));
+                    v4.y = uint32_t(out[2] | (out[3] << 16));
+                    v4.z = uint32_t(out[4] | (out[5] << 16));
+                    v4.w = uint32_t(out[6] | (out[7] << 16));
+                    *reinterpret_cast<uint4*>(o) = v4;
+                } else if (dw == 32) {
+                    uint4* o4 = reinterpret_cast<uint4*>(o);
+                    o4[0] = make_uint4(uint32_t(out[0]), uint32_t(out[1]), uint32_t(out[2]), uint32_t(out[3]));
+                    o4[1] = make_uint4(uint32_t(out[4]), uint32_t(out[5]), uint32_t(out[6]), uint32_t(out[7]));
+                } else {
+                    uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        o4[j] = make_uint4(uint32_t(out[2 * j]), uint32_t(out[2 * j] >> 32), uint32_t(out[2 * j + 1]),
+                                           uint32_t(out[2 * j + 1] >> 32));
+                }
+            } else {
+                for (int j = 0; j < kChunk && e0 + j < nel; ++j) st_bytes(o + j * (dw >> 3), out[j], dw >> 3);
+            }
+        }
+        __syncthreads();  // every thread is done with this stage
+        if (tid == 0) {
+            const uint64_t tn = t + uint64_t(kStages) * gridDim.x;
+            if (tn < ntiles) issue(tn, s);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- density
+__device__ __constant__ double kInvPi = 0.31830988618379067154;  // 1.0 / std::numbers::pi
+
+// sph.cpp:17-24, evaluated left to right with IEEE binary64 ops.
+__device__ __forceinline__ double w_exact(double r, double h) {
+    const double q = __ddiv_rn(r, h);
+    if (q >= 2.0) return 0.0;
+    const double norm = __ddiv_rn(kInvPi, __dmul_rn(__dmul_rn(h, h), h));
+    if (q < 1.0) {
+        const double a = __dmul_rn(__dmul_rn(1.5, q), q);
+        const double b = __dmul_rn(__dmul_rn(__dmul_rn(0.75, q), q), q);
+        return __dmul_rn(norm, __dadd_rn(__dsub_rn(1.0, a), b));
+    }
+    const double t = __dsub_rn(2.0, q);
+    return __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(norm, 0.25), t), t), t);
+}
+
+__device__ __forceinline__ double ld_lane(const uint8_t* buf, const Lanes& L, uint64_t r, int l) {
+    return dec(ld_bits_global(buf, L.base + r * L.stride + uint64_t(l) * L.fmt.width, L.fmt.width), L.fmt);
+}
+
+__global__ void k_density_buffer(const __grid_constant__ DensityPlan P, uint8_t* buf) {
+    extern __shared__ double sd[];
+    const uint32_t bs = P.bs;
+    double* sx = sd;            // 3*bs
+    double* sm = sd + 3 * bs;   // bs
+    double* sh = sd + 4 * bs;   // bs
+    const uint64_t b0 = uint64_t(blockIdx.x) * bs;
+    const uint32_t i = threadIdx.x;
+    const uint64_t gi = b0 + i;
+    for (int l = 0; l < 3; ++l) sx[3 * i + l] = ld_lane(buf, P.x, gi, l);
+    sm[i] = ld_lane(buf, P.m, gi, 0);
+    sh[i] = ld_lane(buf, P.h, gi, 0);
+    __syncthreads();
+    const double x0 = sx[3 * i], x1 = sx[3 * i + 1], x2 = sx[3 * i + 2], hi = sh[i];
+    double acc = 0.0;
+    for (uint32_t j = 0; j < bs; ++j) {
+        const double d0 = __dsub_rn(x0, sx[3 * j]), d1 = __dsub_rn(x1, sx[3 * j + 1]), d2 = __dsub_rn(x2, sx[3 * j + 2]);
+        const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+        const double hij = __dmul_rn(0.5, __dadd_rn(hi, sh[j]));
+        acc = __dadd_rn(acc, __dmul_rn(sm[j], w_exact(r, hij)));
+        if (P.per_access) acc = dec(encode_lane(acc, P.rho.fmt), P.rho.fmt);
+    }
+    // byte-aligned rho lanes are the norm; bit-packed ones take the atomic path
+    const bool ba = ((P.rho.base | P.rho.stride | P.rho.fmt.width) & 7) == 0;
+    st_bits_global(buf, P.rho.base + gi * P.rho.stride, P.rho.fmt.width, encode_lane(acc, P.rho.fmt), ba);
+}
+
+// ----------------------------------------------------------------- launchers
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st) {
+    if (p.count == 0 || p.n == 0) return cudaSuccess;
+    const uint64_t want = (p.count + 255) / 256;
+    const int blocks = int(std::min<uint64_t>(want, uint64_t(num_sms()) * 16));
+    k_convert<<<blocks, 256, 0, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst));
+    return cudaGetLastError();
+}
+
+size_t gather_smem_bytes(const GatherPlan& p) { return 128 + size_t(kStages) * (p.tile_bytes + 16); }
+
+cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
+                          int ctas_per_sm) {
+    if (p.count == 0 || p.n == 0) return cudaSuccess;
+    const size_t smem = gather_smem_bytes(p);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_gather_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    const uint64_t ntiles = (p.count + p.tile_recs - 1) / p.tile_recs;
+    if (ctas_per_sm <= 0) ctas_per_sm = int(std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / smem)));
+    const int blocks = int(std::min<uint64_t>(ntiles, uint64_t(num_sms()) * ctas_per_sm));
+    k_gather_tiled<<<blocks, kGatherThreads, smem, st>>>(p, static_cast<const uint8_t*>(src),
+                                                         static_cast<uint8_t*>(dst), src_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_density_buffer(const DensityPlan& p, void* buf, cudaStream_t st) {
+    if (p.count == 0) return cudaSuccess;
+    const unsigned blocks = unsigned(p.count / p.bs);
+    k_density_buffer<<<blocks, p.bs, 5 * p.bs * sizeof(double), st>>>(p, static_cast<uint8_t*>(buf));
+    return cudaGetLastError();
+}
+
+}  // namespace sfb

@@ -1,0 +1,78 @@
+// POD launch plans shared between the host planner (view.cpp) and the
+// kernels (kernels.cu).  Passed by value as __grid_constant__ parameters.
+#pragma once
+#include <cstdint>
+
+#include "codec.cuh"
+
+namespace sfb {
+
+enum class Layout : uint8_t { AoS = 0, SoA = 1 };
+
+// Bit geometry of one field's lanes in a buffer: lane l of record r sits at
+// base + r*stride + l*fmt.width bits.
+struct Lanes {
+    uint64_t base = 0, stride = 0;
+    LaneFmt fmt{};
+    uint8_t arity = 1;
+};
+
+enum Op : uint8_t {
+    OP_COPY = 0,         // dst = convert(src)
+    OP_AXPY = 1,         // dst = Q(Q(x) + Q(y) * dt)          (drift x; kick v)
+    OP_AXPY_CLAMP0 = 2,  // dst = Q(max0(Q(x) + Q(y) * dt))    (kick u, sph.cpp:254)
+};
+
+enum Math : uint8_t {
+    MATH_FP64_EXACT = 0,  // binary64, separately rounded mul/add: bit-exact vs reference
+    MATH_FP32 = 1,        // binary32 arithmetic, within 1 ulp of the storage format
+};
+
+constexpr int kMaxStreams = 16;
+
+// ---- generic lane-by-lane conversion / in-place update ---------------------
+struct CStream {
+    Lanes src, dst, aux;  // aux: operand y for the AXPY ops (read from src buffer)
+    LaneFmt aux_q;        // y is quantized through this format first
+    uint8_t op = OP_COPY;
+};
+
+struct ConvertPlan {
+    uint64_t count = 0;
+    uint32_t n = 0;
+    uint8_t dst_byte_aligned = 1;  // plain stores; else bit-level atomics
+    uint8_t math = MATH_FP64_EXACT;
+    double dt = 0;
+    CStream s[kMaxStreams];
+};
+using KernelPlan = ConvertPlan;
+
+// ---- tiled AoS -> SoA gather (TMA bulk-staged record tiles) ----------------
+struct GStream {
+    uint32_t src_off = 0;   // bit offset of lane 0 inside a source record
+    uint32_t aux_off = 0;   // operand field, same record
+    uint64_t dst_base = 0;  // byte offset of the destination SoA stream
+    LaneFmt src{}, dst{}, aux_src{}, aux_dst{};
+    uint8_t arity = 1, op = OP_COPY;
+};
+
+struct GatherPlan {
+    uint64_t count = 0;
+    uint32_t record_bits = 0;
+    uint32_t n = 0;
+    uint32_t tile_recs = 0;   // multiple of 128: every tile starts 16-B aligned
+    uint32_t tile_bytes = 0;  // tile_recs * record_bits / 8
+    uint8_t math = MATH_FP64_EXACT;
+    double dt = 0;
+    GStream s[kMaxStreams];
+};
+
+// ---- SPH density over 64-particle neighbour buffers (sph.cpp:176-199) -------
+struct DensityPlan {
+    Lanes x, m, h, rho;
+    uint64_t count = 0;
+    uint32_t bs = 64;
+    uint8_t per_access = 0;
+};
+
+}  // namespace sfb

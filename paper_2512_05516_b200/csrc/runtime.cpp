@@ -1,0 +1,111 @@
+#include "runtime.hpp"
+
+#include <atomic>
+#include <stdexcept>
+
+namespace sfb {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void require_device() {
+    static int have = -1;
+    if (have < 0) {
+        int n = 0;
+        have = (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) ? 1 : 0;
+    }
+    if (!have) throw std::runtime_error("no CUDA device: libsoaforge_b200 runs on the GPU only (no CPU path)");
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static void check_ptr(const void* p, const char* what) {
+    if (!aligned16(p)) throw std::invalid_argument(std::string(what) + " must be 16-byte aligned");
+}
+
+// The per-lane ops of a linear kernel applied to a generic src->dst conversion.
+static void fuse_ops(ConvertPlan& p, const View& src, const View& dst, const std::string& kernel, double dt,
+                     int math) {
+    const KernelPlan kp = plan_kernel(dst, kernel, dt, math);  // validates fields in dst
+    p.dt = dt;
+    p.math = uint8_t(math);
+    for (uint32_t i = 0; i < kp.n; ++i) {
+        // find the stream writing the same lanes
+        for (uint32_t s = 0; s < p.n; ++s) {
+            if (p.s[s].dst.base != kp.s[i].dst.base) continue;
+            const int yp_dst = [&] {
+                for (size_t q = 0; q < dst.subset.size(); ++q)
+                    if (dst.lane_base(int(q)) == kp.s[i].aux.base) return int(q);
+                return -1;
+            }();
+            const int yp_src = src.pos_of(dst.subset[yp_dst]);
+            if (yp_src < 0) throw std::invalid_argument("fused operand missing from the source view");
+            p.s[s].op = kp.s[i].op;
+            p.s[s].aux = src.lanes(yp_src);
+            p.s[s].aux_q = dst.fmt[yp_dst];
+        }
+    }
+}
+
+void gather(const View& src, const void* sp, const View& dst, void* dp, const char* kernel, double dt, int math,
+            cudaStream_t st) {
+    require_device();
+    check_ptr(sp, "source buffer");
+    check_ptr(dp, "destination buffer");
+    if (src.layout == Layout::AoS && dst.layout == Layout::SoA) {
+        const GatherPlan g = kernel ? plan_gather_fused(src, dst, kernel, dt, math) : plan_gather(src, dst);
+        check_cuda(launch_gather(g, sp, src.total_bytes(), dp, st, 0), "gather launch");
+        count_launches(1);
+        return;
+    }
+    ConvertPlan p = plan_convert(src, dst, dst.subset);
+    if (kernel) fuse_ops(p, src, dst, kernel, dt, math);
+    check_cuda(launch_convert(p, sp, dp, st), "convert launch");
+    count_launches(1);
+}
+
+void convert(const View& src, const void* sp, const View& dst, void* dp, cudaStream_t st) {
+    gather(src, sp, dst, dp, nullptr, 0.0, 0, st);
+}
+
+void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, const std::string& kernel,
+                   cudaStream_t st) {
+    require_device();
+    check_ptr(sp, "source buffer");
+    check_ptr(dp, "destination buffer");
+    const KernelSet* ks = dst.schema->kernel(kernel);
+    if (!ks) throw std::invalid_argument("no access set declared for kernel '" + kernel + "'");
+    std::vector<int> fields;
+    for (const auto& w : ks->writes) {
+        const int f = dst.schema->index(w);
+        if (f < 0) throw std::invalid_argument("widen_merge: unknown write field '" + w + "'");
+        fields.push_back(f);
+    }
+    const ConvertPlan p = plan_convert(src, dst, fields);
+    check_cuda(launch_convert(p, sp, dp, st), "scatter launch");
+    count_launches(1);
+}
+
+void run_kernel(const View& v, void* p, const std::string& kernel, double dt, uint64_t bs, int per_access, int math,
+                cudaStream_t st) {
+    require_device();
+    check_ptr(p, "buffer");
+    if (kernel == "density") {
+        if (math != MATH_FP64_EXACT) throw std::invalid_argument("buffer-mode density is binary64 (reference semantics)");
+        const DensityPlan d = plan_density(v, bs, per_access);
+        check_cuda(launch_density_buffer(d, p, st), "density launch");
+        count_launches(1);
+        return;
+    }
+    if (bs == 0 || v.count % bs != 0) throw std::invalid_argument("buffer size must divide the particle count");
+    const KernelPlan kp = plan_kernel(v, kernel, dt, math);
+    check_cuda(launch_convert(kp, p, p, st), "kernel launch");
+    count_launches(1);
+}
+
+}  // namespace sfb

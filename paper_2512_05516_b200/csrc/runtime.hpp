@@ -1,0 +1,45 @@
+// Host runtime behind the C ABI: validates views, builds plans, launches the
+// sm_100a kernels on the caller's stream.  No CPU compute path exists: every
+// entry requires a CUDA device and throws otherwise.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "plans.cuh"
+#include "view.hpp"
+
+namespace sfb {
+
+// kernels.cu / density.cu launchers
+cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st);
+cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
+                          int ctas_per_sm);
+cudaError_t launch_density_buffer(const DensityPlan& p, void* buf, cudaStream_t st);
+
+void check_cuda(cudaError_t e, const char* what);
+void require_device();
+void count_launches(uint64_t n);
+uint64_t launch_count();
+
+void gather(const View& src, const void* sp, const View& dst, void* dp, const char* kernel, double dt, int math,
+            cudaStream_t st);
+void convert(const View& src, const void* sp, const View& dst, void* dp, cudaStream_t st);
+void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, const std::string& kernel,
+                   cudaStream_t st);
+void run_kernel(const View& v, void* p, const std::string& kernel, double dt, uint64_t bs, int per_access, int math,
+                cudaStream_t st);
+
+// density.cu
+void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* cell_start,
+                   int nx, int ny, int nz, int own_x0, int own_x1, float* rho, cudaStream_t st);
+uint64_t bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
+void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int nx, int ny, int nz,
+                   int32_t* cell_start, int32_t* perm, void* scratch, uint64_t scratch_bytes, cudaStream_t st);
+
+// host.cu
+void run_host(const View& src, void* host, const View& dst, const std::string& kernels, double dt, int math,
+              int mode, uint64_t chunk, void* host_soa, double* metrics);
+
+}  // namespace sfb

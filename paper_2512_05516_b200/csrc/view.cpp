@@ -1,0 +1,213 @@
+#include "view.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace sfb {
+
+int View::pos_of(int field) const {
+    for (size_t p = 0; p < subset.size(); ++p)
+        if (subset[p] == field) return int(p);
+    return -1;
+}
+
+int View::pos_of(const std::string& name) const { return pos_of(schema->index(name)); }
+
+uint64_t View::record_bits() const {
+    uint64_t b = 0;
+    for (size_t p = 0; p < subset.size(); ++p) b += uint64_t(arity(int(p))) * width(int(p));
+    return b;
+}
+
+uint64_t View::lane_base(int pos) const {
+    uint64_t b = 0;
+    for (int q = 0; q < pos; ++q) b += uint64_t(arity(q)) * width(q);
+    return layout == Layout::AoS ? b : b * count;
+}
+
+uint64_t View::lane_stride(int pos) const {
+    return layout == Layout::AoS ? record_bits() : uint64_t(arity(pos)) * width(pos);
+}
+
+bool View::byte_aligned() const {
+    for (size_t p = 0; p < subset.size(); ++p)
+        if ((lane_base(int(p)) | lane_stride(int(p)) | width(int(p))) & 7) return false;
+    return true;
+}
+
+Lanes View::lanes(int pos) const {
+    Lanes l;
+    l.base = lane_base(pos);
+    l.stride = lane_stride(pos);
+    l.fmt = fmt[pos];
+    l.arity = uint8_t(arity(pos));
+    return l;
+}
+
+static LaneFmt stored_fmt(const FieldDecl& f) {
+    return f.is_float() ? fmt_compressed(f.stored_width()) : fmt_int();
+}
+
+View make_view(std::shared_ptr<const Schema> s, const char* access_set, Layout layout,
+               int precision, const std::vector<std::string>& exclude, uint64_t count) {
+    View v;
+    v.schema = s;
+    v.count = count;
+    v.layout = layout;
+    const KernelSet* ks = nullptr;
+    if (access_set && *access_set) {
+        ks = s->kernel(access_set);
+        if (!ks) throw std::invalid_argument(std::string("no access set declared for kernel '") + access_set + "'");
+    }
+    // narrow_into: reads ∪ writes in declaration order (layout_ops.cpp:86-101)
+    for (size_t i = 0; i < s->fields.size(); ++i)
+        if (!ks || ks->touches(s->fields[i].name)) v.subset.push_back(int(i));
+    const bool ok_prec = precision == kPrecStored || precision == kPrecNative || precision == kPrecBF16 ||
+                         (precision >= 7 && precision <= 64) ||
+                         (precision >= kPrecPackedT + 7 && precision <= kPrecPackedT + 64);
+    if (!ok_prec) throw std::invalid_argument("unknown precision code " + std::to_string(precision));
+    for (int idx : v.subset) {
+        const FieldDecl& f = s->fields[idx];
+        const bool excluded = std::find(exclude.begin(), exclude.end(), f.name) != exclude.end();
+        LaneFmt fm = stored_fmt(f);
+        if (!f.is_float()) {
+            v.fmt.push_back(fm);
+            continue;
+        }
+        if (precision == kPrecNative) fm = fmt_native(f.stored_width());
+        else if (precision == kPrecBF16) fm = excluded ? fmt_native(f.stored_width()) : fmt_bf16();
+        else if (precision >= 7 && precision <= 64) fm = fmt_native(excluded ? f.stored_width() : precision);
+        else if (precision >= kPrecPackedT) fm = fmt_compressed(excluded ? f.stored_width() : precision - kPrecPackedT);
+        v.fmt.push_back(fm);
+    }
+    return v;
+}
+
+static void check_same_schema(const View& a, const View& b) {
+    if (a.schema->fields.size() != b.schema->fields.size())
+        throw std::invalid_argument("views over different schemas");
+    for (size_t i = 0; i < a.schema->fields.size(); ++i)
+        if (a.schema->fields[i].name != b.schema->fields[i].name ||
+            a.schema->fields[i].arity != b.schema->fields[i].arity ||
+            a.schema->fields[i].is_float() != b.schema->fields[i].is_float())
+            throw std::invalid_argument("views over different schemas");
+    if (a.count != b.count) throw std::invalid_argument("record count mismatch");
+}
+
+ConvertPlan plan_convert(const View& src, const View& dst, const std::vector<int>& fields) {
+    check_same_schema(src, dst);
+    if (fields.size() > size_t(kMaxStreams)) throw std::invalid_argument("too many fields for one plan");
+    ConvertPlan p;
+    p.count = src.count;
+    p.dst_byte_aligned = dst.byte_aligned();
+    for (int f : fields) {
+        const int sp = src.pos_of(f), dp = dst.pos_of(f);
+        if (sp < 0 || dp < 0)
+            throw std::invalid_argument("field '" + src.schema->fields[f].name + "' missing from a view subset");
+        CStream& c = p.s[p.n++];
+        c.src = src.lanes(sp);
+        c.dst = dst.lanes(dp);
+        c.op = OP_COPY;
+    }
+    return p;
+}
+
+GatherPlan plan_gather(const View& src, const View& dst) {
+    check_same_schema(src, dst);
+    if (src.layout != Layout::AoS || dst.layout != Layout::SoA)
+        throw std::invalid_argument("tiled gather maps an AoS view to an SoA view");
+    if (dst.subset.size() > size_t(kMaxStreams)) throw std::invalid_argument("too many streams");
+    GatherPlan g;
+    g.count = src.count;
+    g.record_bits = uint32_t(src.record_bits());
+    const uint64_t unit_bytes = 16ull * g.record_bits;  // bytes of 128 records
+    uint64_t k = std::max<uint64_t>(1, 16384 / unit_bytes);
+    g.tile_recs = uint32_t(128 * k);
+    g.tile_bytes = uint32_t(g.tile_recs * uint64_t(g.record_bits) / 8);
+    for (size_t dp = 0; dp < dst.subset.size(); ++dp) {
+        const int f = dst.subset[dp];
+        const int sp = src.pos_of(f);
+        if (sp < 0) throw std::invalid_argument("destination field missing from the source view");
+        const int w = dst.width(int(dp));
+        if (w != 16 && w != 32 && w != 64) throw std::invalid_argument("SoA gather needs 16/32/64-bit lanes");
+        GStream& s = g.s[g.n++];
+        s.src_off = uint32_t(src.lane_base(sp));
+        s.src = src.fmt[sp];
+        s.dst = dst.fmt[dp];
+        s.dst_base = dst.lane_base(int(dp)) / 8;
+        s.arity = uint8_t(dst.arity(int(dp)));
+        s.op = OP_COPY;
+    }
+    return g;
+}
+
+namespace {
+struct OpSpec { const char* field; const char* operand; uint8_t op; };
+const std::vector<OpSpec>& ops_for(const std::string& k) {
+    // sph.cpp:247-264 — kick: v += a dt, u = max(0, u + du dt); drift: x += v dt
+    static const std::vector<OpSpec> kick = {{"v", "a", OP_AXPY}, {"u", "du", OP_AXPY_CLAMP0}};
+    static const std::vector<OpSpec> drift = {{"x", "v", OP_AXPY}};
+    if (k == "kick") return kick;
+    if (k == "drift") return drift;
+    throw std::invalid_argument("kernel '" + k + "' is not a linear streaming kernel (kick|drift)");
+}
+}  // namespace
+
+KernelPlan plan_kernel(const View& v, const std::string& kernel, double dt, int math) {
+    KernelPlan p;
+    p.count = v.count;
+    p.dt = dt;
+    p.math = uint8_t(math);
+    p.dst_byte_aligned = v.byte_aligned();
+    for (const auto& o : ops_for(kernel)) {
+        const int xp = v.pos_of(o.field), yp = v.pos_of(o.operand);
+        if (xp < 0 || yp < 0)
+            throw std::invalid_argument(std::string("field '") + (xp < 0 ? o.field : o.operand) +
+                                        "' is not present in the buffer view");
+        CStream& c = p.s[p.n++];
+        c.src = c.dst = v.lanes(xp);
+        c.aux = v.lanes(yp);
+        c.aux_q = v.fmt[yp];
+        c.op = o.op;
+    }
+    return p;
+}
+
+GatherPlan plan_gather_fused(const View& src, const View& dst, const std::string& kernel, double dt,
+                             int math) {
+    GatherPlan g = plan_gather(src, dst);
+    g.dt = dt;
+    g.math = uint8_t(math);
+    for (const auto& o : ops_for(kernel)) {
+        const int xf = src.schema->index(o.field), yf = src.schema->index(o.operand);
+        const int xd = dst.pos_of(xf), yd = dst.pos_of(yf), ys = src.pos_of(yf);
+        if (xd < 0 || yd < 0 || ys < 0)
+            throw std::invalid_argument(std::string("fused ") + kernel + " needs fields '" + o.field + "' and '" +
+                                        o.operand + "' in both views");
+        GStream& s = g.s[xd];
+        s.op = o.op;
+        s.aux_off = uint32_t(src.lane_base(ys));
+        s.aux_src = src.fmt[ys];
+        s.aux_dst = dst.fmt[yd];
+    }
+    return g;
+}
+
+DensityPlan plan_density(const View& v, uint64_t bs, int per_access) {
+    DensityPlan p;
+    const int x = v.pos_of("x"), m = v.pos_of("m"), h = v.pos_of("h"), r = v.pos_of("rho");
+    if (x < 0 || m < 0 || h < 0 || r < 0)
+        throw std::invalid_argument("density needs fields x, m, h, rho in the buffer view");
+    if (bs == 0 || bs > 1024 || v.count % bs != 0)
+        throw std::invalid_argument("buffer size must divide the particle count (and be <= 1024)");
+    p.x = v.lanes(x);
+    p.m = v.lanes(m);
+    p.h = v.lanes(h);
+    p.rho = v.lanes(r);
+    p.count = v.count;
+    p.bs = uint32_t(bs);
+    p.per_access = uint8_t(per_access != 0);
+    return p;
+}
+
+}  // namespace sfb

@@ -1,0 +1,326 @@
+"""GPU parity: libsoaforge_b200.so (called through its C ABI) against the
+oracle and the reference's golden checksums.  Bit-exact for every layout /
+precision conversion and for fp64-exact kick/drift/density; stated
+tolerances for the fp32 math mode and the cell-linked density."""
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import apply_kernel, compressed_fmts, golden, native_fmts, schema_for
+
+from paper_2512_05516_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+G = golden("pipeline.json") if True else None
+
+
+def dev(ob: O.Buffer, view: api.View) -> api.PackedBuffer:
+    return api.PackedBuffer.from_host(view, ob.data)
+
+
+def host(pb: api.PackedBuffer) -> np.ndarray:
+    torch.cuda.synchronize()
+    return pb.to_host()
+
+
+def csum(pb: api.PackedBuffer) -> int:
+    return O.checksum(host(pb), pb.view.nbytes * 8 if pb.view.nbytes else 0)
+
+
+def csum_bits(pb: api.PackedBuffer, bits: int) -> int:
+    return O.checksum(host(pb), bits)
+
+
+def default_aos(n=None, seed=None, accel=43):
+    n = n or G["n"]
+    seed = seed or G["seed"]
+    S0 = O.default_schema()
+    ob = O.store_state(O.random_ics(n, seed, accel, G["dt"]), S0)
+    P = api.Schema.default()
+    return ob, P, dev(ob, api.View(P, n, "aos"))
+
+
+# ----------------------------------------------------------- golden pipelines
+@pytest.mark.parametrize("name", ["t16_xincl", "t16_xexcl", "t32_xincl"])
+def test_northstar_composition_goldens(name):
+    T, ex = {"t16_xincl": (16, ""), "t16_xexcl": (16, "x"), "t32_xincl": (32, "")}[name]
+    want = {k: int(v, 16) for k, v in G["northstar"][name].items()}
+    _, P, src = default_aos()
+    n = G["n"]
+    # store_state(T) on the device: default AoS -> T-bit AoS
+    aos_t = api.convert(src, api.View(P, n, "aos", None, api.SF_PREC_PACKED + T, ex))
+    assert csum(aos_t) == want["aos_t"]
+    full = api.gather(src, api.View(P, n, "soa", None, T, ex))
+    assert csum(full) == want["soa_full"]
+    for k in ["drift", "kick", "density"]:
+        v = api.View(P, n, "soa", k, T, ex)
+        soa = api.gather(src, v)
+        assert csum(soa) == want[f"{k}_soa"], k
+        api.run_kernel(soa, k, G["dt"])
+        assert csum(soa) == want[f"{k}_soa_after"], k
+        merged = api.convert(src, aos_t.view)
+        api.widen_merge(soa, merged, k)
+        assert csum(merged) == want[f"{k}_merged_t"], k
+        if k != "density":
+            fused = api.gather_kernel(src, v, k, G["dt"])
+            assert csum(fused) == want[f"{k}_soa_after"], k
+
+
+def test_survey_golden_c2_path():
+    """drift-set SoA 0635880f517e24e8, after drift 6fab44d025d6f18c,
+    default AoS after exact x scatter-back b95ebdfd606469ca."""
+    _, P, src = default_aos(accel=0)
+    v = api.View(P, 4096, "soa", "drift", 16)
+    assert csum(api.gather(src, v)) == 0x0635880f517e24e8
+    fused = api.gather_kernel(src, v, "drift", 1e-3)
+    assert csum(fused) == 0x6fab44d025d6f18c
+    api.widen_merge(fused, src, "drift")
+    assert csum(src) == 0xb95ebdfd606469ca
+
+
+SWEEPS = {"default": (0, "", 43), "t16_xexcl": (16, "x", 43), "t16_xincl": (16, "", 43),
+          "t64_xexcl": (64, "x", 43), "t32_xexcl": (32, "x", 43), "default_ics": (0, "", 0)}
+
+
+@pytest.mark.parametrize("name", list(SWEEPS))
+def test_kernel_sweep_goldens(name):
+    """bench kernels composition (bench.cpp:269-316) on AoS and SoA, in place."""
+    T, ex, acc = SWEEPS[name]
+    want = {k: int(v, 16) for k, v in G["sweeps"][name].items()}
+    S = schema_for(T, ex)
+    P = api.Schema(S.text())
+    n = G["n"]
+    ob = O.store_state(O.random_ics(n, G["seed"], acc, G["dt"]), S)
+    aos = dev(ob, api.View(P, n, "aos"))
+    assert csum(aos) == want["aos"]
+    nat = api.convert(aos, api.View(P, n, "aos", None, api.SF_PREC_NATIVE))
+    soa = api.gather(aos, api.View(P, n, "soa", None, api.SF_PREC_NATIVE))
+    assert csum(soa) == want["soa_full"]
+    packed_view = api.View(P, n, "aos")
+    for k in ["drift", "kick", "density"]:
+        for layout, buf in [("aos", nat), ("soa", soa)]:
+            work = api.PackedBuffer(buf.view, buf.data.clone())
+            api.run_kernel(work, k, G["dt"])
+            assert csum(api.convert(work, packed_view)) == want[f"{k}_{layout}"], (k, layout)
+    work = api.PackedBuffer(nat.view, nat.data.clone())
+    api.run_kernel(work, "density", G["dt"], per_access=True)
+    assert csum(api.convert(work, packed_view)) == want["density_aos_peraccess"]
+
+
+# ----------------------------------------------------------- codec coverage
+def random_bits_schema():
+    return O.Schema("bits", [O.Field("p", "f64", 3), O.Field("q", "f32", 3), O.Field("k", "i64"),
+                             O.Field("r", "f32")], {"all": (["p", "q", "k", "r"], [])})
+
+
+@pytest.mark.parametrize("prec", [16, api.SF_PREC_BF16, 12, 20, 24, 33, 40, 64])
+def test_random_bit_patterns_bit_exact(prec):
+    """10^6 random lanes incl. NaN payloads, +-inf, subnormals, huge values."""
+    S = random_bits_schema()
+    n = 1 << 17  # 8 float lanes per record -> ~1.05 M lanes
+    rng = np.random.default_rng(prec)
+    ob = O._alloc(S, n, "aos", range(4), [f.fmt() for f in S.fields])
+    ob.data[:] = rng.integers(0, 256, size=ob.data.size, dtype=np.uint8)
+    # salt with special values
+    specials64 = np.array([0x7ff8000000000000, 0xfff0000000000001, 0x7ff0000000000000, 1, 0x8000000000000001,
+                           0x000fffffffffffff, 0x3f10000000000000, 0x40f0000000000000, 0x47f0000000000000],
+                          dtype=np.uint64)
+    p_bits = ob.field_bits("p")
+    p_bits[: specials64.size * 100] = np.tile(specials64, 100)
+    from helpers import set_field  # noqa: F401
+    O._write_field_bits(ob, 0, p_bits)
+    P = api.Schema(S.text())
+    src = dev(ob, api.View(P, n, "aos"))
+    fmt_of = (lambda f: O.OR_BF16) if prec == api.SF_PREC_BF16 else (lambda f: O.NATIVE(prec))
+    fmts = [fmt_of(f) if f.is_float else O.OR_I64 for f in S.fields]
+    want = O.transform(ob, "soa", fmts=fmts)
+    got = api.gather(src, api.View(P, n, "soa", None, prec))
+    np.testing.assert_array_equal(host(got), want.data)
+    # generic (non-tiled) kernel, AoS -> AoS
+    want_aos = O.transform(ob, "aos", fmts=fmts)
+    got_aos = api.convert(src, api.View(P, n, "aos", None, prec))
+    np.testing.assert_array_equal(host(got_aos), want_aos.data)
+
+
+def test_bit_packed_truncated_schema():
+    """Non-byte-aligned @truncate widths: tiled gather from a bit-packed AoS
+    and scatter-merge back into it (bit-level atomics path)."""
+    S = O.Schema("tp", [O.Field("x", "f64", 3, 40), O.Field("id", "i64"), O.Field("v", "f32", 3, 20),
+                        O.Field("u", "f32", 1, 12), O.Field("m", "f32", 1, 17)],
+                 {"drift": (["x", "v"], ["x"]), "kick2": (["u", "m"], ["u"])})
+    n = 3001
+    ics = O.random_ics(n, 5, 7)
+    ob = O.store_state(ics, S)
+    P = api.Schema(S.text())
+    assert P.record_bits == S.record_bits == 3 * 40 + 64 + 60 + 12 + 17
+    src = dev(ob, api.View(P, n, "aos"))
+    for access in [None, "drift"]:
+        want = O.transform(ob, "soa", subset=S.subset(access), fmts=[S.fields[i].fmt(True) for i in S.subset(access)])
+        got = api.gather(src, api.View(P, n, "soa", access, api.SF_PREC_NATIVE))
+        np.testing.assert_array_equal(host(got), want.data)
+    soa = api.gather(src, api.View(P, n, "soa", "drift", api.SF_PREC_NATIVE))
+    api.run_kernel(soa, "drift", 1e-3, buffer_size=1)
+    ref_soa = apply_kernel(O.transform(ob, "soa", subset=S.subset("drift"),
+                                       fmts=[S.fields[i].fmt(True) for i in S.subset("drift")]), "drift")
+    np.testing.assert_array_equal(host(soa), ref_soa.data)
+    api.widen_merge(soa, src, "drift")
+    merged = copy.deepcopy(ob)
+    O.merge_into(ref_soa, merged, ["x"])
+    np.testing.assert_array_equal(host(src), merged.data)
+
+
+@pytest.mark.parametrize("n", [1, 7, 127, 128, 129, 1000, 4101, 20000])
+def test_ragged_counts(n):
+    """Partial tiles, sub-16-byte tails, single records."""
+    ob, P, src = default_aos(n=n)
+    S16 = schema_for(16)
+    st = O.transform(ob, "aos", fmts=compressed_fmts(S16), schema=S16)
+    want = O.transform(st, "soa", subset=S16.subset("drift"))
+    v = api.View(P, n, "soa", "drift", 16)
+    np.testing.assert_array_equal(host(api.gather(src, v)), want.data)
+    after = apply_kernel(want, "drift")
+    fused = api.gather_kernel(src, v, "drift", 1e-3)
+    np.testing.assert_array_equal(host(fused), after.data)
+    api.widen_merge(fused, src, "drift")
+    O.merge_into(after, ob, ["x"])
+    np.testing.assert_array_equal(host(src), ob.data)
+
+
+def test_zero_records():
+    P = api.Schema.default()
+    src = api.PackedBuffer.empty(api.View(P, 0, "aos"))
+    out = api.gather(src, api.View(P, 0, "soa", "drift", 16))
+    api.run_kernel(out, "drift", 1e-3, buffer_size=1)
+    torch.cuda.synchronize()
+
+
+def test_kick_fused_and_bf16():
+    ob, P, src = default_aos(n=8192)
+    for prec, fmt in [(api.SF_PREC_BF16, O.OR_BF16), (16, O.NATIVE(16)), (32, O.NATIVE(32))]:
+        S = O.default_schema()
+        sub = S.subset("kick")
+        ref = apply_kernel(O.transform(ob, "soa", subset=sub, fmts=[fmt] * len(sub)), "kick")
+        got = api.gather_kernel(src, api.View(P, 8192, "soa", "kick", prec), "kick", 1e-3)
+        np.testing.assert_array_equal(host(got), ref.data)
+
+
+def test_fp32_math_within_one_storage_ulp():
+    ob, P, src = default_aos(n=1 << 16)
+    v = api.View(P, 1 << 16, "soa", "drift", 16)
+    exact = api.gather_kernel(src, v, "drift", 1e-3, api.SF_MATH_FP64_EXACT)
+    fast = api.gather_kernel(src, v, "drift", 1e-3, api.SF_MATH_FP32)
+    a = host(exact)[: v.nbytes].view(np.float16).astype(np.float64)
+    b = host(fast)[: v.nbytes].view(np.float16).astype(np.float64)
+    assert np.all(np.abs(a - b) <= np.abs(a) * 2.0 ** -10 + 2.0 ** -24)
+
+
+# ----------------------------------------------------------- full-size properties
+def test_c2_full_size_roundtrip_properties():
+    """16M particles (BASELINE configs[1]): size-independent properties."""
+    n = 1 << 24
+    P = api.Schema.default()
+    aos_v = api.View(P, n, "aos")
+    g = torch.Generator(device="cuda").manual_seed(1)
+    src = api.PackedBuffer.empty(aos_v)
+    # synthetic f64/f32 records: random finite values in [-4, 4)
+    f = torch.rand(n, 22, device="cuda", generator=g, dtype=torch.float32) * 8 - 4
+    rec = src.data[: aos_v.nbytes].view(n, 88)
+    rec[:, 0:24] = f[:, 0:3].double().contiguous().view(torch.uint8).view(n, 24)
+    rec[:, 24:32] = torch.arange(n, device="cuda", dtype=torch.int64).view(torch.uint8).view(n, 8)
+    rec[:, 32:88] = f[:, 3:17].contiguous().view(torch.uint8).view(n, 56)
+    orig = src.data.clone()
+    # lossless U∘N∘C then C^T: identity on the full record
+    soa = api.gather(src, api.View(P, n, "soa", None, api.SF_PREC_NATIVE))
+    back = api.convert(soa, aos_v)
+    assert torch.equal(back.data[: aos_v.nbytes], orig[: aos_v.nbytes])
+    # narrowing is idempotent: gather(T16) == gather(T16 of the T16 AoS)
+    v16 = api.View(P, n, "soa", "drift", 16)
+    s1 = api.gather(src, v16)
+    aos16 = api.convert(src, api.View(P, n, "aos", None, 1016))
+    s2 = api.gather(aos16, v16)
+    assert torch.equal(s1.data, s2.data)
+    # fused drift == gather then drift
+    fused = api.gather_kernel(src, v16, "drift", 1e-3)
+    api.run_kernel(s1, "drift", 1e-3, buffer_size=1)
+    assert torch.equal(fused.data, s1.data)
+    # scatter-back of x only: every other byte of the record is untouched
+    api.widen_merge(fused, src, "drift")
+    recs = src.data[: aos_v.nbytes].view(n, 88)
+    o = orig[: aos_v.nbytes].view(n, 88)
+    assert torch.equal(recs[:, 24:], o[:, 24:])
+    x16 = fused.data[: n * 6].view(torch.float16).view(n, 3)
+    assert torch.equal(recs[:, :24].contiguous().view(torch.float64).view(n, 3), x16.double())
+
+
+# ----------------------------------------------------------- cell density
+@pytest.mark.parametrize("prec", [api.SF_PREC_NATIVE, 16, api.SF_PREC_BF16])
+def test_density_cells_vs_oracle(prec):
+    n = 1 << 15
+    rng = np.random.default_rng(3)
+    x = rng.random((n, 3))
+    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3))
+    m = np.full(n, 1.0 / n)
+    dt = {api.SF_PREC_NATIVE: torch.float32, 16: torch.float16, api.SF_PREC_BF16: torch.bfloat16}[prec]
+    xt = torch.tensor(x, device="cuda").to(dt)
+    mt = torch.tensor(m, device="cuda").to(dt)
+    ht = torch.tensor(h, device="cuda").to(dt)
+    cell = float(2 * ht.float().max())
+    nc = int(np.floor(1.0 / cell))
+    cell = 1.0 / nc
+    cs, perm = api.bin_particles(xt.float().contiguous(), (0, 0, 0), cell, (nc, nc, nc))
+    p = perm.long()
+    rho_sorted = api.density_cells(xt[p].contiguous(), mt[p].contiguous(), ht[p].contiguous(), cs,
+                                   (nc, nc, nc), prec=prec)
+    rho = torch.empty_like(rho_sorted)
+    rho[p] = rho_sorted
+    # oracle on exactly the stored (decoded) inputs, binary64
+    xd, md, hd = (t.double().cpu().numpy() for t in (xt, mt, ht))
+    want = O.density_cells(xd.reshape(-1), md, hd, 0.0, 1.0, cell)
+    got = rho.double().cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+    # binning is a stable counting sort
+    cs_h, perm_h = cs.cpu().numpy(), perm.cpu().numpy()
+    assert cs_h[-1] == n and np.all(np.diff(cs_h) >= 0)
+    assert sorted(perm_h.tolist()) == list(range(n))
+
+
+def test_density_buffer_fp64_matches_oracle_random():
+    """Reference-semantics density on random h and masses (exact)."""
+    n = 64 * 50
+    rng = np.random.default_rng(11)
+    ics = O.random_ics(n, 9)
+    ics["h"] = rng.uniform(0.05, 0.6, n)
+    ics["m"] = rng.uniform(0.1, 2.0, n)
+    S = schema_for(64)
+    ob = O.store_state(ics, S)
+    P = api.Schema(S.text())
+    buf = dev(ob, api.View(P, n, "aos"))
+    api.run_kernel(buf, "density", 1e-3, 64)
+    ref = apply_kernel(ob, "density")
+    np.testing.assert_array_equal(host(buf), ref.data)
+
+
+# ----------------------------------------------------------- host orchestration
+@pytest.mark.parametrize("mode", [0, 1])
+def test_run_host_streamed_and_managed(mode):
+    n = 100000
+    ob, P, _ = default_aos(n=n)
+    aos_v = api.View(P, n, "aos")
+    hb = api.HostBuffer(aos_v.nbytes, mode)
+    hb.numpy()[:] = ob.data
+    dst = api.View(P, n, "soa", "kick", 16)
+    dst_all = api.View(P, n, "soa", None, 16)
+    m = api.run_host(aos_v, hb, dst_all, "kick,drift", 1e-3, chunk=16384)
+    assert m["h2d_bytes"] == aos_v.nbytes and m["d2h_bytes"] == aos_v.nbytes
+    # oracle: T16 SoA of everything, kick then drift, merge v,u,x back (exact widen)
+    S = O.default_schema()
+    soa = O.transform(ob, "soa", fmts=[O.NATIVE(16) if f.is_float else O.OR_I64 for f in S.fields])
+    soa = apply_kernel(apply_kernel(soa, "kick"), "drift")
+    O.merge_into(soa, ob, ["v", "u", "x"])
+    np.testing.assert_array_equal(hb.numpy(), ob.data)
+    del dst
+    hb.free()
