@@ -98,6 +98,22 @@ __device__ __forceinline__ void st_bits_global(uint8_t* base, uint64_t bitoff, i
 // ----------------------------------------------------------------- lane ops
 __device__ __forceinline__ double dec(uint64_t b, LaneFmt f) { return decode_lane(b, f); }
 
+// The reference computes x + y*dt with x86-64 SSE2 (mulsd, addsd).  NaN
+// results follow that hardware: a NaN operand propagates quieted (x first,
+// then y), and an invalid operation (inf - inf) yields the x86 default NaN
+// 0xFFF8000000000000.  The GPU's DMUL/DADD return a canonical NaN instead,
+// so NaN outcomes are rebuilt explicitly; every other result is the same
+// IEEE RNE value on both.
+constexpr uint64_t kX86DefaultNaN = 0xFFF8000000000000ull;
+
+__device__ __forceinline__ double axpy_f64_exact(double x, double y, double dt) {
+    const double r = __dadd_rn(x, __dmul_rn(y, dt));
+    if (!isnan(r)) return r;
+    if (isnan(x)) return bits_to_f64(f64_to_bits(x) | (1ull << 51));
+    if (isnan(y)) return bits_to_f64(f64_to_bits(y) | (1ull << 51));
+    return bits_to_f64(kX86DefaultNaN);
+}
+
 // dst = Q(Q(x) + Q(y)*dt) [clamp >= 0]; x already in format fx (the output's),
 // y already in format fy.  Exact mode: binary64 with separately rounded
 // multiply and add (no FMA), exactly BufferView get/set arithmetic.
@@ -105,7 +121,7 @@ __device__ __forceinline__ uint64_t axpy_lane(uint64_t xb, LaneFmt fx, uint64_t 
                                               double dt, uint8_t op, uint8_t math) {
     double r;
     if (math == MATH_FP64_EXACT) {
-        r = __dadd_rn(dec(xb, fx), __dmul_rn(dec(yb, fy), dt));
+        r = axpy_f64_exact(dec(xb, fx), dec(yb, fy), dt);
     } else {
         const float rf = __fadd_rn(float(dec(xb, fx)), __fmul_rn(float(dec(yb, fy)), float(dt)));
         r = double(rf);
@@ -171,6 +187,154 @@ constexpr int kStages = 4;
 constexpr int kGatherThreads = 256;
 constexpr int kChunk = 8;  // SoA elements per work item (16 B of fp16 output)
 
+// ----------------------------------------------------------------- IEEE fast paths
+// Compile-time specialised conversions between plain IEEE lanes: one
+// hardware cvt.rn (F2F / F2FP) plus a NaN select, no runtime format logic.
+template <int B> struct Ieee;
+template <> struct Ieee<B_F64> {
+    static constexpr int m = 52, w = 64;
+    __device__ static bool nan(uint64_t b) { return (b & 0x7fffffffffffffffull) > 0x7ff0000000000000ull; }
+    __device__ static double f64(uint64_t b) { return bits_to_f64(b); }
+    __device__ static uint64_t from(double d) { return f64_to_bits(d); }
+};
+template <> struct Ieee<B_F32> {
+    static constexpr int m = 23, w = 32;
+    __device__ static bool nan(uint64_t b) { return (uint32_t(b) & 0x7fffffffu) > 0x7f800000u; }
+    __device__ static double f64(uint64_t b) { return double(bits_to_f32(uint32_t(b))); }
+    __device__ static uint64_t from(double d) { return f32_to_bits(__double2float_rn(d)); }
+};
+template <> struct Ieee<B_F16> {
+    static constexpr int m = 10, w = 16;
+    __device__ static bool nan(uint64_t b) { return (uint32_t(b) & 0x7fffu) > 0x7c00u; }
+    __device__ static double f64(uint64_t b) {
+        double d;
+        asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(uint16_t(b)));
+        return d;
+    }
+    __device__ static uint64_t from(double d) {
+        uint16_t h;
+        asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(d));
+        return h;
+    }
+};
+template <> struct Ieee<B_BF16> {
+    static constexpr int m = 7, w = 16;
+    __device__ static bool nan(uint64_t b) { return (uint32_t(b) & 0x7fffu) > 0x7f80u; }
+    __device__ static double f64(uint64_t b) { return double(bits_to_f32(uint32_t(b) << 16)); }
+    __device__ static uint64_t from(double d) {
+        uint16_t h;
+        asm("cvt.rn.bf16.f64 %0, %1;" : "=h"(h) : "d"(d));
+        return h;
+    }
+};
+
+// NaN payload rule of decode_bits∘encode_bits: keep the top mantissa bits,
+// never let a NaN collapse to infinity (fpcodec.cpp:49-56).
+template <int SB, int DB>
+__device__ __forceinline__ uint64_t nan_conv(uint64_t s) {
+    constexpr int ms = Ieee<SB>::m, md = Ieee<DB>::m, ws = Ieee<SB>::w, wd = Ieee<DB>::w;
+    const uint64_t sign = (s >> (ws - 1)) & 1;
+    const uint64_t man = s & ((1ull << ms) - 1);
+    uint64_t pay = md <= ms ? (man >> (ms - md)) : (man << (md - ms));
+    if (!pay) pay = 1ull << (md - 1);
+    return (sign << (wd - 1)) | (((1ull << (wd - 1 - md)) - 1) << md) | pay;
+}
+
+template <int SB, int DB>
+__device__ __forceinline__ uint64_t cvt_ieee(uint64_t s) {
+    if constexpr (SB == DB) {
+        return s;
+    } else {
+        uint64_t r;
+        if constexpr (SB == B_F32 && DB == B_F16) {
+            const __half h = __float2half_rn(bits_to_f32(uint32_t(s)));
+            r = *reinterpret_cast<const uint16_t*>(&h);
+        } else if constexpr (SB == B_F32 && DB == B_BF16) {
+            const __nv_bfloat16 h = __float2bfloat16_rn(bits_to_f32(uint32_t(s)));
+            r = *reinterpret_cast<const uint16_t*>(&h);
+        } else {
+            r = Ieee<DB>::from(Ieee<SB>::f64(s));
+        }
+        return Ieee<SB>::nan(s) ? nan_conv<SB, DB>(s) : r;
+    }
+}
+
+template <int B>
+__device__ __forceinline__ uint64_t lds(const uint8_t* p) {
+    if constexpr (Ieee<B>::w == 64) return *reinterpret_cast<const uint64_t*>(p);
+    else if constexpr (Ieee<B>::w == 32) return *reinterpret_cast<const uint32_t*>(p);
+    else return *reinterpret_cast<const uint16_t*>(p);
+}
+
+// x + y*dt in the destination format DB (both operands already quantized to DB).
+template <int DB>
+__device__ __forceinline__ uint64_t axpy_ieee(uint64_t xq, uint64_t yq, double dt, uint8_t op, uint8_t math) {
+    double r;
+    if (math == MATH_FP64_EXACT) {
+        // NaN operands propagate quieted, x first (see axpy_f64_exact); done in
+        // DB space because the hardware widening of a NaN is canonical.
+        constexpr int wd = Ieee<DB>::w, md = Ieee<DB>::m;
+        constexpr uint64_t qbit = 1ull << (md - 1);
+        if (Ieee<DB>::nan(xq)) return xq | qbit;
+        if (Ieee<DB>::nan(yq)) return yq | qbit;
+        r = __dadd_rn(Ieee<DB>::f64(xq), __dmul_rn(Ieee<DB>::f64(yq), dt));
+        if (isnan(r))  // inf - inf: x86 default NaN 0xFFF8... encoded
+            return (1ull << (wd - 1)) | (((1ull << (wd - 1 - md)) - 1) << md) | qbit;
+    } else {
+        r = double(__fadd_rn(float(Ieee<DB>::f64(xq)), __fmul_rn(float(Ieee<DB>::f64(yq)), float(dt))));
+    }
+    if (op == OP_AXPY_CLAMP0 && r < 0.0) r = 0.0;
+    return Ieee<DB>::from(r);
+}
+
+// One work item of the fast path: kChunk consecutive SoA elements of a stream.
+template <int SB, int DB, int AB>
+__device__ __forceinline__ void chunk_fast(const uint8_t* tile, uint32_t rbytes, const GStream& g, uint32_t e0,
+                                           uint32_t nel, double dt, uint8_t math, uint64_t (&out)[kChunk]) {
+    const uint32_t ar = g.arity;
+    const uint8_t* xs = tile + (g.src_off >> 3);
+    const uint8_t* ys = tile + (g.aux_off >> 3);
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+        const uint32_t e = min(e0 + j, nel - 1);
+        const uint32_t r = ar == 1 ? e : e / 3;
+        const uint32_t l = e - r * ar;
+        uint64_t v = cvt_ieee<SB, DB>(lds<SB>(xs + r * rbytes + l * (Ieee<SB>::w / 8)));
+        if constexpr (AB >= 0) {
+            const uint64_t y = cvt_ieee<AB, DB>(lds<AB>(ys + r * rbytes + l * (Ieee<AB>::w / 8)));
+            v = axpy_ieee<DB>(v, y, dt, g.op, math);
+        }
+        out[j] = v;
+    }
+}
+
+// fast code = 1 + sb*12 + db*3 + ab (view.cpp fast_kind)
+__device__ __forceinline__ bool dispatch_fast(const uint8_t* tile, uint32_t rbytes, const GStream& g, uint32_t e0,
+                                              uint32_t nel, double dt, uint8_t math, uint64_t (&out)[kChunk]) {
+    switch (g.fast) {
+#define SFB_CASE(SBI, SB, DBI, DB, ABI, AB)                                              \
+    case 1 + SBI * 12 + DBI * 3 + ABI:                                                   \
+        chunk_fast<SB, DB, AB>(tile, rbytes, g, e0, nel, dt, math, out);                 \
+        return true;
+#define SFB_DST(SBI, SB, DBI, DB)       \
+    SFB_CASE(SBI, SB, DBI, DB, 0, -1)   \
+    SFB_CASE(SBI, SB, DBI, DB, 1, B_F64) \
+    SFB_CASE(SBI, SB, DBI, DB, 2, B_F32)
+#define SFB_SRC(SBI, SB)                 \
+    SFB_DST(SBI, SB, 0, B_F16)           \
+    SFB_DST(SBI, SB, 1, B_BF16)          \
+    SFB_DST(SBI, SB, 2, B_F32)           \
+    SFB_DST(SBI, SB, 3, B_F64)
+        SFB_SRC(0, B_F64)
+        SFB_SRC(1, B_F32)
+#undef SFB_SRC
+#undef SFB_DST
+#undef SFB_CASE
+        default:
+            return false;
+    }
+}
+
 // ----------------------------------------------------------------- k_gather_tiled
 __global__ void __launch_bounds__(kGatherThreads) k_gather_tiled(const __grid_constant__ GatherPlan P,
                                                                  const uint8_t* __restrict__ src,
@@ -232,6 +396,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_tiled(const __grid_co
             const uint32_t e0 = c * kChunk;
             const int sw = g.src.width, aw = g.aux_src.width, dw = g.dst.width;
             uint64_t out[kChunk];
+            if (!(g.fast && dispatch_fast(tile, P.record_bits >> 3, g, e0, nel, P.dt, P.math, out)))
 #pragma unroll
             for (int j = 0; j < kChunk; ++j) {
                 const uint32_t e = min(e0 + j, nel - 1);

@@ -54,6 +54,9 @@ struct GStream {
     uint64_t dst_base = 0;  // byte offset of the destination SoA stream
     LaneFmt src{}, dst{}, aux_src{}, aux_dst{};
     uint8_t arity = 1, op = OP_COPY;
+    // compile-time-specialised IEEE path (kernels.cu gather_fast_kind);
+    // 0 = generic bit-level path
+    uint8_t fast = 0;
 };
 
 struct GatherPlan {

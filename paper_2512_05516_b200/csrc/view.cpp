@@ -112,6 +112,31 @@ ConvertPlan plan_convert(const View& src, const View& dst, const std::vector<int
     return p;
 }
 
+// Fast-path code of one gather stream: 1 + sb*12 + db*3 + ab, where
+// sb in {f64, f32}, db in {f16, bf16, f32, f64}, ab in {none, f64, f32};
+// 0 selects the generic path (truncated/bit-packed lanes, ints, odd shapes).
+static uint8_t fast_kind(const GStream& s, uint32_t record_bits) {
+    auto ieee = [](LaneFmt f) { return fmt_is_ieee(f); };
+    auto src_idx = [](LaneFmt f) { return f.base == B_F64 ? 0 : f.base == B_F32 ? 1 : -1; };
+    auto dst_idx = [](LaneFmt f) {
+        return f.base == B_F16 ? 0 : f.base == B_BF16 ? 1 : f.base == B_F32 ? 2 : f.base == B_F64 ? 3 : -1;
+    };
+    auto aligned = [&](uint32_t off, LaneFmt f) { return off % f.width == 0 && record_bits % f.width == 0; };
+    if (!ieee(s.src) || !ieee(s.dst) || src_idx(s.src) < 0 || dst_idx(s.dst) < 0) return 0;
+    if (!aligned(s.src_off, s.src)) return 0;
+    int ab = 0;
+    if (s.op != OP_COPY) {
+        if (!ieee(s.aux_src) || src_idx(s.aux_src) < 0 || !fmt_eq(s.aux_dst, s.dst) || !aligned(s.aux_off, s.aux_src))
+            return 0;
+        ab = 1 + src_idx(s.aux_src);
+    }
+    return uint8_t(1 + src_idx(s.src) * 12 + dst_idx(s.dst) * 3 + ab);
+}
+
+static void finalize_fast(GatherPlan& g) {
+    for (uint32_t i = 0; i < g.n; ++i) g.s[i].fast = fast_kind(g.s[i], g.record_bits);
+}
+
 GatherPlan plan_gather(const View& src, const View& dst) {
     check_same_schema(src, dst);
     if (src.layout != Layout::AoS || dst.layout != Layout::SoA)
@@ -121,7 +146,7 @@ GatherPlan plan_gather(const View& src, const View& dst) {
     g.count = src.count;
     g.record_bits = uint32_t(src.record_bits());
     const uint64_t unit_bytes = 16ull * g.record_bits;  // bytes of 128 records
-    uint64_t k = std::max<uint64_t>(1, 16384 / unit_bytes);
+    uint64_t k = std::max<uint64_t>(1, (24576 + unit_bytes / 2) / unit_bytes);
     g.tile_recs = uint32_t(128 * k);
     g.tile_bytes = uint32_t(g.tile_recs * uint64_t(g.record_bits) / 8);
     for (size_t dp = 0; dp < dst.subset.size(); ++dp) {
@@ -138,6 +163,7 @@ GatherPlan plan_gather(const View& src, const View& dst) {
         s.arity = uint8_t(dst.arity(int(dp)));
         s.op = OP_COPY;
     }
+    finalize_fast(g);
     return g;
 }
 
@@ -190,6 +216,7 @@ GatherPlan plan_gather_fused(const View& src, const View& dst, const std::string
         s.aux_src = src.fmt[ys];
         s.aux_dst = dst.fmt[yd];
     }
+    finalize_fast(g);
     return g;
 }
 

@@ -324,3 +324,41 @@ def test_run_host_streamed_and_managed(mode):
     np.testing.assert_array_equal(hb.numpy(), ob.data)
     del dst
     hb.free()
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("prec", [16, 32])
+def test_nan_inf_drift_matches_live_reference(prec):
+    """NaN / inf / overflow lanes through store_state(T) -> drift: the GPU
+    reproduces the reference's x86 NaN propagation bit for bit."""
+    n = 4096
+    ob, P, src = default_aos(n=n)
+    rec = ob.data.reshape(n, 88)
+    rng = np.random.default_rng(5)
+    specials64 = np.array([np.nan, -np.nan, np.inf, -np.inf, 1e300, -1e300, 5e-324, 0.0, -0.0])
+    nanpay = np.array([0x7ff0000000000001, 0xfff4000000000000, 0x7ff8000000000123], dtype=np.uint64)
+    for k in range(0, n, 7):
+        lane = int(rng.integers(0, 3))
+        v = specials64[k % specials64.size]
+        rec[k, 8 * lane: 8 * lane + 8] = np.array([v]).view(np.uint8)
+        if k % 3 == 0:
+            rec[k, 0:8] = nanpay[k % 3:k % 3 + 1].view(np.uint8)
+        vl = np.float32([np.nan, np.inf, -np.inf, 3e38][k % 4])
+        rec[k, 32 + 4 * lane: 36 + 4 * lane] = np.array([vl]).view(np.uint8)
+    src = dev(ob, api.View(P, n, "aos"))
+    R = O.RefLib()
+    h = R.L.ref_buf_from_bytes(None, 0, b"", n, O._p(ob.data), ob.data.size)
+    assert h
+    st = R.restore(h, prec)
+    u = R.op(st, "unpack")
+    nw = R.op(u, "narrow", "drift")
+    so = R.op(nw, "aos_to_soa")
+    R.run_kernel(so, "drift", 64, 1e-3)
+    want = R.bytes(so)
+    got = api.gather_kernel(src, api.View(P, n, "soa", "drift", prec), "drift", 1e-3)
+    np.testing.assert_array_equal(host(got), want)
+    # generic (non-tiled) path: run_kernel in place on the gathered SoA
+    soa = api.gather(src, api.View(P, n, "soa", "drift", prec))
+    api.run_kernel(soa, "drift", 1e-3, 64)
+    np.testing.assert_array_equal(host(soa), want)
+    R.free(h, st, u, nw, so)
