@@ -1,8 +1,8 @@
 // sm_100a kernels for the AoS<->SoA + reduced-precision SPH hot path.
 //
-//   k_gather_tiled   AoS -> SoA (U∘N∘C plus narrowing), optionally fused with
-//                    kick/drift.  Persistent CTAs; record tiles staged into
-//                    shared memory by 1-D TMA bulk copies (cp.async.bulk,
+//   k_gather_warp    AoS -> SoA (U∘N∘C plus narrowing), optionally fused with
+//                    kick/drift.  Persistent warps; record tiles staged into
+//                    shared memory by per-warp 1-D TMA bulk copies (cp.async.bulk,
 //                    UBLKCP) through an mbarrier ring; lanes extracted with
 //                    funnel shifts (any bit offset/width); 16-B SoA stores.
 //   k_convert        generic lane-by-lane conversion between any two views
@@ -98,9 +98,10 @@ __device__ __forceinline__ void st_bits_global(uint8_t* base, uint64_t bitoff, i
 // ----------------------------------------------------------------- lane ops
 __device__ __forceinline__ double dec(uint64_t b, LaneFmt f) { return decode_lane(b, f); }
 
-// The reference computes x + y*dt with x86-64 SSE2 (mulsd, addsd).  NaN
-// results follow that hardware: a NaN operand propagates quieted (x first,
-// then y), and an invalid operation (inf - inf) yields the x86 default NaN
+// The reference computes x + y*dt with x86-64 SSE2: g++ -O2 emits
+// t = y*dt (mulsd) then t = t + x (addsd), so a NaN operand propagates
+// quieted with y taking precedence over x (verified against the reference
+// build, tests/test_gpu_parity.py), and an invalid operation (inf - inf) yields the x86 default NaN
 // 0xFFF8000000000000.  The GPU's DMUL/DADD return a canonical NaN instead,
 // so NaN outcomes are rebuilt explicitly; every other result is the same
 // IEEE RNE value on both.
@@ -109,8 +110,8 @@ constexpr uint64_t kX86DefaultNaN = 0xFFF8000000000000ull;
 __device__ __forceinline__ double axpy_f64_exact(double x, double y, double dt) {
     const double r = __dadd_rn(x, __dmul_rn(y, dt));
     if (!isnan(r)) return r;
-    if (isnan(x)) return bits_to_f64(f64_to_bits(x) | (1ull << 51));
     if (isnan(y)) return bits_to_f64(f64_to_bits(y) | (1ull << 51));
+    if (isnan(x)) return bits_to_f64(f64_to_bits(x) | (1ull << 51));
     return bits_to_f64(kX86DefaultNaN);
 }
 
@@ -183,9 +184,6 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src, ui
         : "memory");
 }
 
-constexpr int kStages = 4;
-constexpr int kGatherThreads = 256;
-constexpr int kChunk = 8;  // SoA elements per work item (16 B of fp16 output)
 
 // ----------------------------------------------------------------- IEEE fast paths
 // Compile-time specialised conversions between plain IEEE lanes: one
@@ -271,12 +269,12 @@ template <int DB>
 __device__ __forceinline__ uint64_t axpy_ieee(uint64_t xq, uint64_t yq, double dt, uint8_t op, uint8_t math) {
     double r;
     if (math == MATH_FP64_EXACT) {
-        // NaN operands propagate quieted, x first (see axpy_f64_exact); done in
+        // NaN operands propagate quieted, y first (see axpy_f64_exact); done in
         // DB space because the hardware widening of a NaN is canonical.
         constexpr int wd = Ieee<DB>::w, md = Ieee<DB>::m;
         constexpr uint64_t qbit = 1ull << (md - 1);
-        if (Ieee<DB>::nan(xq)) return xq | qbit;
         if (Ieee<DB>::nan(yq)) return yq | qbit;
+        if (Ieee<DB>::nan(xq)) return xq | qbit;
         r = __dadd_rn(Ieee<DB>::f64(xq), __dmul_rn(Ieee<DB>::f64(yq), dt));
         if (isnan(r))  // inf - inf: x86 default NaN 0xFFF8... encoded
             return (1ull << (wd - 1)) | (((1ull << (wd - 1 - md)) - 1) << md) | qbit;
@@ -287,43 +285,79 @@ __device__ __forceinline__ uint64_t axpy_ieee(uint64_t xq, uint64_t yq, double d
     return Ieee<DB>::from(r);
 }
 
-// One work item of the fast path: kChunk consecutive SoA elements of a stream.
+// ----------------------------------------------------------------- k_gather_warp
+// Warp-autonomous AoS -> SoA pipeline.  Each warp owns a ring of kWStages
+// shared-memory stages fed by 1-D TMA bulk copies (cp.async.bulk, UBLKCP)
+// with its own mbarriers, so no CTA-wide barrier ever stalls the stream.  A
+// warp tile is 32*R whole records (R chosen so every tile starts 16-B
+// aligned); lane l converts records l, l+32, ... (thread per record keeps
+// the shared-memory reads nearly conflict-free), writes each SoA stream's
+// slice into a per-warp staging area, and the warp stores the slice with
+// coalesced 16-B vector stores.
+constexpr int kWStages = 4;
+
+// Fast path: every lane of stream g for this lane's records, IEEE formats
+// known at compile time (view.cpp fast_kind).
 template <int SB, int DB, int AB>
-__device__ __forceinline__ void chunk_fast(const uint8_t* tile, uint32_t rbytes, const GStream& g, uint32_t e0,
-                                           uint32_t nel, double dt, uint8_t math, uint64_t (&out)[kChunk]) {
+__device__ __forceinline__ void stream_fast(const uint8_t* tile, uint32_t rbytes, const GStream& g, uint32_t lane,
+                                            uint32_t recs, double dt, uint8_t math, uint8_t* out) {
+    constexpr int sb = Ieee<SB>::w / 8, db = Ieee<DB>::w / 8;
     const uint32_t ar = g.arity;
-    const uint8_t* xs = tile + (g.src_off >> 3);
-    const uint8_t* ys = tile + (g.aux_off >> 3);
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) {
-        const uint32_t e = min(e0 + j, nel - 1);
-        const uint32_t r = ar == 1 ? e : e / 3;
-        const uint32_t l = e - r * ar;
-        uint64_t v = cvt_ieee<SB, DB>(lds<SB>(xs + r * rbytes + l * (Ieee<SB>::w / 8)));
-        if constexpr (AB >= 0) {
-            const uint64_t y = cvt_ieee<AB, DB>(lds<AB>(ys + r * rbytes + l * (Ieee<AB>::w / 8)));
-            v = axpy_ieee<DB>(v, y, dt, g.op, math);
+    for (uint32_t r = lane; r < recs; r += 32) {
+        const uint8_t* xr = tile + r * rbytes + (g.src_off >> 3);
+        const uint8_t* yr = tile + r * rbytes + (g.aux_off >> 3);
+        uint8_t* o = out + r * ar * db;
+        for (uint32_t l = 0; l < ar; ++l) {
+            uint64_t v = cvt_ieee<SB, DB>(lds<SB>(xr + l * sb));
+            if constexpr (AB >= 0) {
+                constexpr int ab = Ieee<AB>::w / 8;
+                v = axpy_ieee<DB>(v, cvt_ieee<AB, DB>(lds<AB>(yr + l * ab)), dt, g.op, math);
+            }
+            if constexpr (db == 8) *reinterpret_cast<uint64_t*>(o + l * 8) = v;
+            else if constexpr (db == 4) *reinterpret_cast<uint32_t*>(o + l * 4) = uint32_t(v);
+            else *reinterpret_cast<uint16_t*>(o + l * 2) = uint16_t(v);
         }
-        out[j] = v;
     }
 }
 
-// fast code = 1 + sb*12 + db*3 + ab (view.cpp fast_kind)
-__device__ __forceinline__ bool dispatch_fast(const uint8_t* tile, uint32_t rbytes, const GStream& g, uint32_t e0,
-                                              uint32_t nel, double dt, uint8_t math, uint64_t (&out)[kChunk]) {
+// Generic path: any bit offset / width / truncated format, via funnel shifts.
+__device__ __forceinline__ void stream_generic(const uint8_t* tile, uint32_t record_bits, const GStream& g,
+                                               uint32_t lane, uint32_t recs, double dt, uint8_t math, uint8_t* out) {
+    const uint32_t ar = g.arity;
+    const int sw = g.src.width, aw = g.aux_src.width, dbytes = g.dst.width >> 3;
+    for (uint32_t r = lane; r < recs; r += 32) {
+        const uint64_t rb = uint64_t(r) * record_bits;
+        for (uint32_t l = 0; l < ar; ++l) {
+            uint64_t v = convert_lane(ld_bits_smem(tile, rb + g.src_off + uint64_t(l) * sw, sw), g.src, g.dst);
+            if (g.op != OP_COPY) {
+                const uint64_t y =
+                    convert_lane(ld_bits_smem(tile, rb + g.aux_off + uint64_t(l) * aw, aw), g.aux_src, g.aux_dst);
+                v = axpy_lane(v, g.dst, y, g.aux_dst, dt, g.op, math);
+            }
+            uint8_t* o = out + (r * ar + l) * dbytes;
+            if (dbytes == 8) *reinterpret_cast<uint64_t*>(o) = v;
+            else if (dbytes == 4) *reinterpret_cast<uint32_t*>(o) = uint32_t(v);
+            else *reinterpret_cast<uint16_t*>(o) = uint16_t(v);
+        }
+    }
+}
+
+__device__ __forceinline__ void stream_dispatch(const uint8_t* tile, const GatherPlan& P, const GStream& g,
+                                                uint32_t lane, uint32_t recs, uint8_t* out) {
+    const uint32_t rbytes = P.record_bits >> 3;
     switch (g.fast) {
-#define SFB_CASE(SBI, SB, DBI, DB, ABI, AB)                                              \
-    case 1 + SBI * 12 + DBI * 3 + ABI:                                                   \
-        chunk_fast<SB, DB, AB>(tile, rbytes, g, e0, nel, dt, math, out);                 \
-        return true;
-#define SFB_DST(SBI, SB, DBI, DB)       \
-    SFB_CASE(SBI, SB, DBI, DB, 0, -1)   \
+#define SFB_CASE(SBI, SB, DBI, DB, ABI, AB)                                    \
+    case 1 + SBI * 12 + DBI * 3 + ABI:                                         \
+        stream_fast<SB, DB, AB>(tile, rbytes, g, lane, recs, P.dt, P.math, out); \
+        return;
+#define SFB_DST(SBI, SB, DBI, DB)        \
+    SFB_CASE(SBI, SB, DBI, DB, 0, -1)    \
     SFB_CASE(SBI, SB, DBI, DB, 1, B_F64) \
     SFB_CASE(SBI, SB, DBI, DB, 2, B_F32)
-#define SFB_SRC(SBI, SB)                 \
-    SFB_DST(SBI, SB, 0, B_F16)           \
-    SFB_DST(SBI, SB, 1, B_BF16)          \
-    SFB_DST(SBI, SB, 2, B_F32)           \
+#define SFB_SRC(SBI, SB)        \
+    SFB_DST(SBI, SB, 0, B_F16)  \
+    SFB_DST(SBI, SB, 1, B_BF16) \
+    SFB_DST(SBI, SB, 2, B_F32)  \
     SFB_DST(SBI, SB, 3, B_F64)
         SFB_SRC(0, B_F64)
         SFB_SRC(1, B_F32)
@@ -331,114 +365,79 @@ __device__ __forceinline__ bool dispatch_fast(const uint8_t* tile, uint32_t rbyt
 #undef SFB_DST
 #undef SFB_CASE
         default:
-            return false;
+            stream_generic(tile, P.record_bits, g, lane, recs, P.dt, P.math, out);
     }
 }
 
-// ----------------------------------------------------------------- k_gather_tiled
-__global__ void __launch_bounds__(kGatherThreads) k_gather_tiled(const __grid_constant__ GatherPlan P,
-                                                                 const uint8_t* __restrict__ src,
-                                                                 uint8_t* __restrict__ dst, uint64_t src_bytes) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    const uint32_t stage_bytes = P.tile_bytes + 16;  // +16: funnel-shift overread pad
-    uint8_t* tiles = smem + 128;
-    const uint64_t ntiles = (P.count + P.tile_recs - 1) / P.tile_recs;
-    const int tid = threadIdx.x;
+// Warp-wide copy of a staged SoA slice to global memory.
+__device__ __forceinline__ void warp_store(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint32_t elem,
+                                           uint32_t lane) {
+    if (((reinterpret_cast<uintptr_t>(dst) | bytes) & 15) == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (uint32_t i = lane; i < bytes / 16; i += 32) d4[i] = s4[i];
+        return;
+    }
+    for (uint32_t i = lane; i < bytes / elem; i += 32) {
+        uint64_t v = 0;
+        memcpy(&v, src + i * elem, elem);
+        st_bytes(dst + i * elem, v, int(elem));
+    }
+}
 
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+__global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ GatherPlan P,
+                                                        const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                        uint64_t src_bytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * kWStages;
+    const uint32_t stage_bytes = (P.tile_bytes + 16 + 15) & ~15u;   // +16: funnel-shift overread pad
+    uint8_t* stages = smem + 128 * ((warps * kWStages * 8 + 127) / 128) +
+                      size_t(warp) * (kWStages * stage_bytes + P.out_bytes);
+    uint8_t* out = stages + kWStages * stage_bytes;
+    const uint64_t ntiles = (P.count + P.tile_recs - 1) / P.tile_recs;
+    const uint64_t gw = uint64_t(blockIdx.x) * warps + warp, tw = uint64_t(gridDim.x) * warps;
+
+    if (lane == 0) {
+        for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    __syncwarp();
 
     auto issue = [&](uint64_t t, int s) {
         const uint64_t off = t * uint64_t(P.tile_bytes);
-        uint64_t bytes = min(uint64_t(P.tile_bytes), src_bytes - off);
+        const uint64_t bytes = min(uint64_t(P.tile_bytes), src_bytes - off);
         const uint32_t bulk = uint32_t(bytes & ~15ull);
         mbar_expect_tx(&bars[s], bulk);
-        if (bulk) tma_bulk_g2s(tiles + s * stage_bytes, src + off, bulk, &bars[s]);
+        if (bulk) tma_bulk_g2s(stages + s * stage_bytes, src + off, bulk, &bars[s]);
     };
-
-    if (tid == 0)
-        for (int s = 0; s < kStages; ++s) {
-            const uint64_t t = blockIdx.x + uint64_t(s) * gridDim.x;
-            if (t < ntiles) issue(t, s);
-        }
+    if (lane == 0)
+        for (int s = 0; s < kWStages; ++s)
+            if (gw + s * tw < ntiles) issue(gw + s * tw, s);
 
     uint32_t k = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const int s = int(k % kStages);
-        uint8_t* tile = tiles + s * stage_bytes;
-        mbar_wait(&bars[s], (k / kStages) & 1);
+    for (uint64_t t = gw; t < ntiles; t += tw, ++k) {
+        const int s = int(k % kWStages);
+        uint8_t* tile = stages + s * stage_bytes;
+        mbar_wait(&bars[s], (k / kWStages) & 1);
         const uint64_t rec0 = t * P.tile_recs;
         const uint32_t recs = uint32_t(min(uint64_t(P.tile_recs), P.count - rec0));
-        if (recs < P.tile_recs) {  // last tile: the <16-byte tail the bulk copy skipped
+        if (recs < P.tile_recs) {  // the <16-byte tail the bulk copy skipped
             const uint64_t off = t * uint64_t(P.tile_bytes);
             const uint64_t bytes = src_bytes - off;
-            const uint32_t bulk = uint32_t(bytes & ~15ull);
-            for (uint32_t b = bulk + tid; b < bytes; b += blockDim.x) tile[b] = src[off + b];
-            __syncthreads();
+            for (uint32_t b = uint32_t(bytes & ~15ull) + lane; b < bytes; b += 32) tile[b] = src[off + b];
+            __syncwarp();
         }
-        // work items: (stream, chunk of kChunk consecutive SoA elements)
-        uint32_t items = 0;
-        for (uint32_t q = 0; q < P.n; ++q) items += (recs * P.s[q].arity + kChunk - 1) / kChunk;
-        for (uint32_t it = tid; it < items; it += blockDim.x) {
-            uint32_t q = 0, c = it;
-            for (;; ++q) {
-                const uint32_t nc = (recs * P.s[q].arity + kChunk - 1) / kChunk;
-                if (c < nc) break;
-                c -= nc;
-            }
+        for (uint32_t q = 0; q < P.n; ++q) {
             const GStream& g = P.s[q];
-            const uint32_t ar = g.arity;
-            const uint32_t nel = recs * ar;
-            const uint32_t e0 = c * kChunk;
-            const int sw = g.src.width, aw = g.aux_src.width, dw = g.dst.width;
-            uint64_t out[kChunk];
-            if (!(g.fast && dispatch_fast(tile, P.record_bits >> 3, g, e0, nel, P.dt, P.math, out)))
-#pragma unroll
-            for (int j = 0; j < kChunk; ++j) {
-                const uint32_t e = min(e0 + j, nel - 1);
-                const uint32_t r = ar == 1 ? e : e / 3;
-                const uint32_t l = e - r * ar;
-                const uint64_t rb = uint64_t(r) * P.record_bits;
-                uint64_t v = convert_lane(ld_bits_smem(tile, rb + g.src_off + uint64_t(l) * sw, sw), g.src, g.dst);
-                if (g.op != OP_COPY) {
-                    const uint64_t y = convert_lane(ld_bits_smem(tile, rb + g.aux_off + uint64_t(l) * aw, aw), g.aux_src,
-                                                    g.aux_dst);
-                    v = axpy_lane(v, g.dst, y, g.aux_dst, P.dt, g.op, P.math);
-                }
-                out[j] = v;
-            }
-            uint8_t* o = dst + g.dst_base + (rec0 * ar + e0) * uint64_t(dw >> 3);
-            const bool full = e0 + kChunk <= nel && (reinterpret_cast<uintptr_t>(o) & 15) == 0;
-            if (full) {
-                if (dw == 16) {
-                    uint4 v4;
-                    v4.x = uint32_t(out[0] | (out[1] << 16));
-                    v4.y = uint32_t(out[2] | (out[3] << 16));
-                    v4.z = uint32_t(out[4] | (out[5] << 16));
-                    v4.w = uint32_t(out[6] | (out[7] << 16));
-                    *reinterpret_cast<uint4*>(o) = v4;
-                } else if (dw == 32) {
-                    uint4* o4 = reinterpret_cast<uint4*>(o);
-                    o4[0] = make_uint4(uint32_t(out[0]), uint32_t(out[1]), uint32_t(out[2]), uint32_t(out[3]));
-                    o4[1] = make_uint4(uint32_t(out[4]), uint32_t(out[5]), uint32_t(out[6]), uint32_t(out[7]));
-                } else {
-                    uint4* o4 = reinterpret_cast<uint4*>(o);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        o4[j] = make_uint4(uint32_t(out[2 * j]), uint32_t(out[2 * j] >> 32), uint32_t(out[2 * j + 1]),
-                                           uint32_t(out[2 * j + 1] >> 32));
-                }
-            } else {
-                for (int j = 0; j < kChunk && e0 + j < nel; ++j) st_bytes(o + j * (dw >> 3), out[j], dw >> 3);
-            }
+            const uint32_t db = g.dst.width >> 3;
+            stream_dispatch(tile, P, g, lane, recs, out);
+            __syncwarp();
+            warp_store(dst + g.dst_base + rec0 * g.arity * db, out, recs * g.arity * db, db, lane);
+            __syncwarp();
         }
-        __syncthreads();  // every thread is done with this stage
-        if (tid == 0) {
-            const uint64_t tn = t + uint64_t(kStages) * gridDim.x;
+        if (lane == 0) {
+            const uint64_t tn = t + uint64_t(kWStages) * tw;
             if (tn < ntiles) issue(tn, s);
         }
     }
@@ -512,23 +511,30 @@ cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cud
     return cudaGetLastError();
 }
 
-size_t gather_smem_bytes(const GatherPlan& p) { return 128 + size_t(kStages) * (p.tile_bytes + 16); }
+static size_t gather_warp_bytes(const GatherPlan& p) {
+    return size_t(kWStages) * ((p.tile_bytes + 16 + 15) & ~15u) + p.out_bytes;
+}
 
 cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
-                          int ctas_per_sm) {
+                          int /*ctas_per_sm*/) {
     if (p.count == 0 || p.n == 0) return cudaSuccess;
-    const size_t smem = gather_smem_bytes(p);
+    const size_t per_warp = gather_warp_bytes(p);
+    const size_t budget = 220 * 1024;
+    int warps = int(std::min<size_t>(16, (budget - 1024) / per_warp));
+    if (warps < 1) return cudaErrorInvalidValue;
+    const size_t smem = 128 * ((size_t(warps) * kWStages * 8 + 127) / 128) + size_t(warps) * per_warp;
     static size_t configured = 0;
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_gather_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e = cudaFuncSetAttribute(k_gather_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         configured = smem;
     }
     const uint64_t ntiles = (p.count + p.tile_recs - 1) / p.tile_recs;
-    if (ctas_per_sm <= 0) ctas_per_sm = int(std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / smem)));
-    const int blocks = int(std::min<uint64_t>(ntiles, uint64_t(num_sms()) * ctas_per_sm));
-    k_gather_tiled<<<blocks, kGatherThreads, smem, st>>>(p, static_cast<const uint8_t*>(src),
-                                                         static_cast<uint8_t*>(dst), src_bytes);
+    const int ctas = int(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
+    const uint64_t want = (ntiles + warps - 1) / warps;
+    const int blocks = int(std::min<uint64_t>(want, uint64_t(num_sms()) * ctas));
+    k_gather_warp<<<blocks, warps * 32, smem, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst),
+                                                   src_bytes);
     return cudaGetLastError();
 }
 

@@ -63,8 +63,9 @@ struct GatherPlan {
     uint64_t count = 0;
     uint32_t record_bits = 0;
     uint32_t n = 0;
-    uint32_t tile_recs = 0;   // multiple of 128: every tile starts 16-B aligned
+    uint32_t tile_recs = 0;   // per-warp tile: 32*R records, 16-B aligned start
     uint32_t tile_bytes = 0;  // tile_recs * record_bits / 8
+    uint32_t out_bytes = 0;   // per-warp SoA staging (largest stream slice)
     uint8_t math = MATH_FP64_EXACT;
     double dt = 0;
     GStream s[kMaxStreams];

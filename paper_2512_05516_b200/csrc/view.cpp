@@ -1,6 +1,7 @@
 #include "view.hpp"
 
 #include <algorithm>
+#include <numeric>
 #include <stdexcept>
 
 namespace sfb {
@@ -134,7 +135,12 @@ static uint8_t fast_kind(const GStream& s, uint32_t record_bits) {
 }
 
 static void finalize_fast(GatherPlan& g) {
-    for (uint32_t i = 0; i < g.n; ++i) g.s[i].fast = fast_kind(g.s[i], g.record_bits);
+    uint32_t out = 16;
+    for (uint32_t i = 0; i < g.n; ++i) {
+        g.s[i].fast = fast_kind(g.s[i], g.record_bits);
+        out = std::max(out, g.tile_recs * g.s[i].arity * (g.s[i].dst.width / 8u));
+    }
+    g.out_bytes = (out + 15) & ~15u;
 }
 
 GatherPlan plan_gather(const View& src, const View& dst) {
@@ -145,10 +151,11 @@ GatherPlan plan_gather(const View& src, const View& dst) {
     GatherPlan g;
     g.count = src.count;
     g.record_bits = uint32_t(src.record_bits());
-    const uint64_t unit_bytes = 16ull * g.record_bits;  // bytes of 128 records
-    uint64_t k = std::max<uint64_t>(1, (24576 + unit_bytes / 2) / unit_bytes);
-    g.tile_recs = uint32_t(128 * k);
+    // warp tile: 32*R records, R the smallest with 32*R*record_bits % 128 == 0
+    const uint32_t period = 128 / std::gcd(g.record_bits, 128u);  // records per 16-B step
+    g.tile_recs = 32 * std::max<uint32_t>(1, period / 32);
     g.tile_bytes = uint32_t(g.tile_recs * uint64_t(g.record_bits) / 8);
+    if (g.record_bits == 0) throw std::invalid_argument("empty record");
     for (size_t dp = 0; dp < dst.subset.size(); ++dp) {
         const int f = dst.subset[dp];
         const int sp = src.pos_of(f);

@@ -1,0 +1,258 @@
+"""Cell-sharded SPH step across GPUs (BASELINE C5).
+
+Particles are decomposed into x-slabs of whole cell layers (cells of side
+>= 2h, so every neighbour of a particle lies in the 27 surrounding cells).
+Rank r owns layers [x0, x1).  One step:
+
+    kick, drift           in place on the rank's SoA buffer (sm_100a kernels)
+    migrate               particles whose layer left [x0, x1) move to the
+                          neighbouring rank (one neighbour exchange)
+    halo                  boundary layers x0 and x1-1 of (x, m, h) go to the
+                          left/right neighbours: ncclSend/ncclRecv pairs in
+                          one group (torch.distributed batch_isend_irecv)
+    density               counting-sort own+ghost particles into the local
+                          grid (own layers + one ghost layer each side), then
+                          the cell-linked density over the own layers only
+
+NVSwitch makes every peer equidistant, so slab r simply maps to rank r.  The
+exchange uses only neighbour point-to-point traffic; there is no collective
+on the data path.  The same code runs with gloo on CPU tensors (tests) with
+a pluggable density backend.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Tuple
+
+import torch
+
+FIELD_DTYPES = {64: torch.float64, 32: torch.float32, 16: torch.float16}
+
+
+@dataclass
+class Slab:
+    """x-slab of cell layers owned by one rank."""
+    nc: int      # cells per side of the global grid
+    cell: float  # cell side (>= 2h)
+    rank: int
+    world: int
+
+    @property
+    def x0(self) -> int:
+        return self.rank * self.nc // self.world
+
+    @property
+    def x1(self) -> int:
+        return (self.rank + 1) * self.nc // self.world
+
+    def layer(self, xcol: torch.Tensor) -> torch.Tensor:
+        return torch.clamp(torch.floor(xcol.float() / self.cell), 0, self.nc - 1).to(torch.int32)
+
+    @property
+    def local_lo(self) -> int:  # first layer of the local grid (one ghost layer)
+        return max(self.x0 - 1, 0)
+
+    @property
+    def local_hi(self) -> int:
+        return min(self.x1 + 1, self.nc)
+
+
+def grid_for(n_global: int, neighbours: float = 64.0, multiple: int = 8) -> Tuple[float, int, float]:
+    """h with ~`neighbours` particles inside 2h for a uniform unit box, and
+    the cell grid: side 1/nc >= 2h, nc rounded down to a multiple of 8 so
+    1/2/4/8 ranks get equal slabs (200 cells at 2^27)."""
+    h = 0.5 * (3.0 * neighbours / (4.0 * math.pi * n_global)) ** (1.0 / 3.0)
+    nc = int(math.floor(1.0 / (2.0 * h)))
+    if nc >= 2 * multiple:
+        nc -= nc % multiple
+    return h, max(nc, 1), 1.0 / max(nc, 1)
+
+
+def neighbour_exchange(send_left: torch.Tensor, send_right: torch.Tensor, rank: int, world: int,
+                       group=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Rows to rank-1 / rank+1; returns rows received from rank-1 / rank+1.
+    Counts first, then the payloads, each as one grouped send/recv batch
+    (ncclGroupStart; ncclSend/ncclRecv x 4; ncclGroupEnd under NCCL)."""
+    import torch.distributed as dist
+    dev = send_left.device
+    row = tuple(send_left.shape[1:])
+    cnt_out = {d: torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
+               for d, t in ((-1, send_left), (1, send_right))}
+    cnt_in = {d: torch.zeros(1, dtype=torch.int64, device=dev) for d in (-1, 1)}
+    peers = [d for d in (-1, 1) if 0 <= rank + d < world]
+    ops = []
+    for d in peers:
+        ops.append(dist.P2POp(dist.isend, cnt_out[d], rank + d, group))
+        ops.append(dist.P2POp(dist.irecv, cnt_in[d], rank + d, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    recv = {d: torch.empty((int(cnt_in[d].item()),) + row, dtype=send_left.dtype, device=dev) for d in (-1, 1)}
+    ops = []
+    for d in peers:
+        out = send_left if d == -1 else send_right
+        if out.shape[0]:
+            ops.append(dist.P2POp(dist.isend, out.contiguous(), rank + d, group))
+        if recv[d].shape[0]:
+            ops.append(dist.P2POp(dist.irecv, recv[d], rank + d, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    return recv[-1], recv[1]
+
+
+def halo_rows(x: torch.Tensor, m: torch.Tensor, h: torch.Tensor, slab: Slab):
+    """Boundary-layer rows (x0, y, z, m, h) for the left and right neighbours."""
+    ix = slab.layer(x[:, 0])
+    rows = torch.cat([x, m[:, None], h[:, None]], dim=1)
+    left = rows[ix == slab.x0] if slab.rank > 0 else rows[:0]
+    right = rows[ix == slab.x1 - 1] if slab.rank < slab.world - 1 else rows[:0]
+    return left, right
+
+
+def exchange_halo(x, m, h, slab: Slab, group=None):
+    """Ghost particles (x, m, h) received from the neighbouring slabs."""
+    left, right = halo_rows(x, m, h, slab)
+    if slab.world == 1:
+        return x[:0], m[:0], h[:0]
+    gl, gr = neighbour_exchange(left, right, slab.rank, slab.world, group)
+    g = torch.cat([gl, gr], dim=0)
+    return g[:, 0:3].contiguous(), g[:, 3].contiguous(), g[:, 4].contiguous()
+
+
+def migrate_rows(rows: torch.Tensor, xcol: torch.Tensor, slab: Slab, group=None) -> torch.Tensor:
+    """Particles (one row each, any dtype) whose layer left the slab move to
+    the neighbour; returns the rank's new row set (kept + received)."""
+    ix = slab.layer(xcol)
+    go_l = ix < slab.x0
+    go_r = ix >= slab.x1
+    keep = ~(go_l | go_r)
+    if slab.world == 1:
+        return rows
+    rl, rr = neighbour_exchange(rows[go_l], rows[go_r], slab.rank, slab.world, group)
+    return torch.cat([rows[keep], rl, rr], dim=0)
+
+
+DensityFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor, Slab, int], torch.Tensor]
+
+
+def density_with_ghosts(x, m, h, gx, gm, gh, slab: Slab, backend: DensityFn) -> torch.Tensor:
+    """rho of the own particles given the ghosts: own rows come first in the
+    combined set, ghosts after; backend(xc, mc, hc, slab, n_own) -> rho[n_own]."""
+    xc = torch.cat([x, gx.to(x.dtype)], dim=0)
+    mc = torch.cat([m, gm.to(m.dtype)], dim=0)
+    hc = torch.cat([h, gh.to(h.dtype)], dim=0)
+    return backend(xc, mc, hc, slab, x.shape[0])
+
+
+def gpu_density_backend(prec: int):
+    """bin_particles + density_cells on the rank's local grid (own layers
+    plus one ghost layer per side), own layers computed only."""
+    from . import api
+
+    def run(xc, mc, hc, slab: Slab, n_own: int) -> torch.Tensor:
+        lo_layer, hi_layer = slab.local_lo, slab.local_hi
+        dims = (hi_layer - lo_layer, slab.nc, slab.nc)
+        lo = (lo_layer * slab.cell, 0.0, 0.0)
+        cs, perm = api.bin_particles(xc.float().contiguous(), lo, slab.cell, dims)
+        p = perm[: xc.shape[0]].long()
+        rho_sorted = api.density_cells(xc[p].contiguous(), mc[p].contiguous(), hc[p].contiguous(), cs, dims,
+                                       own=(slab.x0 - lo_layer, slab.x1 - lo_layer), prec=prec)
+        rho = torch.empty(xc.shape[0], dtype=torch.float32, device=xc.device)
+        rho[p] = rho_sorted[: xc.shape[0]]
+        return rho[:n_own]
+
+    return run
+
+
+class ShardedState:
+    """One rank's particles: SoA buffer of the reference's default schema at
+    uniform storage precision `prec` (32 or 16; positions included)."""
+
+    def __init__(self, n_global: int, slab: Slab, prec: int = 32, seed: int = 7, device="cuda",
+                 h: Optional[float] = None):
+        from . import api
+        self.api, self.slab, self.prec, self.device = api, slab, prec, device
+        self.schema = api.Schema.default()
+        self.h = h if h is not None else grid_for(n_global)[0]
+        n = n_global // slab.world
+        g = torch.Generator(device=device).manual_seed(seed + slab.rank)
+        x = torch.rand(n, 3, generator=g, device=device, dtype=torch.float64)
+        x[:, 0] = (slab.x0 + x[:, 0] * (slab.x1 - slab.x0)) * slab.cell
+        fields = {
+            "x": x, "id": torch.arange(n, device=device, dtype=torch.int64) + slab.rank * n,
+            "v": torch.rand(n, 3, generator=g, device=device, dtype=torch.float64) * 2 - 1,
+            "u": torch.rand(n, generator=g, device=device, dtype=torch.float64) + 0.5,
+            "m": torch.full((n,), 1.0 / n_global, device=device, dtype=torch.float64),
+            "h": torch.full((n,), self.h, device=device, dtype=torch.float64),
+            "rho": torch.ones(n, device=device, dtype=torch.float64),
+            "P": torch.zeros(n, device=device, dtype=torch.float64),
+            "cs": torch.zeros(n, device=device, dtype=torch.float64),
+            "a": torch.rand(n, 3, generator=g, device=device, dtype=torch.float64) * 2 - 1,
+            "du": torch.rand(n, generator=g, device=device, dtype=torch.float64) * 2 - 1,
+            "dt": torch.full((n,), 1e-3, device=device, dtype=torch.float64),
+        }
+        self.set_fields(fields)
+
+    # -- buffer plumbing ------------------------------------------------------
+    def view(self, n):
+        return self.api.View(self.schema, n, "soa", None, self.prec)
+
+    def set_fields(self, fields):
+        n = fields["id"].shape[0]
+        self.n = n
+        self.buf = self.api.PackedBuffer.empty(self.view(n), self.device)
+        for name, t in fields.items():
+            self.stream(name).copy_(t.reshape(self.stream(name).shape).to(self.stream(name).dtype))
+
+    def stream(self, name) -> torch.Tensor:
+        base, stride, w, ar = self.buf.view.lane(name)
+        dt = torch.int64 if name == "id" else FIELD_DTYPES[w]
+        nbytes = self.n * ar * w // 8
+        t = self.buf.data[base // 8: base // 8 + nbytes].view(dt)
+        return t.view(self.n, ar) if ar == 3 else t
+
+    def rows(self) -> torch.Tensor:
+        """All fields of every particle as one byte row (for migration)."""
+        names = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
+        return torch.cat([self.stream(k).reshape(self.n, -1).view(torch.uint8) for k in names], dim=1)
+
+    def from_rows(self, rows: torch.Tensor):
+        names = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
+        widths = {}
+        for k in names:
+            _, _, w, ar = self.buf.view.lane(k)
+            widths[k] = (w // 8) * ar
+        n = rows.shape[0]
+        fields, c = {}, 0
+        for k in names:
+            b = rows[:, c: c + widths[k]].contiguous()
+            c += widths[k]
+            _, _, w, ar = self.buf.view.lane(k)
+            dt = torch.int64 if k == "id" else FIELD_DTYPES[w]
+            fields[k] = b.view(dt).reshape(n, ar) if ar == 3 else b.view(dt).reshape(n)
+        self.set_fields(fields)
+
+    # -- the step ---------------------------------------------------------------
+    def kick_drift(self, dt=1e-3):
+        self.api.run_kernel(self.buf, "kick", dt, buffer_size=1)
+        self.api.run_kernel(self.buf, "drift", dt, buffer_size=1)
+
+    def migrate(self, group=None):
+        if self.slab.world == 1:
+            return
+        xcol = self.stream("x")[:, 0]
+        self.from_rows(migrate_rows(self.rows(), xcol, self.slab, group))
+
+    def density(self, group=None):
+        x, m, h = self.stream("x"), self.stream("m"), self.stream("h")
+        gx, gm, gh = exchange_halo(x, m, h, self.slab, group)
+        prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
+        rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec))
+        self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
+
+    def step(self, dt=1e-3, group=None):
+        self.kick_drift(dt)
+        self.migrate(group)
+        self.density(group)
