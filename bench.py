@@ -258,7 +258,8 @@ def b200_arm(args):
         ok = bool(torch.equal(got, out.data[: dst_v.nbytes]))
         e2e = {"value": n * world / float(s_t.item()), "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"],
                "d2h_bytes_per_step": m["d2h_bytes"], "chunk_particles": args.chunk, "matches_device_result": ok,
-               "path": "sf_b200_run_host(streamed): pinned AoS -> H2D || k_gather_tiled || D2H SoA"}
+               "path": "sf_b200_run_host(streamed): pinned AoS -> 2-D DMA of the x..v span (44 of 88 B) || "
+                       "k_gather_warp || D2H SoA"}
         hb.free()
         hs.free()
 
@@ -287,6 +288,48 @@ def b200_arm(args):
     return 0
 
 
+def other_arm(args):
+    """--workload c1 | c3 | c4 | c5 (benchmarks/workloads.py)."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "benchmarks"))
+    import workloads as W
+    from paper_2512_05516_b200 import api
+
+    world, rank, local = dist_init()
+    peak, kind = peaks()
+    sampler = ClockSampler(local)
+    sampler.start()
+    l0 = api.launch_count()
+    if args.workload == "c5":
+        res = W.c5(args, peak, kind, world, rank)
+        ms = torch.tensor([res["ms_per_step"]], device="cuda", dtype=torch.float64)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        res["ms_per_step"] = float(ms.item())
+        res["value"] = args.c5_n / (res["ms_per_step"] * 1e-3)
+    else:
+        res = getattr(W, args.workload)(args, peak, kind)
+    launches = api.launch_count() - l0
+    clocks = sampler.stop()
+    if rank == 0:
+        line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f64" if
+                args.workload in ("c1", "c4") else "f32", "data": "synthetic (uniform random, device RNG)",
+                "config": res["config"], "roofline": res["roofline"], "cpu_baseline": None, "e2e": None,
+                "gpu_launches": launches, "clocks": clocks, "impl": "b200", "workload": args.workload}
+        for k in ("kernels", "phases_ms", "particles_local"):
+            if k in res:
+                line[k] = res[k]
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -300,9 +343,15 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c2",
+                    help="BASELINE.json config (default c2 = configs[1], the headline)")
+    ap.add_argument("--c4-n", type=int, default=1 << 26)
+    ap.add_argument("--c5-n", type=int, default=1 << 27)
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.workload != "c2":
+        return other_arm(args)
     return b200_arm(args)
 
 

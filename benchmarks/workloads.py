@@ -1,0 +1,227 @@
+"""The non-default BASELINE.json configs as bench.py workloads (`--workload`).
+
+  c1  kick / drift on 1M particles, AoS full-precision storage, in place
+      (92 MB < L2: L2 flushed between timed launches, each launch timed alone)
+  c3  SPH density, cell-linked, 4M uniform particles, SoA fp32 vs fp16 vs bf16
+  c4  64M host-resident particles: streamed (narrowed 2-D DMA) vs managed vs
+      in-place (whole records), one drift and one kick+drift step each
+  c5  128M particles, density + kick/drift sharded by cell (NCCL halo)
+
+Each returns the same JSON-line dict as the default C2 workload.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+
+import torch
+
+from paper_2512_05516_b200 import api
+
+UNIT = "particle updates/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+class L2Flush:
+    def __init__(self):
+        self.buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def __call__(self):
+        self.buf.fill_(1)
+
+
+def timed_each(fn, steps, flush=None, stream=None):
+    """Per-launch CUDA-event times (ms), L2 flushed before each launch."""
+    stream = stream or torch.cuda.current_stream()
+    times = []
+    for _ in range(steps):
+        if flush:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    return times
+
+
+def random_default_aos(n, seed=1234):
+    P = api.Schema.default()
+    v = api.View(P, n, "aos")
+    src = api.PackedBuffer.empty(v)
+    rec = src.data[: v.nbytes].view(n, 88)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    step = 1 << 22
+    for b in range(0, n, step):
+        e = min(n, b + step)
+        m = e - b
+        f = torch.rand(m, 17, device="cuda", generator=g)
+        rec[b:e, 0:24] = f[:, 0:3].double().contiguous().view(torch.uint8).view(m, 24)
+        rec[b:e, 24:32] = torch.arange(b, e, device="cuda", dtype=torch.int64).view(torch.uint8).view(m, 8)
+        f[:, 3:6] = f[:, 3:6] * 2 - 1
+        f[:, 13:17] = f[:, 13:17] * 2 - 1   # a, du ~ U(-1, 1): kick is not a no-op
+        rec[b:e, 32:88] = f[:, 3:17].contiguous().view(torch.uint8).view(m, 56)
+    return P, v, src
+
+
+def roofline(bytes_per_unit, units, ms, peak, kind, kernel, traffic=None):
+    ach = bytes_per_unit * units / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_kind": kind, "kernel": kernel, "algorithmic_bytes_per_particle": bytes_per_unit,
+            "traffic": traffic}
+
+
+# ----------------------------------------------------------------------- C1
+def c1(args, peak, peak_kind):
+    n = 1 << 20
+    P, v, src = random_default_aos(n)
+    nat = api.convert(src, api.View(P, n, "aos", None, api.SF_PREC_NATIVE))
+    flush = L2Flush()
+    out = {}
+    for k, bpp in (("kick", 48), ("drift", 60)):
+        fn = lambda: api.run_kernel(nat, k, 1e-3, buffer_size=64)  # noqa: E731
+        for _ in range(args.warmup):
+            fn()
+        t = timed_each(fn, args.steps, flush)
+        ms = sum(t) / len(t)
+        out[k] = {"ms": ms, "value": n / (ms * 1e-3),
+                  "roofline": roofline(bpp, n, ms, peak, peak_kind, "k_convert (in-place %s, AoS f64/f32)" % k)}
+    ms = out["kick"]["ms"] + out["drift"]["ms"]
+    return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": out["drift"]["roofline"],
+            "config": {"workload": "C1 (BASELINE configs[0]): kick then drift in place on 1M particles, AoS "
+                                   "full-precision storage (default 88-B schema)", "particles": n,
+                       "l2": "92 MB < 126 MB L2: L2 flushed (512 MB write) before every timed launch",
+                       "arith": "binary64, bit-exact vs reference"},
+            "kernels": out}
+
+
+# ----------------------------------------------------------------------- C3
+def c3(args, peak, peak_kind):
+    from paper_2512_05516_b200.sharded import grid_for
+    n = 1 << 22
+    h, nc, cell = grid_for(n)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(n, 3, generator=g, device="cuda", dtype=torch.float32)
+    m = torch.full((n,), 1.0 / n, device="cuda")
+    hh = torch.full((n,), h, device="cuda")
+    dims = (nc, nc, nc)
+    out = {}
+    for name, prec, dt in (("fp32", api.SF_PREC_NATIVE, torch.float32), ("fp16", 16, torch.float16),
+                           ("bf16", api.SF_PREC_BF16, torch.bfloat16)):
+        xs, ms_, hs = x.to(dt), m.to(dt), hh.to(dt)
+        cs, perm = api.bin_particles(xs.float().contiguous(), (0, 0, 0), cell, dims)
+        p = perm.long()
+        xs, ms_, hs = xs[p].contiguous(), ms_[p].contiguous(), hs[p].contiguous()
+        rho = torch.empty(n, device="cuda")
+        fn = lambda: api.density_cells(xs, ms_, hs, cs, dims, prec=prec, rho=rho)  # noqa: E731
+        for _ in range(args.warmup):
+            fn()
+        t = timed_each(fn, max(3, args.steps // 5))
+        tb = timed_each(lambda: api.bin_particles(x, (0, 0, 0), cell, dims, cell_start=cs, perm=perm),
+                        max(3, args.steps // 5))
+        msd, msb = sum(t) / len(t), sum(tb) / len(tb)
+        # pairs inside the support, for pairs/s
+        pairs = None
+        if name == "fp32":
+            sample = x[:4096]
+            d = torch.cdist(sample.double(), x.double())
+            pairs = float((d < 2 * h).sum().item()) / 4096 * n
+        bytes_pp = {"fp32": 24, "fp16": 12, "bf16": 12}[name]
+        out[name] = {"density_ms": msd, "bin_ms": msb, "value": n / (msd * 1e-3),
+                     "hbm_GBps_algorithmic": bytes_pp * n / (msd * 1e-3) / 1e9,
+                     "pairs_in_support": pairs}
+    ms = out["fp32"]["density_ms"]
+    rl = {"bound": "compute (FP32 + MUFU)", "achieved": out["fp32"]["hbm_GBps_algorithmic"], "peak": peak,
+          "unit": "GB/s", "frac": out["fp32"]["hbm_GBps_algorithmic"] / peak, "peak_kind": peak_kind,
+          "kernel": "k_density_cells (fp32)", "algorithmic_bytes_per_particle": 24, "traffic": None}
+    if out["fp32"]["pairs_in_support"]:
+        rl["pairs_per_s"] = out["fp32"]["pairs_in_support"] / (ms * 1e-3)
+    return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": rl,
+            "config": {"workload": "C3 (BASELINE configs[2]): SPH density, cell-linked, 4M uniform particles, "
+                                   "SoA fp32 vs fp16 vs bf16", "particles": n, "h": h, "cells_per_side": nc,
+                       "value_is": "fp32 density kernel; binning reported separately"},
+            "kernels": out}
+
+
+# ----------------------------------------------------------------------- C4
+def c4(args, peak, peak_kind):
+    n = args.c4_n
+    P, v, src = random_default_aos(n)
+    pinned = api.HostBuffer(v.nbytes, 0)
+    managed = api.HostBuffer(v.nbytes, 1)
+    hp, hm = pinned.numpy(), managed.numpy()
+    step = 1 << 22
+    for b in range(0, v.nbytes, step * 88):
+        e = min(v.nbytes, b + step * 88)
+        blk = src.data[b:e].cpu().numpy()
+        hp[b:e] = blk
+        hm[b:e] = blk
+    del src
+    torch.cuda.empty_cache()
+    out = {}
+    for kernels, dst_set in (("drift", "drift"), ("kick,drift", None)):
+        dst = api.View(P, n, "soa", dst_set, 16)
+        for mode, name, hb in ((0, "streamed", pinned), (1, "managed", managed), (2, "inplace", pinned)):
+            api.run_host(v, hb, dst, kernels, 1e-3, chunk=args.chunk, mode=mode)
+            secs = []
+            for _ in range(max(2, min(args.steps, 5))):
+                m = api.run_host(v, hb, dst, kernels, 1e-3, chunk=args.chunk, mode=mode)
+                secs.append(m["seconds"])
+            s = sum(secs) / len(secs)
+            out["%s:%s" % (kernels, name)] = {"ms": s * 1e3, "value": n / s, "h2d_bytes": m["h2d_bytes"],
+                                              "d2h_bytes": m["d2h_bytes"],
+                                              "pcie_GBps": (m["h2d_bytes"] + m["d2h_bytes"]) / s / 1e9}
+    pinned.free()
+    managed.free()
+    best = out["drift:streamed"]
+    return {"value": best["value"], "ms_per_step": best["ms"],
+            "roofline": {"bound": "pcie", "achieved": best["pcie_GBps"], "peak": None, "unit": "GB/s",
+                         "frac": None, "kernel": "run_host streamed (2-D DMA + k_gather_warp + scatter)"},
+            "config": {"workload": "C4 (BASELINE configs[3]): 64M host-resident particles, streamed vs managed "
+                                   "vs in-place, one drift and one kick+drift step (gather, compute, scatter-back)",
+                       "particles": n, "chunk": args.chunk, "soa_precision": "binary16"},
+            "kernels": out}
+
+
+# ----------------------------------------------------------------------- C5
+def c5(args, peak, peak_kind, world, rank, group=None):
+    from paper_2512_05516_b200.sharded import ShardedState, Slab, grid_for
+    n = args.c5_n
+    h, nc, cell = grid_for(n)
+    slab = Slab(nc, cell, rank, world)
+    st = ShardedState(n, slab, prec=32, h=h)
+    for _ in range(max(1, min(args.warmup, 2))):
+        st.step(group=group)
+    torch.cuda.synchronize()
+    phases = {"kick_drift": [], "migrate": [], "density": []}
+    times = []
+    for _ in range(max(2, min(args.steps, 5))):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        c = torch.cuda.Event(enable_timing=True); d = torch.cuda.Event(enable_timing=True)
+        a.record()
+        st.kick_drift()
+        b.record()
+        st.migrate(group)
+        c.record()
+        st.density(group)
+        d.record()
+        d.synchronize()
+        phases["kick_drift"].append(a.elapsed_time(b))
+        phases["migrate"].append(b.elapsed_time(c))
+        phases["density"].append(c.elapsed_time(d))
+        times.append(a.elapsed_time(d))
+    ms = sum(times) / len(times)
+    return {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
+            "roofline": {"bound": "compute (density)", "achieved": None, "peak": peak, "unit": "GB/s",
+                         "frac": None, "kernel": "k_density_cells + k_convert(kick/drift)"},
+            "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + kick/drift sharded by cell "
+                                   "with NCCL halo exchange" % (n >> 20), "particles_total": n,
+                       "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},
+            "phases_ms": {k: sum(v) / len(v) for k, v in phases.items()},
+            "particles_local": st.n}

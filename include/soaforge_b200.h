@@ -147,15 +147,19 @@ SF_API uint64_t sf_b200_bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
  * records of `src` (full field set, AoS).  One step = gather + `kernels`
  * (comma list of kick,drift) in the dst view's precision + scatter-back of
  * every write set into the AoS, for every record.
- *   mode 0 STREAMED: pinned host memory, chunked cudaMemcpyAsync ring
- *                    (H2D k+1 ∥ compute k ∥ D2H k-1) on 3 streams;
+ *   mode 0 STREAMED: pinned host memory; per chunk only the contiguous field
+ *                    span the kernels touch crosses PCIe (one 2-D DMA, pitch =
+ *                    record) — the reference's narrowed streaming transfers;
  *   mode 1 MANAGED:  host_aos is cudaMallocManaged; prefetch/advise hints and
- *                    in-place conversion on the migrated pages.
+ *                    in-place conversion on the migrated pages;
+ *   mode 2 INPLACE:  pinned host memory, whole records each way (the
+ *                    reference's in-place round trip).
+ * All modes pipeline H2D k+1 ∥ compute k ∥ D2H k-1 over 3 streams.
  * host_soa (optional): when non-NULL the SoA result (dst view, all
  * records) is copied to this host buffer instead of scattering back into
  * the AoS — the end-to-end form of the fused gather+kernel path.
  * metrics[0..4] = {seconds, h2d_bytes, d2h_bytes, chunks, kernel_launches}. */
-enum { SF_MODE_STREAMED = 0, SF_MODE_MANAGED = 1 };
+enum { SF_MODE_STREAMED = 0, SF_MODE_MANAGED = 1, SF_MODE_INPLACE = 2 };
 SF_API sf_status sf_b200_run_host(const sf_view* src, void* host_aos, const sf_view* dst,
                                   const char* kernels, double dt, int math, int mode,
                                   uint64_t chunk_records, void* host_soa, double* metrics);

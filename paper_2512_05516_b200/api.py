@@ -278,13 +278,17 @@ class HostBuffer:
 
 
 def run_host(src_view: View, host: HostBuffer, dst_view: View, kernels: str = "drift", dt: float = 1e-3,
-             math: int = SF_MATH_FP64_EXACT, chunk: int = 1 << 22, soa_out: Optional[HostBuffer] = None) -> dict:
-    """One whole-population step on host-resident AoS (streamed or managed).
+             math: int = SF_MATH_FP64_EXACT, chunk: int = 1 << 21, soa_out: Optional[HostBuffer] = None,
+             mode: Optional[int] = None) -> dict:
+    """One whole-population step on host-resident AoS: mode 0 streamed
+    (narrowed 2-D DMA, pinned), 1 managed (host buffer must be managed),
+    2 in-place (whole records, pinned); default: the host buffer's kind.
     With `soa_out` the SoA result lands in host memory instead of being
     scattered back into the AoS."""
     m = (C.c_double * 5)()
     check(lib().sf_b200_run_host(src_view.handle, host.ptr, dst_view.handle, kernels.encode(), dt, math,
-                                 host.mode, chunk, soa_out.ptr if soa_out is not None else None, m))
+                                 host.mode if mode is None else mode, chunk,
+                                 soa_out.ptr if soa_out is not None else None, m))
     return {"seconds": m[0], "h2d_bytes": int(m[1]), "d2h_bytes": int(m[2]), "chunks": int(m[3]),
             "launches": int(m[4])}
 

@@ -1,21 +1,27 @@
-// Host-resident particle orchestration (C4): the paper's stream-vs-in-place
-// question (pipelines.cpp:231-296, PAPER §6) re-posed for a PCIe-attached
-// B200.
+// Host-resident particle orchestration (C4): the paper's streaming vs
+// in-place question (pipelines.cpp:231-296, §6) re-posed for a
+// PCIe-attached B200.  Three modes, all chunked over 3 rotating streams so
+// the two copy engines and the SMs overlap (H2D k+1 ∥ compute k ∥ D2H k-1):
 //
-//   STREAMED  pinned host AoS, chunked: on each of 3 rotating streams
-//             H2D(chunk) -> fused gather+kernel -> [more kernels on SoA]
-//             -> scatter-merge write sets into the AoS chunk -> D2H(chunk).
-//             The copy engines (H2D, D2H) and the SMs overlap across chunks.
-//   MANAGED   cudaMallocManaged AoS (preferred location: host); per chunk
-//             cudaMemPrefetchAsync to the GPU, the same kernels run in place
-//             on the migrated pages, prefetch back to the host.
+//   STREAMED (0) pinned host AoS; per chunk only the contiguous field span
+//                the kernels touch crosses PCIe, as one 2-D DMA (pitch =
+//                record, width = span): the reference's run_dev_streaming
+//                ships narrowed records (streamed_bytes_one_way,
+//                pipelines.cpp:434-441) — here the narrowing is the DMA's
+//                own stride, no host-side gather.
+//   MANAGED  (1) cudaMallocManaged AoS (preferred location: host); per chunk
+//                cudaMemPrefetchAsync to the GPU, kernels run in place on the
+//                migrated pages, prefetch back.
+//   INPLACE  (2) pinned host AoS, whole records each way (the reference's
+//                run_dev_inplace round trip, inplace_bytes_one_way).
 //
-// Either way the whole record moves each way (88 B/particle at the default
-// schema), conversion happens on the GPU, and the AoS in host memory ends up
-// exactly as the reference's run_dev_inplace would leave it for a DevSoA
-// composition of the same kernels.
+// Per chunk on the device: fused gather + first kernel (k_gather_warp) ->
+// further kernels on the SoA -> either the SoA slice to a host SoA buffer
+// (host_soa != NULL) or scatter-merge of every write set into the AoS chunk
+// and back to the host.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -44,6 +50,18 @@ View with_count(const View& v, uint64_t count) {
     return c;
 }
 
+// AoS view over the contiguous run of fields [lo, hi] (declaration order).
+View span_view(const View& full, int lo, int hi) {
+    View v = full;
+    v.subset.clear();
+    v.fmt.clear();
+    for (int f = lo; f <= hi; ++f) {
+        v.subset.push_back(f);
+        v.fmt.push_back(full.fmt[full.pos_of(f)]);
+    }
+    return v;
+}
+
 }  // namespace
 
 void run_host(const View& src, void* host, const View& dst, const std::string& kernels, double dt, int math, int mode,
@@ -52,28 +70,44 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
     if (src.layout != Layout::AoS || src.subset.size() != src.schema->fields.size())
         throw std::invalid_argument("run_host expects an AoS view over the full field set");
     if (dst.layout != Layout::SoA) throw std::invalid_argument("run_host computes on an SoA view");
-    std::vector<std::string> ks = split_names(kernels);
+    if (mode < 0 || mode > 2) throw std::invalid_argument("unknown host orchestration mode");
+    const std::vector<std::string> ks = split_names(kernels);
     if (ks.empty()) throw std::invalid_argument("no kernels given");
     for (const auto& k : ks)
         if (k != "kick" && k != "drift") throw std::invalid_argument("run_host runs kick and drift");
-    if (chunk == 0) chunk = 1ull << 22;
+    if (chunk == 0) chunk = 1ull << 21;
     chunk = (chunk + 127) / 128 * 128;  // 16-B aligned chunk starts for any record width
     const uint64_t n = src.count;
     const uint64_t rb = src.record_bits();
-    const int slots = 3;
+
+    // the contiguous span of fields the kernels (and the SoA view) touch
+    int lo = int(src.schema->fields.size()), hi = -1;
+    for (int f : dst.subset) lo = std::min(lo, f), hi = std::max(hi, f);
+    for (const auto& k : ks) {
+        const KernelSet* set = src.schema->kernel(k);
+        if (!set) throw std::invalid_argument("no access set declared for kernel '" + k + "'");
+        for (size_t f = 0; f < src.schema->fields.size(); ++f)
+            if (set->touches(src.schema->fields[f].name)) lo = std::min(lo, int(f)), hi = std::max(hi, int(f));
+    }
+    const View dev_view = mode == 0 ? span_view(src, lo, hi) : src;  // layout of the device-side AoS chunk
+    const uint64_t span_off_bits = src.lane_base(lo);
+    const uint64_t span_bits = dev_view.record_bits();
+    if (mode == 0 && ((span_off_bits | span_bits | rb) & 7))
+        throw std::invalid_argument("streamed mode needs a byte-aligned field span (use INPLACE for bit-packed AoS)");
 
     cudaPointerAttributes attr{};
     check_cuda(cudaPointerGetAttributes(&attr, host), "pointer attributes");
-    if (mode == 0 && attr.type != cudaMemoryTypeHost)
-        throw std::invalid_argument("streamed mode needs pinned host memory (sf_b200_host_alloc mode 0)");
+    if (mode != 1 && attr.type != cudaMemoryTypeHost)
+        throw std::invalid_argument("streamed/inplace modes need pinned host memory (sf_b200_host_alloc mode 0)");
     if (mode == 1 && attr.type != cudaMemoryTypeManaged)
         throw std::invalid_argument("managed mode needs cudaMallocManaged memory (sf_b200_host_alloc mode 1)");
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "device");
 
+    const int slots = 3;
     static thread_local std::unique_ptr<DeviceSlots> pool;
-    const size_t aos_bytes = size_t((chunk * rb + 7) / 8);
-    const size_t soa_bytes = size_t(with_count(dst, chunk).total_bytes());
+    const size_t aos_bytes = size_t((chunk * rb + 7) / 8) + 16;
+    const size_t soa_bytes = size_t(with_count(dst, chunk).total_bytes()) + 16;
     if (!pool || pool->aos_bytes < aos_bytes || pool->soa_bytes < soa_bytes) {
         pool.reset(new DeviceSlots());
         pool->aos_bytes = aos_bytes;
@@ -92,10 +126,6 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
     }
     if (mode == 1) {
         const size_t total = size_t((n * rb + 7) / 8);
-        cudaMemLocation loc{};
-        loc.type = cudaMemLocationTypeHost;
-        loc.id = 0;
-        (void)loc;
         check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId), "advise");
         check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetAccessedBy, dev), "advise");
     }
@@ -111,6 +141,7 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
 
     uint64_t h2d = 0, d2h = 0, nchunks = 0;
     const uint64_t launches0 = launch_count();
+    const size_t rbytes = size_t(rb / 8), sbytes = size_t(span_bits / 8), soff = size_t(span_off_bits / 8);
     for (uint64_t r0 = 0; r0 < n; r0 += chunk, ++nchunks) {
         const int s = int(nchunks % slots);
         cudaStream_t st = pool->streams[s];
@@ -118,14 +149,19 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
         const size_t off = size_t(r0 * rb / 8);
         const size_t bytes = size_t((cnt * rb + 7) / 8);
         uint8_t* hchunk = static_cast<uint8_t*>(host) + off;
-        void* aos = mode == 0 ? pool->aos[s] : static_cast<void*>(hchunk);
+        void* aos = mode == 1 ? static_cast<void*>(hchunk) : pool->aos[s];
         if (mode == 0) {
+            check_cuda(cudaMemcpy2DAsync(aos, sbytes, hchunk + soff, rbytes, sbytes, cnt, cudaMemcpyHostToDevice, st),
+                       "H2D 2D");
+            h2d += sbytes * cnt;
+        } else if (mode == 2) {
             check_cuda(cudaMemcpyAsync(aos, hchunk, bytes, cudaMemcpyHostToDevice, st), "H2D");
+            h2d += bytes;
         } else {
             check_cuda(cudaMemPrefetchAsync(hchunk, bytes, dev, st), "prefetch");
+            h2d += bytes;
         }
-        h2d += bytes;
-        const View sv = with_count(src, cnt), dv = with_count(dst, cnt);
+        const View sv = with_count(dev_view, cnt), dv = with_count(dst, cnt);
         gather(sv, aos, dv, pool->soa[s], ks[0].c_str(), dt, math, st);
         for (size_t k = 1; k < ks.size(); ++k) run_kernel(dv, pool->soa[s], ks[k], dt, 1, 0, math, st);
         if (host_soa) {
@@ -143,11 +179,16 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
         } else {
             for (const auto& k : ks) scatter_merge(dv, pool->soa[s], sv, aos, k, st);
             if (mode == 0) {
+                check_cuda(cudaMemcpy2DAsync(hchunk + soff, rbytes, aos, sbytes, sbytes, cnt, cudaMemcpyDeviceToHost, st),
+                           "D2H 2D");
+                d2h += sbytes * cnt;
+            } else if (mode == 2) {
                 check_cuda(cudaMemcpyAsync(hchunk, aos, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+                d2h += bytes;
             } else {
                 check_cuda(cudaMemPrefetchAsync(hchunk, bytes, cudaCpuDeviceId, st), "prefetch");
+                d2h += bytes;
             }
-            d2h += bytes;
         }
     }
     for (int s = 0; s < slots; ++s) {

@@ -10,5 +10,5 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench exit $?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/launches.log 2>&1
 echo "ncu1 exit $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gather_tiled -s 5 -c 1 -o gpurun_out/prof_gather python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gather -s 5 -c 1 -o gpurun_out/prof_gather python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1
 echo "ncu2 exit $?"

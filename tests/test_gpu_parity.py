@@ -305,25 +305,47 @@ def test_density_buffer_fp64_matches_oracle_random():
 
 
 # ----------------------------------------------------------- host orchestration
-@pytest.mark.parametrize("mode", [0, 1])
-def test_run_host_streamed_and_managed(mode):
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("subset", ["all", "kick"])
+def test_run_host_streamed_managed_inplace(mode, subset):
     n = 100000
     ob, P, _ = default_aos(n=n)
     aos_v = api.View(P, n, "aos")
-    hb = api.HostBuffer(aos_v.nbytes, mode)
+    hb = api.HostBuffer(aos_v.nbytes, 1 if mode == 1 else 0)
     hb.numpy()[:] = ob.data
-    dst = api.View(P, n, "soa", "kick", 16)
-    dst_all = api.View(P, n, "soa", None, 16)
-    m = api.run_host(aos_v, hb, dst_all, "kick,drift", 1e-3, chunk=16384)
-    assert m["h2d_bytes"] == aos_v.nbytes and m["d2h_bytes"] == aos_v.nbytes
+    kernels = "kick,drift" if subset == "all" else "kick"
+    dst = api.View(P, n, "soa", None if subset == "all" else "kick", 16)
+    m = api.run_host(aos_v, hb, dst, kernels, 1e-3, chunk=16384, mode=mode)
+    if mode == 0 and subset == "kick":
+        assert m["h2d_bytes"] == n * 52 == m["d2h_bytes"]  # span v..du (bytes 32..83) of the 88-B record
+    else:
+        assert m["h2d_bytes"] == aos_v.nbytes and m["d2h_bytes"] == aos_v.nbytes
     # oracle: T16 SoA of everything, kick then drift, merge v,u,x back (exact widen)
     S = O.default_schema()
     soa = O.transform(ob, "soa", fmts=[O.NATIVE(16) if f.is_float else O.OR_I64 for f in S.fields])
-    soa = apply_kernel(apply_kernel(soa, "kick"), "drift")
-    O.merge_into(soa, ob, ["v", "u", "x"])
+    soa = apply_kernel(soa, "kick")
+    if subset == "all":
+        soa = apply_kernel(soa, "drift")
+    O.merge_into(soa, ob, ["v", "u", "x"] if subset == "all" else ["v", "u"])
     np.testing.assert_array_equal(hb.numpy(), ob.data)
-    del dst
     hb.free()
+
+
+def test_run_host_streamed_soa_out_drift_span():
+    """C2 end to end: only bytes 0..43 (x, id, v) of each record cross PCIe."""
+    n = 50000
+    ob, P, src = default_aos(n=n)
+    aos_v = api.View(P, n, "aos")
+    hb = api.HostBuffer(aos_v.nbytes, 0)
+    hb.numpy()[:] = ob.data
+    v = api.View(P, n, "soa", "drift", 16)
+    hs = api.HostBuffer(v.nbytes, 0)
+    m = api.run_host(aos_v, hb, v, "drift", 1e-3, chunk=8192, soa_out=hs)
+    assert m["h2d_bytes"] == n * 44 and m["d2h_bytes"] == n * 12
+    want = api.gather_kernel(src, v, "drift", 1e-3)
+    np.testing.assert_array_equal(hs.numpy()[: v.nbytes], host(want))
+    hb.free()
+    hs.free()
 
 
 @pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
