@@ -5,7 +5,7 @@ binary16 storage of position/velocity, fused into drift, 16M particles.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 One step = one pass of the hot path over the whole 16M-particle population:
-the default 88-B AoS (f64 x, f32 v, ...) in HBM -> k_gather_tiled (TMA-staged
+the default 88-B AoS (f64 x, f32 v, ...) in HBM -> k_gather_warp (TMA-staged
 record tiles, RNE narrowing to binary16, drift x += v*dt in binary64) ->
 SoA binary16 {x', v}.  Under torchrun every rank runs its own 16M particles
 (weak scaling: particles shard with no data-path collective); timing is the
@@ -244,11 +244,11 @@ def b200_arm(args):
             hb_np[b:e] = src.data[b:e].cpu().numpy()
         hs = api.HostBuffer(dst_v.nbytes, 0)
         for _ in range(max(1, min(args.warmup, 2))):
-            api.run_host(aos_v, hb, dst_v, "drift", 1e-3, chunk=args.chunk, soa_out=hs)
+            api.run_host(aos_v, hb, dst_v, "drift", 1e-3, chunk=args.chunk, soa_out=hs, mode=2)
         barrier()
         secs = []
         for _ in range(args.e2e_steps):
-            m = api.run_host(aos_v, hb, dst_v, "drift", 1e-3, chunk=args.chunk, soa_out=hs)
+            m = api.run_host(aos_v, hb, dst_v, "drift", 1e-3, chunk=args.chunk, soa_out=hs, mode=2)
             secs.append(m["seconds"])
         s_t = torch.tensor([sum(secs) / len(secs)], device="cuda", dtype=torch.float64)
         if dist is not None:
@@ -258,8 +258,8 @@ def b200_arm(args):
         ok = bool(torch.equal(got, out.data[: dst_v.nbytes]))
         e2e = {"value": n * world / float(s_t.item()), "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"],
                "d2h_bytes_per_step": m["d2h_bytes"], "chunk_particles": args.chunk, "matches_device_result": ok,
-               "path": "sf_b200_run_host(streamed): pinned AoS -> 2-D DMA of the x..v span (44 of 88 B) || "
-                       "k_gather_warp || D2H SoA"}
+               "path": "sf_b200_run_host(mode 2): pinned AoS, whole records H2D || k_gather_warp (fused drift) || "
+                       "D2H SoA, 3-stream chunk pipeline"}
         hb.free()
         hs.free()
 

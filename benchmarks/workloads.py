@@ -124,10 +124,11 @@ def c3(args, peak, peak_kind):
         msd, msb = sum(t) / len(t), sum(tb) / len(tb)
         # pairs inside the support, for pairs/s
         pairs = None
-        if name == "fp32":
-            sample = x[:4096]
-            d = torch.cdist(sample.double(), x.double())
-            pairs = float((d < 2 * h).sum().item()) / 4096 * n
+        if name == "fp32":  # neighbours inside 2h, sampled (256 particles x all, in chunks)
+            cnt = 0
+            for b in range(0, n, 1 << 20):
+                cnt += int((torch.cdist(x[:256], x[b:b + (1 << 20)]) < 2 * h).sum().item())
+            pairs = cnt / 256 * n
         bytes_pp = {"fp32": 24, "fp16": 12, "bf16": 12}[name]
         out[name] = {"density_ms": msd, "bin_ms": msb, "value": n / (msd * 1e-3),
                      "hbm_GBps_algorithmic": bytes_pp * n / (msd * 1e-3) / 1e9,

@@ -70,14 +70,4 @@ void write_output(const RunConfig& c, const std::string& text) {
     o << text;
 }
 
-static std::string pending(const char* what) {
-    throw std::runtime_error(std::string(what) + ": GPU command not yet available in this build");
-}
-
-std::string cmd_bench_transform(const RunConfig&) { return pending("bench transform"); }
-std::string cmd_bench_kernels(const RunConfig&) { return pending("bench kernels"); }
-std::string cmd_bench_pipeline(const RunConfig&) { return pending("bench pipeline"); }
-std::string cmd_study_truncation(const RunConfig&) { return pending("study truncation"); }
-std::string cmd_validate(const RunConfig&, int&) { return pending("validate"); }
-
 }  // namespace sfb

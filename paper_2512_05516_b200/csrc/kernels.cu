@@ -320,6 +320,74 @@ __device__ __forceinline__ void stream_fast(const uint8_t* tile, uint32_t rbytes
     }
 }
 
+// Hot loop of the fast path: arity unrolled at compile time, no NaN selects.
+// Any NaN operand (or a NaN result, i.e. inf - inf) raises `bad`; the caller
+// then redoes the warp's slice through stream_fast, which reproduces the
+// reference's NaN payloads exactly.  Finite lanes give identical bits on
+// both paths.
+template <int SB, int DB, int AB, int AR>
+__device__ __forceinline__ bool stream_hot(const uint8_t* tile, uint32_t rbytes, const GStream& g, uint32_t lane,
+                                           uint32_t recs, double dt, uint8_t math, uint8_t* out) {
+    constexpr int sb = Ieee<SB>::w / 8, db = Ieee<DB>::w / 8;
+    bool bad = false;
+    const bool clamp = g.op == OP_AXPY_CLAMP0;
+    for (uint32_t r = lane; r < recs; r += 32) {
+        const uint8_t* xr = tile + r * rbytes + (g.src_off >> 3);
+        uint64_t v[AR];
+#pragma unroll
+        for (int l = 0; l < AR; ++l) {
+            const uint64_t s = lds<SB>(xr + l * sb);
+            bad |= Ieee<SB>::nan(s);
+            if constexpr (SB == DB) v[l] = s;
+            else if constexpr (SB == B_F32 && DB == B_F16) {
+                const __half h = __float2half_rn(bits_to_f32(uint32_t(s)));
+                v[l] = *reinterpret_cast<const uint16_t*>(&h);
+            } else if constexpr (SB == B_F32 && DB == B_BF16) {
+                const __nv_bfloat16 h = __float2bfloat16_rn(bits_to_f32(uint32_t(s)));
+                v[l] = *reinterpret_cast<const uint16_t*>(&h);
+            } else {
+                v[l] = Ieee<DB>::from(Ieee<SB>::f64(s));
+            }
+        }
+        if constexpr (AB >= 0) {
+            constexpr int ab = Ieee<AB>::w / 8;
+            const uint8_t* yr = tile + r * rbytes + (g.aux_off >> 3);
+#pragma unroll
+            for (int l = 0; l < AR; ++l) {
+                const uint64_t ys = lds<AB>(yr + l * ab);
+                bad |= Ieee<AB>::nan(ys);
+                const uint64_t yq = (AB == DB) ? ys : Ieee<DB>::from(Ieee<AB>::f64(ys));
+                double res;
+                if (math == MATH_FP64_EXACT) {
+                    res = __dadd_rn(Ieee<DB>::f64(v[l]), __dmul_rn(Ieee<DB>::f64(yq), dt));
+                } else {
+                    res = double(__fadd_rn(float(Ieee<DB>::f64(v[l])), __fmul_rn(float(Ieee<DB>::f64(yq)), float(dt))));
+                }
+                bad |= isnan(res);
+                if (clamp && res < 0.0) res = 0.0;
+                v[l] = Ieee<DB>::from(res);
+            }
+        }
+        uint8_t* o = out + r * AR * db;
+#pragma unroll
+        for (int l = 0; l < AR; ++l) {
+            if constexpr (db == 8) *reinterpret_cast<uint64_t*>(o + l * 8) = v[l];
+            else if constexpr (db == 4) *reinterpret_cast<uint32_t*>(o + l * 4) = uint32_t(v[l]);
+            else *reinterpret_cast<uint16_t*>(o + l * 2) = uint16_t(v[l]);
+        }
+    }
+    return bad;
+}
+
+template <int SB, int DB, int AB>
+__device__ __forceinline__ void stream_fast_dispatch(const uint8_t* tile, uint32_t rbytes, const GStream& g,
+                                                     uint32_t lane, uint32_t recs, double dt, uint8_t math,
+                                                     uint8_t* out) {
+    const bool bad = g.arity == 3 ? stream_hot<SB, DB, AB, 3>(tile, rbytes, g, lane, recs, dt, math, out)
+                                  : stream_hot<SB, DB, AB, 1>(tile, rbytes, g, lane, recs, dt, math, out);
+    if (__any_sync(0xffffffffu, bad)) stream_fast<SB, DB, AB>(tile, rbytes, g, lane, recs, dt, math, out);
+}
+
 // Generic path: any bit offset / width / truncated format, via funnel shifts.
 __device__ __forceinline__ void stream_generic(const uint8_t* tile, uint32_t record_bits, const GStream& g,
                                                uint32_t lane, uint32_t recs, double dt, uint8_t math, uint8_t* out) {
@@ -348,7 +416,7 @@ __device__ __forceinline__ void stream_dispatch(const uint8_t* tile, const Gathe
     switch (g.fast) {
 #define SFB_CASE(SBI, SB, DBI, DB, ABI, AB)                                    \
     case 1 + SBI * 12 + DBI * 3 + ABI:                                         \
-        stream_fast<SB, DB, AB>(tile, rbytes, g, lane, recs, P.dt, P.math, out); \
+        stream_fast_dispatch<SB, DB, AB>(tile, rbytes, g, lane, recs, P.dt, P.math, out); \
         return;
 #define SFB_DST(SBI, SB, DBI, DB)        \
     SFB_CASE(SBI, SB, DBI, DB, 0, -1)    \
@@ -491,6 +559,80 @@ __global__ void k_density_buffer(const __grid_constant__ DensityPlan P, uint8_t*
     st_bits_global(buf, P.rho.base + gi * P.rho.stride, P.rho.fmt.width, encode_lane(acc, P.rho.fmt), ba);
 }
 
+// ----------------------------------------------------------------- force
+// dw_dr (sph.cpp:26-33), left-to-right binary64.
+__device__ __forceinline__ double dwdr_exact(double r, double h) {
+    const double q = __ddiv_rn(r, h);
+    if (q >= 2.0) return 0.0;
+    const double norm = __ddiv_rn(kInvPi, __dmul_rn(__dmul_rn(__dmul_rn(h, h), h), h));
+    if (q < 1.0) return __dmul_rn(norm, __dadd_rn(__dmul_rn(-3.0, q), __dmul_rn(__dmul_rn(2.25, q), q)));
+    const double t = __dsub_rn(2.0, q);
+    return __dmul_rn(norm, __dmul_rn(__dmul_rn(-0.75, t), t));
+}
+
+__device__ int g_force_degenerate;  // set when a particle has rho == 0 (domain_error)
+
+// force_kernel (sph.cpp:201-245): symmetric pressure force and du, j ascending,
+// self pair skipped; PerAccess quantizes a after every neighbour.
+__global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf) {
+    extern __shared__ double sf[];
+    const uint32_t bs = P.bs;
+    double* sx = sf;            // 3 bs
+    double* sv = sf + 3 * bs;   // 3 bs
+    double* sm = sf + 6 * bs;
+    double* sh = sf + 7 * bs;
+    double* srho = sf + 8 * bs;
+    double* sP = sf + 9 * bs;
+    const uint64_t b0 = uint64_t(blockIdx.x) * bs;
+    const uint32_t i = threadIdx.x;
+    const uint64_t gi = b0 + i;
+    for (int l = 0; l < 3; ++l) {
+        sx[3 * i + l] = ld_lane(buf, P.x, gi, l);
+        sv[3 * i + l] = ld_lane(buf, P.v, gi, l);
+    }
+    sm[i] = ld_lane(buf, P.m, gi, 0);
+    sh[i] = ld_lane(buf, P.h, gi, 0);
+    srho[i] = ld_lane(buf, P.rho, gi, 0);
+    sP[i] = ld_lane(buf, P.P, gi, 0);
+    __syncthreads();
+    const double rho_i = srho[i];
+    if (rho_i == 0.0) atomicOr(&g_force_degenerate, 1);
+    const double pi_rho2 = __ddiv_rn(sP[i], __dmul_rn(rho_i, rho_i));
+    double acc[3] = {0.0, 0.0, 0.0}, compr = 0.0;
+    for (uint32_t j = 0; j < bs; ++j) {
+        if (j == i) continue;
+        const double d0 = __dsub_rn(sx[3 * i], sx[3 * j]), d1 = __dsub_rn(sx[3 * i + 1], sx[3 * j + 1]),
+                     d2 = __dsub_rn(sx[3 * i + 2], sx[3 * j + 2]);
+        const double hij = __dmul_rn(0.5, __dadd_rn(sh[i], sh[j]));
+        const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+        if (r != 0.0) {
+            const double s = __ddiv_rn(dwdr_exact(r, hij), r);
+            g0 = __dmul_rn(s, d0);
+            g1 = __dmul_rn(s, d1);
+            g2 = __dmul_rn(s, d2);
+        }
+        const double mj = sm[j], rho_j = srho[j];
+        if (rho_j == 0.0) atomicOr(&g_force_degenerate, 1);
+        const double pf = __dadd_rn(pi_rho2, __ddiv_rn(sP[j], __dmul_rn(rho_j, rho_j)));
+        const double mpf = __dmul_rn(mj, pf);
+        acc[0] = __dsub_rn(acc[0], __dmul_rn(mpf, g0));
+        acc[1] = __dsub_rn(acc[1], __dmul_rn(mpf, g1));
+        acc[2] = __dsub_rn(acc[2], __dmul_rn(mpf, g2));
+        const double dv0 = __dsub_rn(sv[3 * i], sv[3 * j]), dv1 = __dsub_rn(sv[3 * i + 1], sv[3 * j + 1]),
+                     dv2 = __dsub_rn(sv[3 * i + 2], sv[3 * j + 2]);
+        compr = __dadd_rn(compr, __dmul_rn(mj, __dadd_rn(__dadd_rn(__dmul_rn(dv0, g0), __dmul_rn(dv1, g1)),
+                                                         __dmul_rn(dv2, g2))));
+        if (P.per_access)
+            for (int l = 0; l < 3; ++l) acc[l] = dec(encode_lane(acc[l], P.a.fmt), P.a.fmt);
+    }
+    for (int l = 0; l < 3; ++l)
+        st_bits_global(buf, P.a.base + gi * P.a.stride + uint64_t(l) * P.a.fmt.width, P.a.fmt.width,
+                       encode_lane(acc[l], P.a.fmt), P.byte_aligned);
+    st_bits_global(buf, P.du.base + gi * P.du.stride, P.du.fmt.width, encode_lane(__dmul_rn(pi_rho2, compr), P.du.fmt),
+                   P.byte_aligned);
+}
+
 // ----------------------------------------------------------------- launchers
 static int g_num_sms = 0;
 static int num_sms() {
@@ -536,6 +678,23 @@ cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_byt
     k_gather_warp<<<blocks, warps * 32, smem, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst),
                                                    src_bytes);
     return cudaGetLastError();
+}
+
+cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate) {
+    if (p.count == 0) {
+        *degenerate = false;
+        return cudaSuccess;
+    }
+    int zero = 0, flag = 0;
+    cudaError_t e = cudaMemcpyToSymbolAsync(g_force_degenerate, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    k_force_buffer<<<unsigned(p.count / p.bs), p.bs, 10 * p.bs * sizeof(double), st>>>(p, static_cast<uint8_t*>(buf));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = cudaMemcpyFromSymbolAsync(&flag, g_force_degenerate, sizeof(int), 0, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);
+    *degenerate = flag != 0;
+    return e;
 }
 
 cudaError_t launch_density_buffer(const DensityPlan& p, void* buf, cudaStream_t st) {

@@ -79,4 +79,13 @@ struct DensityPlan {
     uint8_t per_access = 0;
 };
 
+// ---- SPH force over 64-particle neighbour buffers (sph.cpp:201-245) ---------
+struct ForcePlan {
+    Lanes x, v, m, h, rho, P, a, du;
+    uint64_t count = 0;
+    uint32_t bs = 64;
+    uint8_t per_access = 0;
+    uint8_t byte_aligned = 1;  // a/du stores: plain or bit-level atomics
+};
+
 }  // namespace sfb

@@ -102,7 +102,24 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
         count_launches(1);
         return;
     }
+    if (kernel == "force") {
+        if (math != MATH_FP64_EXACT) throw std::invalid_argument("buffer-mode force is binary64 (reference semantics)");
+        const ForcePlan f = plan_force(v, bs, per_access);
+        bool degenerate = false;
+        check_cuda(launch_force_buffer(f, p, st, &degenerate), "force launch");
+        count_launches(1);
+        if (degenerate) throw std::domain_error("force: degenerate state, rho == 0");
+        return;
+    }
     if (bs == 0 || v.count % bs != 0) throw std::invalid_argument("buffer size must divide the particle count");
+    if (kernel == "identity") {  // sph.cpp:266-270: x = Q(x), a bitwise no-op on stored lanes
+        const int x = v.pos_of("x");
+        if (x < 0) throw std::invalid_argument("field 'x' is not present in the buffer view");
+        const ConvertPlan cp = plan_convert(v, v, {v.subset[x]});
+        check_cuda(launch_convert(cp, p, p, st), "identity launch");
+        count_launches(1);
+        return;
+    }
     const KernelPlan kp = plan_kernel(v, kernel, dt, math);
     check_cuda(launch_convert(kp, p, p, st), "kernel launch");
     count_launches(1);

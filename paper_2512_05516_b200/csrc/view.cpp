@@ -245,3 +245,25 @@ DensityPlan plan_density(const View& v, uint64_t bs, int per_access) {
 }
 
 }  // namespace sfb
+
+namespace sfb {
+
+ForcePlan plan_force(const View& v, uint64_t bs, int per_access) {
+    ForcePlan p;
+    const char* need[] = {"x", "v", "m", "h", "rho", "P", "a", "du"};
+    Lanes* slot[] = {&p.x, &p.v, &p.m, &p.h, &p.rho, &p.P, &p.a, &p.du};
+    for (int k = 0; k < 8; ++k) {
+        const int pos = v.pos_of(need[k]);
+        if (pos < 0) throw std::invalid_argument(std::string("field '") + need[k] + "' is not present in the buffer view");
+        *slot[k] = v.lanes(pos);
+    }
+    if (bs == 0 || bs > 1024 || v.count % bs != 0)
+        throw std::invalid_argument("buffer size must divide the particle count (and be <= 1024)");
+    p.count = v.count;
+    p.bs = uint32_t(bs);
+    p.per_access = uint8_t(per_access != 0);
+    p.byte_aligned = v.byte_aligned();
+    return p;
+}
+
+}  // namespace sfb

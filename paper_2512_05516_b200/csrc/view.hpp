@@ -56,5 +56,6 @@ KernelPlan plan_kernel(const View& v, const std::string& kernel, double dt, int 
 GatherPlan plan_gather_fused(const View& src, const View& dst, const std::string& kernel, double dt,
                              int math);
 DensityPlan plan_density(const View& v, uint64_t buffer_size, int per_access);
+ForcePlan plan_force(const View& v, uint64_t buffer_size, int per_access);
 
 }  // namespace sfb

@@ -79,10 +79,11 @@ def pipeline():
         nat = R.op(aos, "unpack")
         soa = R.op(nat, "aos_to_soa")
         rec["soa_full"] = R.checksum(soa)
-        for k in ["drift", "kick", "density"]:
+        for k in ["drift", "kick", "density", "force", "density,force"]:
             for layout, buf in [("aos", nat), ("soa", soa)]:
                 h = R.L.ref_buf_clone(buf)
-                R.run_kernel(h, k, 64, dt)
+                for kk in k.split(","):
+                    R.run_kernel(h, kk, 64, dt)
                 back = R.op(h, "soa_to_aos") if layout == "soa" else R.L.ref_buf_clone(h)
                 packed = R.op(back, "pack")
                 rec[f"{k}_{layout}"] = R.checksum(packed)
@@ -92,6 +93,11 @@ def pipeline():
         R.run_kernel(h, "density", 64, dt, per_access=True)
         packed = R.op(h, "pack")
         rec["density_aos_peraccess"] = R.checksum(packed)
+        R.free(h, packed)
+        h = R.L.ref_buf_clone(nat)
+        R.run_kernel(h, "force", 64, dt, per_access=True)
+        packed = R.op(h, "pack")
+        rec["force_aos_peraccess"] = R.checksum(packed)
         R.free(h, packed, aos, nat, soa)
         out["sweeps"][name] = {k: f"{v:016x}" for k, v in rec.items()}
     # north-star composition: default AoS -> T-bit store -> narrow drift -> SoA -> drift -> merge

@@ -1,0 +1,99 @@
+"""The reference's batch commands (sf_run_*) through libsoaforge_b200.so,
+against the same commands of the unmodified reference library
+(oracle/_ref/libsoaforge_ref.so, test_capi.cpp semantics): identical CSV
+checksum columns, validate PASS/fault behaviour, truncation anchor row."""
+import ctypes as C
+import os
+
+import pytest
+
+import oracle as O
+from paper_2512_05516_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+REF_SO = os.path.join(os.path.dirname(O.__file__), "_ref", "libsoaforge_ref.so")
+
+
+def _bind(lib):
+    for name in ["sf_run_bench_kernels", "sf_run_bench_pipeline", "sf_run_study_truncation", "sf_run_validate"]:
+        getattr(lib, name).argtypes = [C.c_void_p, C.POINTER(C.c_char_p)]
+        getattr(lib, name).restype = C.c_int
+    lib.sf_config_create.argtypes = [C.POINTER(C.c_void_p)]
+    lib.sf_config_set_int.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+    lib.sf_config_set_string.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
+    lib.sf_config_destroy.argtypes = [C.c_void_p]
+    lib.sf_last_error.restype = C.c_char_p
+    return lib
+
+
+def run(lib, cmd, ints=(), strs=()):
+    cfg = C.c_void_p()
+    assert lib.sf_config_create(C.byref(cfg)) == 0
+    for k, v in ints:
+        assert lib.sf_config_set_int(cfg, k.encode(), v) == 0
+    for k, v in strs:
+        assert lib.sf_config_set_string(cfg, k.encode(), v.encode()) == 0
+    out = C.c_char_p()
+    st = getattr(lib, cmd)(cfg, C.byref(out))
+    text = out.value.decode() if out.value else ""
+    lib.sf_config_destroy(cfg)
+    return st, text
+
+
+def csv_rows(text):
+    lines = [l for l in text.splitlines() if l and not l.startswith("#")]
+    head = lines[0].split(",")
+    return [dict(zip(head, l.split(","))) for l in lines[1:]]
+
+
+@pytest.fixture(scope="module")
+def libs():
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    return _bind(C.CDLL(L.LIB_PATH)), _bind(C.CDLL(REF_SO))
+
+
+def test_bench_kernels_checksums_match_reference(libs):
+    ours, ref = libs
+    args = dict(ints=[("particles", 1024), ("threads", 2)], strs=[("precision", "64,32,16,20")])
+    s1, t1 = run(ours, "sf_run_bench_kernels", **args)
+    s2, t2 = run(ref, "sf_run_bench_kernels", **args)
+    assert s1 == 0 and s2 == 0, L.lib().sf_last_error()
+    r1, r2 = csv_rows(t1), csv_rows(t2)
+    assert len(r1) == len(r2) == 4 * 4 * 2
+    for a, b in zip(r1, r2):
+        assert (a["kernel"], a["layout"], a["precision"]) == (b["kernel"], b["layout"], b["precision"])
+        assert a["checksum"] == b["checksum"], (a, b)
+
+
+def test_bench_pipeline_checksums_match_reference(libs):
+    ours, ref = libs
+    args = dict(ints=[("particles", 256), ("threads", 1)], strs=[("precision", "32,16")])
+    s1, t1 = run(ours, "sf_run_bench_pipeline", **args)
+    s2, t2 = run(ref, "sf_run_bench_pipeline", **args)
+    assert s1 == 0 and s2 == 0
+    r1, r2 = csv_rows(t1), csv_rows(t2)
+    assert len(r1) == len(r2) == 2 * 8 * 2
+    for a, b in zip(r1, r2):
+        assert (a["variant"], a["mode"]) == (b["variant"], b["mode"])
+        assert a["checksum"] == b["checksum"], (a, b)
+
+
+def test_validate_and_fault(libs):  # test_capi.cpp:72-87
+    ours, _ = libs
+    st, rep = run(ours, "sf_run_validate", ints=[("particles", 128), ("threads", 2)])
+    assert st == 0, rep
+    assert "PASS" in rep and "FAIL" not in rep
+    st, rep = run(ours, "sf_run_validate", ints=[("particles", 128), ("threads", 2), ("fault", 1)])
+    assert st == L.SF_CHECK_FAILED
+    assert "FAIL cross-variant-checksums" in rep
+
+
+def test_truncation_study(libs):  # test_capi.cpp:89-101
+    ours, ref = libs
+    args = dict(ints=[("particles", 256), ("threads", 2)], strs=[("precision", "64,32,16")])
+    st, text = run(ours, "sf_run_study_truncation", **args)
+    assert st == 0
+    assert text.startswith("# soaforge v") and "\n64,0,0\n" in text
+    _, rtext = run(ref, "sf_run_study_truncation", **args)
+    assert text == rtext  # binary64 density+force: every digit agrees

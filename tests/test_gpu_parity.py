@@ -101,14 +101,16 @@ def test_kernel_sweep_goldens(name):
     soa = api.gather(aos, api.View(P, n, "soa", None, api.SF_PREC_NATIVE))
     assert csum(soa) == want["soa_full"]
     packed_view = api.View(P, n, "aos")
-    for k in ["drift", "kick", "density"]:
+    for k in ["drift", "kick", "density", "force", "density,force"]:
         for layout, buf in [("aos", nat), ("soa", soa)]:
             work = api.PackedBuffer(buf.view, buf.data.clone())
-            api.run_kernel(work, k, G["dt"])
+            for kk in k.split(","):
+                api.run_kernel(work, kk, G["dt"])
             assert csum(api.convert(work, packed_view)) == want[f"{k}_{layout}"], (k, layout)
-    work = api.PackedBuffer(nat.view, nat.data.clone())
-    api.run_kernel(work, "density", G["dt"], per_access=True)
-    assert csum(api.convert(work, packed_view)) == want["density_aos_peraccess"]
+    for k in ["density", "force"]:
+        work = api.PackedBuffer(nat.view, nat.data.clone())
+        api.run_kernel(work, k, G["dt"], per_access=True)
+        assert csum(api.convert(work, packed_view)) == want[f"{k}_aos_peraccess"], k
 
 
 # ----------------------------------------------------------- codec coverage
@@ -286,6 +288,19 @@ def test_density_cells_vs_oracle(prec):
     cs_h, perm_h = cs.cpu().numpy(), perm.cpu().numpy()
     assert cs_h[-1] == n and np.all(np.diff(cs_h) >= 0)
     assert sorted(perm_h.tolist()) == list(range(n))
+
+
+def test_force_degenerate_state_is_an_error():
+    """force with rho == 0 raises like the reference's std::domain_error."""
+    n = 128
+    ics = O.random_ics(n, 9)
+    ics["rho"][:] = 0.0
+    S = schema_for(64)
+    ob = O.store_state(ics, S)
+    P = api.Schema(S.text())
+    buf = dev(ob, api.View(P, n, "aos"))
+    with pytest.raises(api.L.SfError, match="rho == 0"):
+        api.run_kernel(buf, "force", 1e-3, 64)
 
 
 def test_density_buffer_fp64_matches_oracle_random():
