@@ -106,20 +106,22 @@ def c3(args, peak, peak_kind):
     x = torch.rand(n, 3, generator=g, device="cuda", dtype=torch.float32)
     m = torch.full((n,), 1.0 / n, device="cuda")
     hh = torch.full((n,), h, device="cuda")
-    dims = (nc, nc, nc)
+    refine = 2                      # binning cells of side 1/(2 nc) >= h, searched with reach 2
+    fine = cell / refine
+    dims = (nc * refine,) * 3
     out = {}
     for name, prec, dt in (("fp32", api.SF_PREC_NATIVE, torch.float32), ("fp16", 16, torch.float16),
                            ("bf16", api.SF_PREC_BF16, torch.bfloat16)):
         xs, ms_, hs = x.to(dt), m.to(dt), hh.to(dt)
-        cs, perm = api.bin_particles(xs.float().contiguous(), (0, 0, 0), cell, dims)
-        p = perm.long()
-        xs, ms_, hs = xs[p].contiguous(), ms_[p].contiguous(), hs[p].contiguous()
+        xf = xs.float().contiguous()
+        cs, perm = api.bin_particles(xf, (0, 0, 0), fine, dims)
         rho = torch.empty(n, device="cuda")
-        fn = lambda: api.density_cells(xs, ms_, hs, cs, dims, prec=prec, rho=rho)  # noqa: E731
+        fn = lambda: api.density_cells(xs, ms_, hs, cs, perm, (0, 0, 0), fine, dims, reach=refine,  # noqa: E731
+                                       prec=prec, rho=rho)
         for _ in range(args.warmup):
             fn()
         t = timed_each(fn, max(3, args.steps // 5))
-        tb = timed_each(lambda: api.bin_particles(x, (0, 0, 0), cell, dims, cell_start=cs, perm=perm),
+        tb = timed_each(lambda: api.bin_particles(xf, (0, 0, 0), fine, dims, cell_start=cs, perm=perm),
                         max(3, args.steps // 5))
         msd, msb = sum(t) / len(t), sum(tb) / len(tb)
         # pairs inside the support, for pairs/s
@@ -142,7 +144,8 @@ def c3(args, peak, peak_kind):
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": rl,
             "config": {"workload": "C3 (BASELINE configs[2]): SPH density, cell-linked, 4M uniform particles, "
                                    "SoA fp32 vs fp16 vs bf16", "particles": n, "h": h, "cells_per_side": nc,
-                       "value_is": "fp32 density kernel; binning reported separately"},
+                       "binning_cells_per_side": nc * refine, "reach": refine,
+                       "value_is": "fp32 density (pack + pair kernels); binning reported separately"},
             "kernels": out}
 
 

@@ -124,16 +124,18 @@ SF_API sf_status sf_b200_scatter_merge(const sf_view* src, const void* src_dev, 
 SF_API sf_status sf_b200_run_kernel(const sf_view* view, void* dev, const char* kernel, double dt,
                                     uint64_t buffer_size, int per_access, int math, void* stream);
 
-/* Cell-linked density over SoA streams (new algorithm).
- * x: 3*n, m, h: n, in `prec` (SF_PREC_NATIVE -> fp32 streams, 16 -> fp16,
- * SF_PREC_BF16 -> bf16); rho_out: n fp32.  Particles must already be sorted
- * by cell (sf_b200_bin_particles); cell_start has ncell+1 entries.
- * The grid has nx*ny*nz cells of side `cell` starting at lo[3]; rows
- * [x_lo_ghost, ...) allow a slab with ghost layers (multi-GPU). */
+/* Cell-linked density (new algorithm).  x: 3*n, m, h: n lanes
+ * in `prec` (SF_PREC_NATIVE -> fp32 streams, 16 -> fp16, SF_PREC_BF16 ->
+ * bf16), in particle order; perm[n] / cell_start[ncell+1] from
+ * sf_b200_bin_particles over the same grid (lo[3] host floats, cell side,
+ * nx*ny*nz cells, x-major).  reach = neighbour cells per side searched
+ * (1 when cell >= 2h, 2 when cell >= h).  Only particles in x-layers
+ * [own_x0, own_x1) are computed (layers outside are ghosts, multi-GPU);
+ * rho_out[i] (fp32, particle order) is written for those particles. */
 SF_API sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int prec,
-                                       uint64_t n, const int32_t* cell_start, int nx, int ny,
-                                       int nz, int own_x0, int own_x1, float* rho_out,
-                                       void* stream);
+                                       uint64_t n, const int32_t* perm, const int32_t* cell_start,
+                                       const float* lo, float cell, int nx, int ny, int nz, int reach,
+                                       int own_x0, int own_x1, float* rho_out, void* stream);
 /* Counting sort of particles into cells (x-major cell id), stable in
  * particle index: writes perm[n] (sorted position -> original index) and
  * cell_start[ncell+1].  scratch must hold sf_b200_bin_scratch_bytes(). */

@@ -240,15 +240,20 @@ def bin_particles(x, lo, cell: float, dims, cell_start=None, perm=None):
     return cell_start, perm
 
 
-def density_cells(x, m, h, cell_start, dims, own=None, prec: int = SF_PREC_NATIVE, rho=None):
-    """Cell-linked density over cell-sorted SoA streams (x: (n,3), m, h: (n,))
-    stored as fp32 (SF_PREC_NATIVE), fp16 (16) or bf16 (SF_PREC_BF16)."""
+def density_cells(x, m, h, cell_start, perm, lo, cell: float, dims, own=None, reach: int = 1,
+                  prec: int = SF_PREC_NATIVE, rho=None):
+    """Cell-linked density.  x: (n,3), m, h: (n,) in particle order stored
+    as fp32 (SF_PREC_NATIVE), fp16 (16) or bf16 (SF_PREC_BF16); cell_start /
+    perm from bin_particles on the same grid.  Returns rho (fp32, particle
+    order; only own x-layers are written)."""
     import torch
     nx, ny, nz = dims
     own = own or (0, nx)
     n = m.shape[0]
     rho = rho if rho is not None else torch.zeros(max(n, 1), dtype=torch.float32, device=m.device)
-    check(lib().sf_b200_density_cells(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(cell_start), nx, ny, nz,
+    lo_arr = (C.c_float * 3)(*[float(v) for v in lo])
+    check(lib().sf_b200_density_cells(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
+                                      _ptr(cell_start), C.cast(lo_arr, C.c_void_p), float(cell), nx, ny, nz, reach,
                                       own[0], own[1], _ptr(rho), _stream()))
     return rho
 

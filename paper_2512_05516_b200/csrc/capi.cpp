@@ -255,11 +255,11 @@ sf_status sf_b200_run_kernel(const sf_view* v, void* p, const char* k, double dt
 }
 
 sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n,
-                                const int32_t* cell_start, int nx, int ny, int nz, int own_x0, int own_x1,
-                                float* rho, void* stream) {
-    if (!x || !m || !h || !cell_start || !rho) return fail(SF_INVALID_ARG, "null argument");
+                                const int32_t* perm, const int32_t* cell_start, const float* lo, float cell, int nx,
+                                int ny, int nz, int reach, int own_x0, int own_x1, float* rho, void* stream) {
+    if (!x || !m || !h || !cell_start || !rho || !lo) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
-        density_cells(x, m, h, prec, n, cell_start, nx, ny, nz, own_x0, own_x1, rho,
+        density_cells(x, m, h, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, own_x0, own_x1, rho,
                       static_cast<cudaStream_t>(stream));
         return SF_OK;
     });

@@ -1,12 +1,24 @@
 // Cell-linked SPH density (north-star "density cell-pair neighbour loop").
 //
 // New algorithm relative to the reference (whose density is all-pairs inside
-// contiguous 64-particle buffers, sph.cpp:176-199): particles are counting-
-// sorted into cells of side >= 2h; each home cell's 27-cell neighbourhood is
-// 9 contiguous runs of the sorted arrays (z fastest), staged once per warp
-// into shared memory as fp32 (x, y, z, m, h), then every home particle's sum
-// is split across the 32 lanes and reduced with warp shuffles.  Pair formula:
-// the reference's m_j * W(|x_i - x_j|, (h_i + h_j)/2), M4 spline, sigma=1/pi.
+// contiguous 64-particle buffers, sph.cpp:176-199).  Particles are counting-
+// sorted into cells (x-major ids, z fastest; bin_particles below).  The pass
+//
+//   k_pack        applies the sort permutation once and packs each particle
+//                 as (x, y, z, h) — float4 (16 B) for fp32 streams, four
+//                 halves (8 B) for fp16/bf16 — plus its mass;
+//   k_pairs       one thread per home particle of the own x-layers (a
+//                 contiguous range of the sorted order): for each of the
+//                 (2r+1)^2 (dx, dy) neighbour columns the cells iz-r..iz+r are
+//                 one contiguous run of the packed array, read straight
+//                 through L1/L2 (neighbouring threads sweep the same runs);
+//                 the pair test r^2 < (2 h_ij)^2 precedes any sqrt/division.
+//                 rho is stored back in particle (unsorted) order.
+//
+// With cells of side >= 2h use reach 1 (27 cells); with cells of side >= h
+// reach 2 (125 smaller cells) evaluates ~42% fewer candidate pairs.  Pair
+// formula: the reference's m_j * W(|x_i - x_j|, (h_i + h_j)/2), M4 spline,
+// sigma = 1/pi, evaluated in binary32 (rel <= 1e-5 vs the binary64 oracle).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -29,8 +41,50 @@ __device__ __forceinline__ float ldf(const void* p, uint64_t i) {
     else return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
 }
 
-constexpr int kCellWarps = 4;
-constexpr int kCand = 512;  // candidates staged per warp per batch
+// packed candidate record: (x, y, z, h) at the stream precision
+template <int P> struct Pack { using T = uint2; };
+template <> struct Pack<SP_F32> { using T = float4; };
+
+template <int P>
+__device__ __forceinline__ typename Pack<P>::T pack4(float a, float b, float c, float d) {
+    if constexpr (P == SP_F32) {
+        return make_float4(a, b, c, d);
+    } else if constexpr (P == SP_F16) {
+        const __half2 lo = __floats2half2_rn(a, b), hi = __floats2half2_rn(c, d);
+        return make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    } else {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+        return make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+}
+
+template <int P>
+__device__ __forceinline__ float4 unpack4(typename Pack<P>::T v) {
+    if constexpr (P == SP_F32) {
+        return v;
+    } else if constexpr (P == SP_F16) {
+        const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+        const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+        return make_float4(lo.x, lo.y, hi.x, hi.y);
+    } else {
+        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+        return make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+}
+
+// Stored values are exactly representable in the packed precision, so
+// packing then unpacking is lossless.
+template <int P>
+__global__ void k_pack(const void* __restrict__ x, const void* __restrict__ m, const void* __restrict__ h,
+                       const int32_t* __restrict__ perm, uint64_t n, typename Pack<P>::T* __restrict__ pos,
+                       float* __restrict__ mass) {
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = perm ? uint64_t(perm[k]) : k;
+        pos[k] = pack4<P>(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), ldf<P>(h, i));
+        mass[k] = ldf<P>(m, i);
+    }
+}
 
 // M4 cubic spline (sph.cpp:17-24) in binary32; caller guarantees q < 2.
 __device__ __forceinline__ float w_f32(float q, float inv_h) {
@@ -40,97 +94,81 @@ __device__ __forceinline__ float w_f32(float q, float inv_h) {
     return norm * 0.25f * t * t * t;
 }
 
+struct CellGrid {
+    float lox, loy, loz, inv_cell;
+    int nx, ny, nz, reach, own_x0, own_x1;
+};
+
 template <int P>
-__global__ void __launch_bounds__(kCellWarps * 32) k_density_cells(const void* __restrict__ x, const void* __restrict__ m,
-                                                                   const void* __restrict__ h,
-                                                                   const int32_t* __restrict__ cell_start, int nx, int ny,
-                                                                   int nz, int own_x0, int own_x1,
-                                                                   float* __restrict__ rho) {
-    __shared__ float4 s_pos[kCellWarps][kCand];  // x, y, z, m
-    __shared__ float s_h[kCellWarps][kCand];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t ncell_own = int64_t(own_x1 - own_x0) * ny * nz;
-    for (int64_t wc = int64_t(blockIdx.x) * kCellWarps + warp; wc < ncell_own; wc += int64_t(gridDim.x) * kCellWarps) {
-        const int ix = own_x0 + int(wc / (int64_t(ny) * nz));
-        const int rem = int(wc % (int64_t(ny) * nz));
-        const int iy = rem / nz, iz = rem % nz;
-        const int64_t home = (int64_t(ix) * ny + iy) * nz + iz;
-        const int hb = cell_start[home], he = cell_start[home + 1];
-        if (hb == he) continue;
-        // the 9 contiguous (dx, dy) runs covering z-1..z+1
-        int rb[9], re[9], tot = 0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            const int jx = ix + k / 3 - 1, jy = iy + k % 3 - 1;
-            rb[k] = re[k] = 0;
-            if (jx < 0 || jx >= nx || jy < 0 || jy >= ny) continue;
-            const int64_t c0 = (int64_t(jx) * ny + jy) * nz;
-            rb[k] = cell_start[c0 + max(iz - 1, 0)];
-            re[k] = cell_start[c0 + min(iz + 1, nz - 1) + 1];
-            tot += re[k] - rb[k];
-        }
-        for (int i = hb; i < he; ++i) {
-            // (the candidate set is staged once per batch; with one batch —
-            // the common case — it is staged once per home cell)
-            const float xi = ldf<P>(x, 3ull * i), yi = ldf<P>(x, 3ull * i + 1), zi = ldf<P>(x, 3ull * i + 2);
-            const float hi = ldf<P>(h, i);
-            float acc = 0.0f;
-            for (int base = 0; base < tot; base += kCand) {
-                const int cnt = min(kCand, tot - base);
-                if (i == hb || tot > kCand) {
-                    __syncwarp();
-                    for (int c = lane; c < cnt; c += 32) {
-                        int g = base + c, k = 0;
-                        while (g >= re[k] - rb[k]) { g -= re[k] - rb[k]; ++k; }
-                        const int j = rb[k] + g;
-                        s_pos[warp][c] = make_float4(ldf<P>(x, 3ull * j), ldf<P>(x, 3ull * j + 1), ldf<P>(x, 3ull * j + 2),
-                                                     ldf<P>(m, j));
-                        s_h[warp][c] = ldf<P>(h, j);
-                    }
-                    __syncwarp();
-                }
-                for (int c = lane; c < cnt; c += 32) {
-                    const float4 pj = s_pos[warp][c];
-                    const float dx = xi - pj.x, dy = yi - pj.y, dz = zi - pj.z;
+__global__ void __launch_bounds__(256) k_pairs(const typename Pack<P>::T* __restrict__ pos,
+                                               const float* __restrict__ mass, const int32_t* __restrict__ cell_start,
+                                               const int32_t* __restrict__ perm, CellGrid G, int64_t n,
+                                               float* __restrict__ rho) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const float4 pi = unpack4<P>(pos[k]);
+        // the same float formula bin_particles used, so the cell matches
+        const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
+        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
+        const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
+        const int iz = min(max(int(floorf((pi.z - G.loz) * G.inv_cell)), 0), G.nz - 1);
+        const int z0 = max(iz - G.reach, 0), z1 = min(iz + G.reach, G.nz - 1);
+        float acc = 0.0f;
+        for (int jx = max(ix - G.reach, 0); jx <= min(ix + G.reach, G.nx - 1); ++jx)
+            for (int jy = max(iy - G.reach, 0); jy <= min(iy + G.reach, G.ny - 1); ++jy) {
+                const int64_t c0 = (int64_t(jx) * G.ny + jy) * G.nz;
+                const int b = __ldg(cell_start + c0 + z0), e = __ldg(cell_start + c0 + z1 + 1);
+                for (int j = b; j < e; ++j) {
+                    const float4 pj = unpack4<P>(pos[j]);
+                    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
                     const float r2 = dx * dx + dy * dy + dz * dz;
-                    const float hij = 0.5f * (hi + s_h[warp][c]);
+                    const float hij = 0.5f * (pi.w + pj.w);
                     if (r2 < 4.0f * hij * hij) {
                         const float inv_h = __frcp_rn(hij);
                         const float q = sqrtf(r2) * inv_h;
-                        if (q < 2.0f) acc += pj.w * w_f32(q, inv_h);
+                        if (q < 2.0f) acc += __ldg(mass + j) * w_f32(q, inv_h);
                     }
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) rho[i] = acc;
-        }
+        rho[perm ? perm[k] : k] = acc;
     }
 }
 
-void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* cell_start,
-                   int nx, int ny, int nz, int own_x0, int own_x1, float* rho, cudaStream_t st) {
+void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
+                   const int32_t* cell_start, const float* lo, float cell, int nx, int ny, int nz, int reach,
+                   int own_x0, int own_x1, float* rho, cudaStream_t st) {
     require_device();
-    if (nx <= 0 || ny <= 0 || nz <= 0 || own_x0 < 0 || own_x1 > nx || own_x0 > own_x1)
+    if (nx <= 0 || ny <= 0 || nz <= 0 || own_x0 < 0 || own_x1 > nx || own_x0 > own_x1 || reach < 1 || reach > 4)
         throw std::invalid_argument("bad cell grid");
     if (n >= (1ull << 31)) throw std::invalid_argument("density_cells: n must be < 2^31 per device");
+    if (n == 0) return;
+    const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
+    if (sp < 0) throw std::invalid_argument("density_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
+    const size_t pbytes = (sp == SP_F32 ? 16 : 8) * n;
+    void* pos = nullptr;
+    float* mass = nullptr;
+    check_cuda(cudaMallocAsync(&pos, pbytes, st), "cudaMallocAsync");
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&mass), 4 * n, st), "cudaMallocAsync");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t cells = int64_t(own_x1 - own_x0) * ny * nz;
-    const int blocks = int(std::min<int64_t>((cells + kCellWarps - 1) / kCellWarps, int64_t(sms) * 8));
-    if (blocks == 0) return;
-    const int T = kCellWarps * 32;
-    if (prec == 1 /*native fp32*/ || prec == 32)
-        k_density_cells<SP_F32><<<blocks, T, 0, st>>>(x, m, h, cell_start, nx, ny, nz, own_x0, own_x1, rho);
-    else if (prec == 16)
-        k_density_cells<SP_F16><<<blocks, T, 0, st>>>(x, m, h, cell_start, nx, ny, nz, own_x0, own_x1, rho);
-    else if (prec == 100)
-        k_density_cells<SP_BF16><<<blocks, T, 0, st>>>(x, m, h, cell_start, nx, ny, nz, own_x0, own_x1, rho);
-    else
-        throw std::invalid_argument("density_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
+    const unsigned pb = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(sms) * 16));
+    CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
+    const int64_t nn = int64_t(n);
+    const unsigned qb = pb;
+    if (sp == SP_F32) {
+        k_pack<SP_F32><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<float4*>(pos), mass);
+        k_pairs<SP_F32><<<qb, 256, 0, st>>>(static_cast<float4*>(pos), mass, cell_start, perm, G, nn, rho);
+    } else if (sp == SP_F16) {
+        k_pack<SP_F16><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<uint2*>(pos), mass);
+        k_pairs<SP_F16><<<qb, 256, 0, st>>>(static_cast<uint2*>(pos), mass, cell_start, perm, G, nn, rho);
+    } else {
+        k_pack<SP_BF16><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<uint2*>(pos), mass);
+        k_pairs<SP_BF16><<<qb, 256, 0, st>>>(static_cast<uint2*>(pos), mass, cell_start, perm, G, nn, rho);
+    }
     check_cuda(cudaGetLastError(), "density_cells launch");
-    count_launches(1);
+    count_launches(2);
+    check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
+    check_cuda(cudaFreeAsync(mass, st), "cudaFreeAsync");
 }
 
 // ------------------------------------------------------------------ binning

@@ -146,21 +146,22 @@ def density_with_ghosts(x, m, h, gx, gm, gh, slab: Slab, backend: DensityFn) -> 
     return backend(xc, mc, hc, slab, x.shape[0])
 
 
-def gpu_density_backend(prec: int):
-    """bin_particles + density_cells on the rank's local grid (own layers
-    plus one ghost layer per side), own layers computed only."""
+def gpu_density_backend(prec: int, refine: int = 2):
+    """bin_particles + density_cells on the rank's local grid (own layers plus
+    one ghost layer per side).  Binning cells are the slab cells split
+    `refine` times per axis (side >= 2h/refine), searched with reach=refine:
+    ~42% fewer candidate pairs at refine 2 than 27 cells of side 2h."""
     from . import api
 
     def run(xc, mc, hc, slab: Slab, n_own: int) -> torch.Tensor:
         lo_layer, hi_layer = slab.local_lo, slab.local_hi
-        dims = (hi_layer - lo_layer, slab.nc, slab.nc)
+        cell = slab.cell / refine
+        dims = ((hi_layer - lo_layer) * refine, slab.nc * refine, slab.nc * refine)
         lo = (lo_layer * slab.cell, 0.0, 0.0)
-        cs, perm = api.bin_particles(xc.float().contiguous(), lo, slab.cell, dims)
-        p = perm[: xc.shape[0]].long()
-        rho_sorted = api.density_cells(xc[p].contiguous(), mc[p].contiguous(), hc[p].contiguous(), cs, dims,
-                                       own=(slab.x0 - lo_layer, slab.x1 - lo_layer), prec=prec)
-        rho = torch.empty(xc.shape[0], dtype=torch.float32, device=xc.device)
-        rho[p] = rho_sorted[: xc.shape[0]]
+        cs, perm = api.bin_particles(xc.float().contiguous(), lo, cell, dims)
+        own = ((slab.x0 - lo_layer) * refine, (slab.x1 - lo_layer) * refine)
+        rho = api.density_cells(xc.contiguous(), mc.contiguous(), hc.contiguous(), cs, perm, lo, cell, dims,
+                                own=own, reach=refine, prec=prec)
         return rho[:n_own]
 
     return run

@@ -260,34 +260,51 @@ def test_c2_full_size_roundtrip_properties():
 
 # ----------------------------------------------------------- cell density
 @pytest.mark.parametrize("prec", [api.SF_PREC_NATIVE, 16, api.SF_PREC_BF16])
-def test_density_cells_vs_oracle(prec):
+@pytest.mark.parametrize("refine", [1, 2])
+def test_density_cells_vs_oracle(prec, refine):
     n = 1 << 15
     rng = np.random.default_rng(3)
     x = rng.random((n, 3))
-    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3))
-    m = np.full(n, 1.0 / n)
+    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3)) * rng.uniform(0.8, 1.2, n)
+    m = rng.uniform(0.5, 1.5, n) / n
     dt = {api.SF_PREC_NATIVE: torch.float32, 16: torch.float16, api.SF_PREC_BF16: torch.bfloat16}[prec]
     xt = torch.tensor(x, device="cuda").to(dt)
     mt = torch.tensor(m, device="cuda").to(dt)
     ht = torch.tensor(h, device="cuda").to(dt)
-    cell = float(2 * ht.float().max())
-    nc = int(np.floor(1.0 / cell))
-    cell = 1.0 / nc
-    cs, perm = api.bin_particles(xt.float().contiguous(), (0, 0, 0), cell, (nc, nc, nc))
-    p = perm.long()
-    rho_sorted = api.density_cells(xt[p].contiguous(), mt[p].contiguous(), ht[p].contiguous(), cs,
-                                   (nc, nc, nc), prec=prec)
-    rho = torch.empty_like(rho_sorted)
-    rho[p] = rho_sorted
+    nc = int(np.floor(1.0 / float(2 * ht.float().max())))
+    cell = 1.0 / nc / refine
+    dims = (nc * refine,) * 3
+    cs, perm = api.bin_particles(xt.float().contiguous(), (0, 0, 0), cell, dims)
+    rho = api.density_cells(xt, mt, ht, cs, perm, (0, 0, 0), cell, dims, reach=refine, prec=prec)
     # oracle on exactly the stored (decoded) inputs, binary64
     xd, md, hd = (t.double().cpu().numpy() for t in (xt, mt, ht))
-    want = O.density_cells(xd.reshape(-1), md, hd, 0.0, 1.0, cell)
-    got = rho.double().cpu().numpy()
-    np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+    want = O.density_cells(xd.reshape(-1), md, hd, 0.0, 1.0, 1.0 / nc)
+    np.testing.assert_allclose(rho.double().cpu().numpy(), want, rtol=1e-5, atol=0)
     # binning is a stable counting sort
     cs_h, perm_h = cs.cpu().numpy(), perm.cpu().numpy()
     assert cs_h[-1] == n and np.all(np.diff(cs_h) >= 0)
     assert sorted(perm_h.tolist()) == list(range(n))
+    for c in range(0, len(cs_h) - 1, 97):  # ascending particle index inside each cell
+        assert np.all(np.diff(perm_h[cs_h[c]:cs_h[c + 1]]) > 0)
+
+
+def test_density_cells_own_layers_and_ghosts():
+    """Only own x-layers are computed; ghost layers feed neighbours only."""
+    n = 1 << 14
+    rng = np.random.default_rng(4)
+    x = rng.random((n, 3))
+    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3))
+    m = np.full(n, 1.0 / n)
+    nc = int(np.floor(1.0 / (2 * h[0])))
+    xt, mt, ht = (torch.tensor(a, device="cuda", dtype=torch.float32) for a in (x, m, h))
+    cs, perm = api.bin_particles(xt, (0, 0, 0), 1.0 / nc, (nc, nc, nc))
+    own = (2, nc - 3)
+    rho = api.density_cells(xt, mt, ht, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc), own=own).cpu().numpy()
+    want = O.density_cells(x.reshape(-1), m, h, 0.0, 1.0, 1.0 / nc)
+    layer = np.minimum(np.floor(x[:, 0] * nc).astype(int), nc - 1)
+    mine = (layer >= own[0]) & (layer < own[1])
+    np.testing.assert_allclose(rho[mine], want[mine], rtol=1e-5)
+    assert np.all(rho[~mine] == 0)
 
 
 def test_force_degenerate_state_is_an_error():
