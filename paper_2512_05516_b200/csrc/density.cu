@@ -251,10 +251,34 @@ __global__ void k_place(const int32_t* __restrict__ cid, uint64_t n, const int32
     }
 }
 
+// Sort a run of <= N particle indices in registers: fully unrolled
+// compare-exchange network (branchless min/max), padding with INT_MAX.
+template <int N>
+__device__ __forceinline__ void sort_run_regs(int32_t* __restrict__ perm, int b, int len) {
+    int32_t a[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) a[k] = k < len ? perm[b + k] : 0x7fffffff;
+#pragma unroll
+    for (int i = 1; i < N; ++i)
+#pragma unroll
+        for (int j = i; j > 0; --j) {
+            const int32_t lo = min(a[j - 1], a[j]), hi = max(a[j - 1], a[j]);
+            a[j - 1] = lo;
+            a[j] = hi;
+        }
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        if (k < len) perm[b + k] = a[k];
+}
+
 // make each cell's run ascending in particle index (deterministic order)
 __global__ void k_sort_runs(const int32_t* __restrict__ start, int64_t ncell, int32_t* __restrict__ perm) {
     for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < ncell; c += int64_t(gridDim.x) * blockDim.x) {
         const int b = start[c], e = start[c + 1];
+        const int len = e - b;
+        if (len <= 1) continue;
+        if (len <= 8) { sort_run_regs<8>(perm, b, len); continue; }
+        if (len <= 24) { sort_run_regs<24>(perm, b, len); continue; }
         for (int i = b + 1; i < e; ++i) {
             const int32_t v = perm[i];
             int j = i - 1;

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "codec.cuh"
 #include "plans.cuh"
@@ -453,6 +454,99 @@ __device__ __forceinline__ void warp_store(uint8_t* dst, const uint8_t* src, uin
     }
 }
 
+// Per-tile work policies of k_gather_warp.
+//
+// ProcGeneric: every stream through stream_dispatch (any plan).
+struct ProcGeneric {
+    __device__ static void tile(const uint8_t* tile, const GatherPlan& P, uint32_t lane, uint32_t recs, uint64_t rec0,
+                                uint8_t* out, uint8_t* dst) {
+        for (uint32_t q = 0; q < P.n; ++q) {
+            const GStream& g = P.s[q];
+            const uint32_t db = g.dst.width >> 3;
+            stream_dispatch(tile, P, g, lane, recs, out);
+            __syncwarp();
+            warp_store(dst + g.dst_base + rec0 * g.arity * db, out, recs * g.arity * db, db, lane);
+            __syncwarp();
+        }
+    }
+};
+
+// ProcXV<DB>: the drift-set shape (view.cpp proc_kind) — stream 0 = x (f64 x3,
+// copied or drifted with stream 1's source as operand), stream 1 = v
+// (f32 x3), both to DB.  One record per lane, all six lanes in registers;
+// NaN operands / NaN results redo the tile through the exact path.
+template <int DB>
+struct ProcXV {
+    __device__ static void tile(const uint8_t* tile, const GatherPlan& P, uint32_t lane, uint32_t recs, uint64_t rec0,
+                                uint8_t* out, uint8_t* dst) {
+        constexpr int db = Ieee<DB>::w / 8;
+        const GStream& gx = P.s[0];
+        const GStream& gv = P.s[1];
+        const uint32_t rbytes = P.record_bits >> 3;
+        uint8_t* ox = out;
+        uint8_t* ov = out + 32 * 3 * db;
+        const bool axpy = gx.op != OP_COPY;
+        bool bad = false;
+        if (lane < recs) {
+            const uint8_t* rp = tile + lane * rbytes;
+            uint64_t xs[3];
+            uint32_t vs[3];
+            uint64_t xq[3], vq[3];
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+                xs[l] = *reinterpret_cast<const uint64_t*>(rp + (gx.src_off >> 3) + 8 * l);
+                vs[l] = *reinterpret_cast<const uint32_t*>(rp + (gv.src_off >> 3) + 4 * l);
+            }
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+                bad |= Ieee<B_F64>::nan(xs[l]) | Ieee<B_F32>::nan(vs[l]);
+                xq[l] = Ieee<DB>::from(bits_to_f64(xs[l]));
+                if constexpr (DB == B_F16) {
+                    const __half h = __float2half_rn(bits_to_f32(vs[l]));
+                    vq[l] = *reinterpret_cast<const uint16_t*>(&h);
+                } else if constexpr (DB == B_BF16) {
+                    const __nv_bfloat16 h = __float2bfloat16_rn(bits_to_f32(vs[l]));
+                    vq[l] = *reinterpret_cast<const uint16_t*>(&h);
+                } else {
+                    vq[l] = vs[l];
+                }
+            }
+            if (axpy) {
+#pragma unroll
+                for (int l = 0; l < 3; ++l) {
+                    double r;
+                    if (P.math == MATH_FP64_EXACT)
+                        r = __dadd_rn(Ieee<DB>::f64(xq[l]), __dmul_rn(Ieee<DB>::f64(vq[l]), P.dt));
+                    else
+                        r = double(__fadd_rn(float(Ieee<DB>::f64(xq[l])), __fmul_rn(float(Ieee<DB>::f64(vq[l])), float(P.dt))));
+                    bad |= isnan(r);
+                    xq[l] = Ieee<DB>::from(r);
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+                if constexpr (db == 4) {
+                    reinterpret_cast<uint32_t*>(ox)[3 * lane + l] = uint32_t(xq[l]);
+                    reinterpret_cast<uint32_t*>(ov)[3 * lane + l] = uint32_t(vq[l]);
+                } else {
+                    reinterpret_cast<uint16_t*>(ox)[3 * lane + l] = uint16_t(xq[l]);
+                    reinterpret_cast<uint16_t*>(ov)[3 * lane + l] = uint16_t(vq[l]);
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, bad)) {
+            if (axpy) stream_fast<B_F64, DB, B_F32>(tile, rbytes, gx, lane, recs, P.dt, P.math, ox);
+            else stream_fast<B_F64, DB, -1>(tile, rbytes, gx, lane, recs, P.dt, P.math, ox);
+            stream_fast<B_F32, DB, -1>(tile, rbytes, gv, lane, recs, P.dt, P.math, ov);
+        }
+        __syncwarp();
+        warp_store(dst + gx.dst_base + rec0 * 3 * db, ox, recs * 3 * db, db, lane);
+        warp_store(dst + gv.dst_base + rec0 * 3 * db, ov, recs * 3 * db, db, lane);
+        __syncwarp();
+    }
+};
+
+template <class Proc>
 __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ GatherPlan P,
                                                         const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                                         uint64_t src_bytes) {
@@ -496,14 +590,7 @@ __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ 
             for (uint32_t b = uint32_t(bytes & ~15ull) + lane; b < bytes; b += 32) tile[b] = src[off + b];
             __syncwarp();
         }
-        for (uint32_t q = 0; q < P.n; ++q) {
-            const GStream& g = P.s[q];
-            const uint32_t db = g.dst.width >> 3;
-            stream_dispatch(tile, P, g, lane, recs, out);
-            __syncwarp();
-            warp_store(dst + g.dst_base + rec0 * g.arity * db, out, recs * g.arity * db, db, lane);
-            __syncwarp();
-        }
+        Proc::tile(tile, P, lane, recs, rec0, out, dst);
         if (lane == 0) {
             const uint64_t tn = t + uint64_t(kWStages) * tw;
             if (tn < ntiles) issue(tn, s);
@@ -557,6 +644,66 @@ __global__ void k_density_buffer(const __grid_constant__ DensityPlan P, uint8_t*
     // byte-aligned rho lanes are the norm; bit-packed ones take the atomic path
     const bool ba = ((P.rho.base | P.rho.stride | P.rho.fmt.width) & 7) == 0;
     st_bits_global(buf, P.rho.base + gi * P.rho.stride, P.rho.fmt.width, encode_lane(acc, P.rho.fmt), ba);
+}
+
+// ----------------------------------------------------------------- k_update_soa
+// In-place x = Q(Q(x) + Q(y)*dt) [max 0] over two contiguous SoA streams of
+// plain IEEE lanes (kick: v/a, u/du; drift: x/v).  Eight lanes per thread
+// per step with 16-B (or narrower) vector accesses; NaN operands and
+// inf - inf fall back per chunk to the exact scalar rule (axpy_lane).
+template <typename T> struct alignas(sizeof(T) * 8 > 16 ? 16 : sizeof(T) * 8) Vec8 { T v[8]; };
+
+template <int XB, int YB>
+__global__ void __launch_bounds__(256) k_update_soa(uint8_t* __restrict__ xs, const uint8_t* __restrict__ ys,
+                                                    uint64_t n, double dt, uint8_t op, uint8_t math) {
+    using TX = typename std::conditional<Ieee<XB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<XB>::w == 32, uint32_t, uint16_t>::type>::type;
+    using TY = typename std::conditional<Ieee<YB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<YB>::w == 32, uint32_t, uint16_t>::type>::type;
+    TX* x = reinterpret_cast<TX*>(xs);
+    const TY* y = reinterpret_cast<const TY*>(ys);
+    const bool clamp = op == OP_AXPY_CLAMP0;
+    const uint64_t chunks = (n + 7) / 8;
+    for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < chunks; c += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t e0 = c * 8;
+        const int cnt = n - e0 < 8 ? int(n - e0) : 8;
+        Vec8<TX> xv;
+        Vec8<TY> yv;
+        if (cnt == 8) {
+            xv = *reinterpret_cast<const Vec8<TX>*>(x + e0);
+            yv = *reinterpret_cast<const Vec8<TY>*>(y + e0);
+        } else {
+            for (int j = 0; j < 8; ++j) {
+                xv.v[j] = j < cnt ? x[e0 + j] : TX(0);
+                yv.v[j] = j < cnt ? y[e0 + j] : TY(0);
+            }
+        }
+        bool bad = false;
+        Vec8<TX> out;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            bad |= Ieee<XB>::nan(xv.v[j]) | Ieee<YB>::nan(yv.v[j]);
+            double r;
+            if (math == MATH_FP64_EXACT) {
+                r = __dadd_rn(Ieee<XB>::f64(xv.v[j]), __dmul_rn(Ieee<YB>::f64(yv.v[j]), dt));
+            } else {
+                r = double(__fadd_rn(float(Ieee<XB>::f64(xv.v[j])), __fmul_rn(float(Ieee<YB>::f64(yv.v[j])), float(dt))));
+            }
+            bad |= isnan(r);
+            if (clamp && r < 0.0) r = 0.0;
+            out.v[j] = TX(Ieee<XB>::from(r));
+        }
+        if (bad) {  // rare: exact reference NaN semantics, lane by lane
+            const LaneFmt fx = XB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<XB>::w);
+            const LaneFmt fy = YB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<YB>::w);
+            for (int j = 0; j < 8; ++j) out.v[j] = TX(axpy_lane(xv.v[j], fx, yv.v[j], fy, dt, op, math));
+        }
+        if (cnt == 8) {
+            *reinterpret_cast<Vec8<TX>*>(x + e0) = out;
+        } else {
+            for (int j = 0; j < cnt; ++j) x[e0 + j] = out.v[j];
+        }
+    }
 }
 
 // ----------------------------------------------------------------- force
@@ -665,19 +812,23 @@ cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_byt
     int warps = int(std::min<size_t>(16, (budget - 1024) / per_warp));
     if (warps < 1) return cudaErrorInvalidValue;
     const size_t smem = 128 * ((size_t(warps) * kWStages * 8 + 127) / 128) + size_t(warps) * per_warp;
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_gather_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
     const uint64_t ntiles = (p.count + p.tile_recs - 1) / p.tile_recs;
     const int ctas = int(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
     const uint64_t want = (ntiles + warps - 1) / warps;
     const int blocks = int(std::min<uint64_t>(want, uint64_t(num_sms()) * ctas));
-    k_gather_warp<<<blocks, warps * 32, smem, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst),
-                                                   src_bytes);
-    return cudaGetLastError();
+    auto go = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<blocks, warps * 32, smem, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst),
+                                               src_bytes);
+        return cudaGetLastError();
+    };
+    switch (p.proc) {
+        case PROC_XV_F16: return go(k_gather_warp<ProcXV<B_F16>>);
+        case PROC_XV_BF16: return go(k_gather_warp<ProcXV<B_BF16>>);
+        case PROC_XV_F32: return go(k_gather_warp<ProcXV<B_F32>>);
+        default: return go(k_gather_warp<ProcGeneric>);
+    }
 }
 
 cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate) {
@@ -695,6 +846,25 @@ cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, 
     e = cudaStreamSynchronize(st);
     *degenerate = flag != 0;
     return e;
+}
+
+// x/y bases: BaseKind of plain IEEE lanes; pointers 16-B aligned (caller checks).
+cudaError_t launch_update_soa(int xb, int yb, void* x, const void* y, uint64_t n, double dt, uint8_t op, uint8_t math,
+                              cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<uint64_t>((n / 8 + 255) / 256 + 1, uint64_t(num_sms()) * 16));
+    uint8_t* xp = static_cast<uint8_t*>(x);
+    const uint8_t* yp = static_cast<const uint8_t*>(y);
+#define SFB_U(XB, YB)                                                                       \
+    if (xb == XB && yb == YB) {                                                             \
+        k_update_soa<XB, YB><<<blocks, 256, 0, st>>>(xp, yp, n, dt, op, math);              \
+        return cudaGetLastError();                                                          \
+    }
+#define SFB_UY(XB) SFB_U(XB, B_F16) SFB_U(XB, B_BF16) SFB_U(XB, B_F32) SFB_U(XB, B_F64)
+    SFB_UY(B_F16) SFB_UY(B_BF16) SFB_UY(B_F32) SFB_UY(B_F64)
+#undef SFB_UY
+#undef SFB_U
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_density_buffer(const DensityPlan& p, void* buf, cudaStream_t st) {

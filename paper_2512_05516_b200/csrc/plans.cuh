@@ -48,6 +48,8 @@ struct ConvertPlan {
 using KernelPlan = ConvertPlan;
 
 // ---- tiled AoS -> SoA gather (TMA bulk-staged record tiles) ----------------
+enum Proc : uint8_t { PROC_GENERIC = 0, PROC_XV_F16 = 1, PROC_XV_BF16 = 2, PROC_XV_F32 = 3 };
+
 struct GStream {
     uint32_t src_off = 0;   // bit offset of lane 0 inside a source record
     uint32_t aux_off = 0;   // operand field, same record
@@ -66,6 +68,7 @@ struct GatherPlan {
     uint32_t tile_recs = 0;   // per-warp tile: 32*R records, 16-B aligned start
     uint32_t tile_bytes = 0;  // tile_recs * record_bits / 8
     uint32_t out_bytes = 0;   // per-warp SoA staging (largest stream slice)
+    uint8_t proc = 0;         // per-tile policy (PROC_*), chosen by view.cpp proc_kind
     uint8_t math = MATH_FP64_EXACT;
     double dt = 0;
     GStream s[kMaxStreams];

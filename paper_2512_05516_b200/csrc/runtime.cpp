@@ -57,7 +57,11 @@ void gather(const View& src, const void* sp, const View& dst, void* dp, const ch
     require_device();
     check_ptr(sp, "source buffer");
     check_ptr(dp, "destination buffer");
-    if (src.layout == Layout::AoS && dst.layout == Layout::SoA) {
+    bool tiled = src.layout == Layout::AoS && dst.layout == Layout::SoA && dst.subset.size() <= size_t(kMaxStreams);
+    for (size_t q = 0; q < dst.subset.size() && tiled; ++q)
+        tiled = (dst.width(int(q)) == 16 || dst.width(int(q)) == 32 || dst.width(int(q)) == 64) &&
+                dst.lane_base(int(q)) % 8 == 0;
+    if (tiled) {
         const GatherPlan g = kernel ? plan_gather_fused(src, dst, kernel, dt, math) : plan_gather(src, dst);
         check_cuda(launch_gather(g, sp, src.total_bytes(), dp, st, 0), "gather launch");
         count_launches(1);
@@ -121,6 +125,25 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
         return;
     }
     const KernelPlan kp = plan_kernel(v, kernel, dt, math);
+    // SoA streams of plain IEEE lanes: vectorised streaming update per stream pair
+    bool vec = v.layout == Layout::SoA;
+    for (uint32_t i = 0; i < kp.n && vec; ++i) {
+        const CStream& c = kp.s[i];
+        vec = fmt_is_ieee(c.dst.fmt) && fmt_is_ieee(c.aux.fmt) && c.dst.fmt.base != B_INT &&
+              c.aux.fmt.base != B_INT && c.dst.arity == c.aux.arity && ((c.dst.base | c.aux.base) % 128) == 0 &&
+              (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+    }
+    if (vec) {
+        for (uint32_t i = 0; i < kp.n; ++i) {
+            const CStream& c = kp.s[i];
+            uint8_t* base = static_cast<uint8_t*>(p);
+            check_cuda(launch_update_soa(c.dst.fmt.base, c.aux.fmt.base, base + c.dst.base / 8, base + c.aux.base / 8,
+                                         v.count * c.dst.arity, dt, c.op, kp.math, st),
+                       "update launch");
+        }
+        count_launches(kp.n);
+        return;
+    }
     check_cuda(launch_convert(kp, p, p, st), "kernel launch");
     count_launches(1);
 }

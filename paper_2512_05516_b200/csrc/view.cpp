@@ -134,12 +134,34 @@ static uint8_t fast_kind(const GStream& s, uint32_t record_bits) {
     return uint8_t(1 + src_idx(s.src) * 12 + dst_idx(s.dst) * 3 + ab);
 }
 
+// Per-tile policy: PROC_XV_* for the drift-set shape (x: f64 x3, v: f32 x3,
+// both narrowed to one IEEE format, x optionally drifted by v), else generic.
+static uint8_t proc_kind(const GatherPlan& g) {
+    if (g.n != 2 || g.tile_recs != 32 || g.record_bits % 64) return PROC_GENERIC;
+    const GStream &x = g.s[0], &v = g.s[1];
+    const bool x_ok = x.arity == 3 && fmt_is_ieee(x.src) && x.src.base == B_F64 && x.src_off % 64 == 0 &&
+                      fmt_is_ieee(x.dst);
+    const bool v_ok = v.arity == 3 && fmt_is_ieee(v.src) && v.src.base == B_F32 && v.src_off % 32 == 0 &&
+                      v.op == OP_COPY && fmt_eq(v.dst, x.dst);
+    const bool op_ok = x.op == OP_COPY ||
+                       (x.op == OP_AXPY && x.aux_off == v.src_off && fmt_eq(x.aux_src, v.src) && fmt_eq(x.aux_dst, x.dst));
+    if (!x_ok || !v_ok || !op_ok) return PROC_GENERIC;
+    switch (x.dst.base) {
+        case B_F16: return PROC_XV_F16;
+        case B_BF16: return PROC_XV_BF16;
+        case B_F32: return PROC_XV_F32;
+        default: return PROC_GENERIC;
+    }
+}
+
 static void finalize_fast(GatherPlan& g) {
     uint32_t out = 16;
     for (uint32_t i = 0; i < g.n; ++i) {
         g.s[i].fast = fast_kind(g.s[i], g.record_bits);
         out = std::max(out, g.tile_recs * g.s[i].arity * (g.s[i].dst.width / 8u));
     }
+    g.proc = proc_kind(g);
+    if (g.proc != PROC_GENERIC) out = 2 * g.tile_recs * 3 * (g.s[0].dst.width / 8u);  // x and v slices
     g.out_bytes = (out + 15) & ~15u;
 }
 
