@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <stdexcept>
+#include <type_traits>
 #include <vector>
 
 #include "runtime.hpp"
@@ -133,6 +134,62 @@ __global__ void __launch_bounds__(256) k_pairs(const typename Pack<P>::T* __rest
     }
 }
 
+// Same pair loop with the reach fixed at compile time: the (2R+1) run bounds
+// of a neighbour row are loaded together (independent loads in flight), and
+// candidates are consumed two at a time.
+template <int P, int R>
+__global__ void __launch_bounds__(256) k_pairs_r(const typename Pack<P>::T* __restrict__ pos,
+                                                 const float* __restrict__ mass,
+                                                 const int32_t* __restrict__ cell_start,
+                                                 const int32_t* __restrict__ perm, CellGrid G, int64_t n,
+                                                 float* __restrict__ rho) {
+    constexpr int W = 2 * R + 1;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const float4 pi = unpack4<P>(pos[k]);
+        const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
+        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
+        const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
+        const int iz = min(max(int(floorf((pi.z - G.loz) * G.inv_cell)), 0), G.nz - 1);
+        const int z0 = max(iz - R, 0), z1 = min(iz + R, G.nz - 1);
+        float acc = 0.0f;
+        auto pair = [&](const float4 pj, int j) {
+            const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            const float r2 = dx * dx + dy * dy + dz * dz;
+            const float hij = 0.5f * (pi.w + pj.w);
+            if (r2 < 4.0f * hij * hij) {
+                const float inv_h = __frcp_rn(hij);
+                const float q = sqrtf(r2) * inv_h;
+                if (q < 2.0f) acc += __ldg(mass + j) * w_f32(q, inv_h);
+            }
+        };
+#pragma unroll 1
+        for (int dxi = -R; dxi <= R; ++dxi) {
+            const int jx = ix + dxi;
+            if (jx < 0 || jx >= G.nx) continue;
+            int b[W], e[W];
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+                const int jy = iy - R + t;
+                const bool ok = jy >= 0 && jy < G.ny;
+                const int64_t c0 = (int64_t(jx) * G.ny + (ok ? jy : 0)) * G.nz;
+                b[t] = ok ? __ldg(cell_start + c0 + z0) : 0;
+                e[t] = ok ? __ldg(cell_start + c0 + z1 + 1) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+                int j = b[t];
+                for (; j + 1 < e[t]; j += 2) {
+                    const float4 p0 = unpack4<P>(pos[j]), p1 = unpack4<P>(pos[j + 1]);
+                    pair(p0, j);
+                    pair(p1, j + 1);
+                }
+                if (j < e[t]) pair(unpack4<P>(pos[j]), j);
+            }
+        }
+        rho[perm ? perm[k] : k] = acc;
+    }
+}
+
 void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
                    const int32_t* cell_start, const float* lo, float cell, int nx, int ny, int nz, int reach,
                    int own_x0, int own_x1, float* rho, cudaStream_t st) {
@@ -155,15 +212,21 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
     const int64_t nn = int64_t(n);
     const unsigned qb = pb;
+    auto pairs = [&](auto tag, auto* p) {
+        constexpr int SP = decltype(tag)::value;
+        if (reach == 1) k_pairs_r<SP, 1><<<qb, 256, 0, st>>>(p, mass, cell_start, perm, G, nn, rho);
+        else if (reach == 2) k_pairs_r<SP, 2><<<qb, 256, 0, st>>>(p, mass, cell_start, perm, G, nn, rho);
+        else k_pairs<SP><<<qb, 256, 0, st>>>(p, mass, cell_start, perm, G, nn, rho);
+    };
     if (sp == SP_F32) {
         k_pack<SP_F32><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<float4*>(pos), mass);
-        k_pairs<SP_F32><<<qb, 256, 0, st>>>(static_cast<float4*>(pos), mass, cell_start, perm, G, nn, rho);
+        pairs(std::integral_constant<int, SP_F32>{}, static_cast<float4*>(pos));
     } else if (sp == SP_F16) {
         k_pack<SP_F16><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<uint2*>(pos), mass);
-        k_pairs<SP_F16><<<qb, 256, 0, st>>>(static_cast<uint2*>(pos), mass, cell_start, perm, G, nn, rho);
+        pairs(std::integral_constant<int, SP_F16>{}, static_cast<uint2*>(pos));
     } else {
         k_pack<SP_BF16><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<uint2*>(pos), mass);
-        k_pairs<SP_BF16><<<qb, 256, 0, st>>>(static_cast<uint2*>(pos), mass, cell_start, perm, G, nn, rho);
+        pairs(std::integral_constant<int, SP_BF16>{}, static_cast<uint2*>(pos));
     }
     check_cuda(cudaGetLastError(), "density_cells launch");
     count_launches(2);
