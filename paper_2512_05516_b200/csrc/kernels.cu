@@ -546,6 +546,31 @@ struct ProcXV {
     }
 };
 
+// ProcAoSUpdate: in-place kick/drift on an AoS buffer (the reference's
+// native AoS path, sph.cpp:247-264): records arrive through the TMA ring,
+// every op stream's lanes are updated from the staged copy and only those
+// lanes are stored back (dst == the AoS buffer; tiles never overlap).
+struct ProcAoSUpdate {
+    __device__ static void tile(const uint8_t* tile, const GatherPlan& P, uint32_t lane, uint32_t recs, uint64_t rec0,
+                                uint8_t* /*out*/, uint8_t* dst) {
+        const bool ba = P.out_bytes != 0;  // byte-aligned lanes (set by plan_aos_update)
+        for (uint32_t q = 0; q < P.n; ++q) {
+            const GStream& g = P.s[q];
+            const int w = g.src.width, aw = g.aux_src.width;
+            for (uint32_t r = lane; r < recs; r += 32) {
+                const uint64_t rb = uint64_t(r) * P.record_bits;
+                const uint64_t gb = (rec0 + r) * uint64_t(P.record_bits);
+                for (uint32_t l = 0; l < g.arity; ++l) {
+                    const uint64_t xb = ld_bits_smem(tile, rb + g.src_off + uint64_t(l) * w, w);
+                    const uint64_t yb = ld_bits_smem(tile, rb + g.aux_off + uint64_t(l) * aw, aw);
+                    const uint64_t v = axpy_lane(xb, g.src, yb, g.aux_src, P.dt, g.op, P.math);
+                    st_bits_global(dst, gb + g.src_off + uint64_t(l) * w, w, v, ba);
+                }
+            }
+        }
+    }
+};
+
 template <class Proc>
 __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ GatherPlan P,
                                                         const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
@@ -827,6 +852,7 @@ cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_byt
         case PROC_XV_F16: return go(k_gather_warp<ProcXV<B_F16>>);
         case PROC_XV_BF16: return go(k_gather_warp<ProcXV<B_BF16>>);
         case PROC_XV_F32: return go(k_gather_warp<ProcXV<B_F32>>);
+        case PROC_AOS_UPDATE: return go(k_gather_warp<ProcAoSUpdate>);
         default: return go(k_gather_warp<ProcGeneric>);
     }
 }

@@ -124,6 +124,12 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
         count_launches(1);
         return;
     }
+    if (v.layout == Layout::AoS && v.count > 0) {  // records through the warp TMA ring, lanes stored back
+        const GatherPlan g = plan_aos_update(v, kernel, dt, math);
+        check_cuda(launch_gather(g, p, v.total_bytes(), p, st, 0), "aos update launch");
+        count_launches(1);
+        return;
+    }
     const KernelPlan kp = plan_kernel(v, kernel, dt, math);
     // SoA streams of plain IEEE lanes: vectorised streaming update per stream pair
     bool vec = v.layout == Layout::SoA;
