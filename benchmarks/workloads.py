@@ -196,6 +196,7 @@ def c5(args, peak, peak_kind, world, rank, group=None):
     h, nc, cell = grid_for(n)
     slab = Slab(nc, cell, rank, world)
     st = ShardedState(n, slab, prec=32, h=h)
+    st.sort_by_cell()  # particles kept in cell order (re-sorted every few steps in a long run)
     for _ in range(max(1, min(args.warmup, 2))):
         st.step(group=group)
     torch.cuda.synchronize()

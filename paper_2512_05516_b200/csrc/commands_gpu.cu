@@ -321,8 +321,11 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
     VariantResult res;
     const bool stream_mode = mode == "streaming" && !is_cpu(variant);
     if (!is_cpu(variant) && !stream_mode) {  // one full round trip each way
-        res.to_dev += aos.total_bytes();
-        res.to_host += aos.total_bytes();
+        // dev variants move the compressed state, host variants the unpacked one
+        const uint64_t b = is_host(variant) ? make_view(pop.schema, nullptr, Layout::AoS, kPrecNative, {}, n).total_bytes()
+                                            : aos.total_bytes();
+        res.to_dev += b;
+        res.to_host += b;
         res.transfers += 2;
     }
     for (const auto& k : c.kernels) {

@@ -546,31 +546,6 @@ struct ProcXV {
     }
 };
 
-// ProcAoSUpdate: in-place kick/drift on an AoS buffer (the reference's
-// native AoS path, sph.cpp:247-264): records arrive through the TMA ring,
-// every op stream's lanes are updated from the staged copy and only those
-// lanes are stored back (dst == the AoS buffer; tiles never overlap).
-struct ProcAoSUpdate {
-    __device__ static void tile(const uint8_t* tile, const GatherPlan& P, uint32_t lane, uint32_t recs, uint64_t rec0,
-                                uint8_t* /*out*/, uint8_t* dst) {
-        const bool ba = P.out_bytes != 0;  // byte-aligned lanes (set by plan_aos_update)
-        for (uint32_t q = 0; q < P.n; ++q) {
-            const GStream& g = P.s[q];
-            const int w = g.src.width, aw = g.aux_src.width;
-            for (uint32_t r = lane; r < recs; r += 32) {
-                const uint64_t rb = uint64_t(r) * P.record_bits;
-                const uint64_t gb = (rec0 + r) * uint64_t(P.record_bits);
-                for (uint32_t l = 0; l < g.arity; ++l) {
-                    const uint64_t xb = ld_bits_smem(tile, rb + g.src_off + uint64_t(l) * w, w);
-                    const uint64_t yb = ld_bits_smem(tile, rb + g.aux_off + uint64_t(l) * aw, aw);
-                    const uint64_t v = axpy_lane(xb, g.src, yb, g.aux_src, P.dt, g.op, P.math);
-                    st_bits_global(dst, gb + g.src_off + uint64_t(l) * w, w, v, ba);
-                }
-            }
-        }
-    }
-};
-
 template <class Proc>
 __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ GatherPlan P,
                                                         const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
@@ -731,6 +706,48 @@ __global__ void __launch_bounds__(256) k_update_soa(uint8_t* __restrict__ xs, co
     }
 }
 
+// ----------------------------------------------------------------- k_update_rec
+// In-place x = Q(Q(x) + Q(y)*dt) on plain IEEE lanes addressed per record
+// (AoS: stride = record bytes): one thread per record, typed loads of just
+// the lanes the op touches, stores of x only.  NaN / inf - inf -> exact rule.
+template <int XB, int YB, int AR>
+__global__ void __launch_bounds__(256) k_update_rec(uint8_t* __restrict__ buf, uint64_t n, uint32_t stride,
+                                                    uint32_t xoff, uint32_t yoff, double dt, uint8_t op,
+                                                    uint8_t math) {
+    using TX = typename std::conditional<Ieee<XB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<XB>::w == 32, uint32_t, uint16_t>::type>::type;
+    using TY = typename std::conditional<Ieee<YB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<YB>::w == 32, uint32_t, uint16_t>::type>::type;
+    const bool clamp = op == OP_AXPY_CLAMP0;
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
+        TX* x = reinterpret_cast<TX*>(buf + r * stride + xoff);
+        const TY* y = reinterpret_cast<const TY*>(buf + r * stride + yoff);
+        TX xv[AR], out[AR];
+        TY yv[AR];
+#pragma unroll
+        for (int l = 0; l < AR; ++l) xv[l] = x[l], yv[l] = y[l];
+        bool bad = false;
+#pragma unroll
+        for (int l = 0; l < AR; ++l) {
+            bad |= Ieee<XB>::nan(xv[l]) | Ieee<YB>::nan(yv[l]);
+            double v;
+            if (math == MATH_FP64_EXACT) v = __dadd_rn(Ieee<XB>::f64(xv[l]), __dmul_rn(Ieee<YB>::f64(yv[l]), dt));
+            else v = double(__fadd_rn(float(Ieee<XB>::f64(xv[l])), __fmul_rn(float(Ieee<YB>::f64(yv[l])), float(dt))));
+            bad |= isnan(v);
+            if (clamp && v < 0.0) v = 0.0;
+            out[l] = TX(Ieee<XB>::from(v));
+        }
+        if (bad) {
+            const LaneFmt fx = XB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<XB>::w);
+            const LaneFmt fy = YB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<YB>::w);
+#pragma unroll
+            for (int l = 0; l < AR; ++l) out[l] = TX(axpy_lane(xv[l], fx, yv[l], fy, dt, op, math));
+        }
+#pragma unroll
+        for (int l = 0; l < AR; ++l) x[l] = out[l];
+    }
+}
+
 // ----------------------------------------------------------------- force
 // dw_dr (sph.cpp:26-33), left-to-right binary64.
 __device__ __forceinline__ double dwdr_exact(double r, double h) {
@@ -852,7 +869,6 @@ cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_byt
         case PROC_XV_F16: return go(k_gather_warp<ProcXV<B_F16>>);
         case PROC_XV_BF16: return go(k_gather_warp<ProcXV<B_BF16>>);
         case PROC_XV_F32: return go(k_gather_warp<ProcXV<B_F32>>);
-        case PROC_AOS_UPDATE: return go(k_gather_warp<ProcAoSUpdate>);
         default: return go(k_gather_warp<ProcGeneric>);
     }
 }
@@ -872,6 +888,23 @@ cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, 
     e = cudaStreamSynchronize(st);
     *degenerate = flag != 0;
     return e;
+}
+
+cudaError_t launch_update_rec(int xb, int yb, int arity, void* buf, uint64_t n, uint32_t stride, uint32_t xoff,
+                              uint32_t yoff, double dt, uint8_t op, uint8_t math, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    uint8_t* b = static_cast<uint8_t*>(buf);
+#define SFB_R(XB, YB)                                                                                       \
+    if (xb == XB && yb == YB) {                                                                             \
+        if (arity == 3) k_update_rec<XB, YB, 3><<<blocks, 256, 0, st>>>(b, n, stride, xoff, yoff, dt, op, math); \
+        else k_update_rec<XB, YB, 1><<<blocks, 256, 0, st>>>(b, n, stride, xoff, yoff, dt, op, math);      \
+        return cudaGetLastError();                                                                          \
+    }
+    SFB_R(B_F64, B_F64) SFB_R(B_F64, B_F32) SFB_R(B_F32, B_F32) SFB_R(B_F32, B_F64)
+    SFB_R(B_F16, B_F16) SFB_R(B_BF16, B_BF16)
+#undef SFB_R
+    return cudaErrorInvalidValue;
 }
 
 // x/y bases: BaseKind of plain IEEE lanes; pointers 16-B aligned (caller checks).

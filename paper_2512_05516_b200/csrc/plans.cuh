@@ -48,7 +48,7 @@ struct ConvertPlan {
 using KernelPlan = ConvertPlan;
 
 // ---- tiled AoS -> SoA gather (TMA bulk-staged record tiles) ----------------
-enum Proc : uint8_t { PROC_GENERIC = 0, PROC_XV_F16 = 1, PROC_XV_BF16 = 2, PROC_XV_F32 = 3, PROC_AOS_UPDATE = 4 };
+enum Proc : uint8_t { PROC_GENERIC = 0, PROC_XV_F16 = 1, PROC_XV_BF16 = 2, PROC_XV_F32 = 3 };
 
 struct GStream {
     uint32_t src_off = 0;   // bit offset of lane 0 inside a source record

@@ -124,13 +124,28 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
         count_launches(1);
         return;
     }
-    if (v.layout == Layout::AoS && v.count > 0) {  // records through the warp TMA ring, lanes stored back
-        const GatherPlan g = plan_aos_update(v, kernel, dt, math);
-        check_cuda(launch_gather(g, p, v.total_bytes(), p, st, 0), "aos update launch");
-        count_launches(1);
-        return;
-    }
     const KernelPlan kp = plan_kernel(v, kernel, dt, math);
+    if (v.layout == Layout::AoS && v.byte_aligned()) {  // typed per-record lanes when every op is plain IEEE
+        bool ok = true;
+        const uint64_t rb = v.record_bits();
+        for (uint32_t i = 0; i < kp.n && ok; ++i) {
+            const CStream& c = kp.s[i];
+            const auto al = [&](const Lanes& L) { return L.base % L.fmt.width == 0 && rb % L.fmt.width == 0; };
+            ok = fmt_is_ieee(c.dst.fmt) && fmt_is_ieee(c.aux.fmt) && c.dst.fmt.base != B_INT &&
+                 c.aux.fmt.base != B_INT && c.dst.arity == c.aux.arity && al(c.dst) && al(c.aux) &&
+                 (reinterpret_cast<uintptr_t>(p) & 7) == 0;
+        }
+        if (ok) {
+            for (uint32_t i = 0; i < kp.n; ++i) {
+                const CStream& c = kp.s[i];
+                check_cuda(launch_update_rec(c.dst.fmt.base, c.aux.fmt.base, c.dst.arity, p, v.count, uint32_t(rb / 8),
+                                             uint32_t(c.dst.base / 8), uint32_t(c.aux.base / 8), dt, c.op, kp.math, st),
+                           "aos update launch");
+            }
+            count_launches(kp.n);
+            return;
+        }
+    }
     // SoA streams of plain IEEE lanes: vectorised streaming update per stream pair
     bool vec = v.layout == Layout::SoA;
     for (uint32_t i = 0; i < kp.n && vec; ++i) {

@@ -292,33 +292,4 @@ ForcePlan plan_force(const View& v, uint64_t bs, int per_access) {
 
 namespace sfb {
 
-// In-place kick/drift over an AoS view through the warp TMA ring
-// (ProcAoSUpdate): one stream per op, lanes addressed inside the record.
-GatherPlan plan_aos_update(const View& v, const std::string& kernel, double dt, int math) {
-    if (v.layout != Layout::AoS) throw std::invalid_argument("plan_aos_update needs an AoS view");
-    const KernelPlan kp = plan_kernel(v, kernel, dt, math);
-    GatherPlan g;
-    g.count = v.count;
-    g.record_bits = uint32_t(v.record_bits());
-    const uint32_t period = 128 / std::gcd(g.record_bits, 128u);
-    g.tile_recs = 32 * std::max<uint32_t>(1, period / 32);
-    g.tile_bytes = uint32_t(g.tile_recs * uint64_t(g.record_bits) / 8);
-    g.dt = dt;
-    g.math = uint8_t(math);
-    for (uint32_t i = 0; i < kp.n; ++i) {
-        GStream& s = g.s[g.n++];
-        s.src_off = uint32_t(kp.s[i].dst.base);
-        s.src = kp.s[i].dst.fmt;
-        s.dst = kp.s[i].dst.fmt;
-        s.aux_off = uint32_t(kp.s[i].aux.base);
-        s.aux_src = kp.s[i].aux.fmt;
-        s.aux_dst = kp.s[i].aux_q;
-        s.arity = kp.s[i].dst.arity;
-        s.op = kp.s[i].op;
-    }
-    g.proc = PROC_AOS_UPDATE;
-    g.out_bytes = v.byte_aligned() ? 16 : 0;  // doubles as the byte-aligned flag; staging unused
-    return g;
-}
-
 }  // namespace sfb

@@ -57,6 +57,5 @@ GatherPlan plan_gather_fused(const View& src, const View& dst, const std::string
                              int math);
 DensityPlan plan_density(const View& v, uint64_t buffer_size, int per_access);
 ForcePlan plan_force(const View& v, uint64_t buffer_size, int per_access);
-GatherPlan plan_aos_update(const View& v, const std::string& kernel, double dt, int math);
 
 }  // namespace sfb

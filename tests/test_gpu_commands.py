@@ -77,6 +77,8 @@ def test_bench_pipeline_checksums_match_reference(libs):
     for a, b in zip(r1, r2):
         assert (a["variant"], a["mode"]) == (b["variant"], b["mode"])
         assert a["checksum"] == b["checksum"], (a, b)
+        # the byte ledger (pipelines.cpp:434-447 semantics) agrees exactly
+        assert (a["bytes_to_device"], a["bytes_to_host"]) == (b["bytes_to_device"], b["bytes_to_host"]), (a, b)
 
 
 def test_validate_and_fault(libs):  # test_capi.cpp:72-87

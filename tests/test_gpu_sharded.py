@@ -1,0 +1,56 @@
+"""C5 sharded path on one B200: a full N=1 step against the oracle, and the
+per-rank density with ghost layers (simulated 2- and 4-rank splits of one
+population) against the global oracle density."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2512_05516_b200 import api
+from paper_2512_05516_b200.sharded import ShardedState, Slab, density_with_ghosts, gpu_density_backend, grid_for
+
+pytestmark = pytest.mark.gpu
+
+
+def test_single_rank_step_matches_oracle():
+    n = 1 << 15
+    h, nc, cell = grid_for(n)
+    st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h)
+    st.sort_by_cell()
+    before = {k: st.stream(k).double().cpu().numpy().copy() for k in ["x", "v", "u", "a", "du", "m", "h"]}
+    st.step(1e-3)
+    torch.cuda.synchronize()
+    # kick then drift, binary64 arithmetic on the binary32 stored lanes, stored back as binary32
+    v2, u2 = O.kick(before["v"], before["u"], before["a"], before["du"], 1e-3)
+    v2 = v2.astype(np.float32).astype(np.float64)
+    u2 = u2.astype(np.float32).astype(np.float64)
+    x2 = O.drift(before["x"], v2, 1e-3).astype(np.float32).astype(np.float64)
+    np.testing.assert_array_equal(st.stream("v").double().cpu().numpy(), v2)
+    np.testing.assert_array_equal(st.stream("u").double().cpu().numpy(), u2)
+    np.testing.assert_array_equal(st.stream("x").double().cpu().numpy(), x2)
+    want = O.density_cells(x2.reshape(-1), before["m"], before["h"], 0.0, 1.0, cell)
+    got = st.stream("rho").double().cpu().numpy()
+    np.testing.assert_allclose(got, want.astype(np.float32), rtol=2e-5)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_rank_density_with_ghost_layers(world):
+    n = 1 << 15
+    rng = np.random.default_rng(9)
+    x = rng.random((n, 3))
+    h, nc, cell = grid_for(n)
+    hh = np.full(n, h)
+    m = np.full(n, 1.0 / n)
+    want = O.density_cells(x.reshape(-1), m, hh, 0.0, 1.0, cell)
+    layer = np.minimum(np.floor(x[:, 0] / cell).astype(int), nc - 1)
+    seen = np.zeros(n, bool)
+    for r in range(world):
+        slab = Slab(nc, cell, r, world)
+        own = (layer >= slab.x0) & (layer < slab.x1)
+        ghost = ((layer == slab.x0 - 1) | (layer == slab.x1)) & ~own
+        t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+        rho = density_with_ghosts(t(x[own]), t(m[own]), t(hh[own]), t(x[ghost]), t(m[ghost]), t(hh[ghost]), slab,
+                                  gpu_density_backend(api.SF_PREC_NATIVE))
+        np.testing.assert_allclose(rho.double().cpu().numpy(), want[own], rtol=1e-5)
+        seen |= own
+    assert seen.all()
