@@ -18,6 +18,16 @@ void require_device() {
     if (have < 0) {
         int n = 0;
         have = (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) ? 1 : 0;
+        // Stream-ordered scratch (density_cells) comes from the device's default
+        // pool; keep freed blocks cached instead of unmapping them at every
+        // synchronize (the default release threshold is 0).
+        for (int d = 0; d < n && have; ++d) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
     }
     if (!have) throw std::runtime_error("no CUDA device: libsoaforge_b200 runs on the GPU only (no CPU path)");
 }

@@ -113,9 +113,9 @@ def halo_rows(x: torch.Tensor, m: torch.Tensor, h: torch.Tensor, slab: Slab):
 
 def exchange_halo(x, m, h, slab: Slab, group=None):
     """Ghost particles (x, m, h) received from the neighbouring slabs."""
-    left, right = halo_rows(x, m, h, slab)
     if slab.world == 1:
         return x[:0], m[:0], h[:0]
+    left, right = halo_rows(x, m, h, slab)
     gl, gr = neighbour_exchange(left, right, slab.rank, slab.world, group)
     g = torch.cat([gl, gr], dim=0)
     return g[:, 0:3].contiguous(), g[:, 3].contiguous(), g[:, 4].contiguous()
