@@ -222,11 +222,23 @@ def c5(args, peak, peak_kind, world, rank, group=None):
         phases["density"].append(c.elapsed_time(d))
         times.append(a.elapsed_time(d))
     ms = sum(times) / len(times)
+    # one more step with sub-phase events (not part of the timed mean)
+    import paper_2512_05516_b200.sharded as SH
+    SH.PHASES.clear()
+    SH.PHASES["_on"] = True
+    st.step(group=group)
+    torch.cuda.synchronize()
+    ev = SH.PHASES.pop("_events", [])
+    SH.PHASES.clear()
+    sub = {}
+    for (a, ea), (_, eb) in zip(ev, ev[1:]):
+        sub[a] = sub.get(a, 0.0) + ea.elapsed_time(eb)
+    phases["density_sub"] = [sub]
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
             "roofline": {"bound": "compute (density)", "achieved": None, "peak": peak, "unit": "GB/s",
                          "frac": None, "kernel": "k_density_cells + k_convert(kick/drift)"},
             "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + kick/drift sharded by cell "
                                    "with NCCL halo exchange" % (n >> 20), "particles_total": n,
                        "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},
-            "phases_ms": {k: sum(v) / len(v) for k, v in phases.items()},
+            "phases_ms": {k: (sum(v) / len(v) if k != "density_sub" else v[0]) for k, v in phases.items()},
             "particles_local": st.n}

@@ -175,21 +175,15 @@ __global__ void __launch_bounds__(256) k_pairs_r(const typename Pack<P>::T* __re
                 b[t] = ok ? __ldg(cell_start + c0 + z0) : 0;
                 e[t] = ok ? __ldg(cell_start + c0 + z1 + 1) : 0;
             }
-            // the row's W runs as one flattened candidate sequence: the warp
-            // iterates max-over-lanes of the row total, not of every run
-            int total = 0;
 #pragma unroll
-            for (int t = 0; t < W; ++t) total += e[t] - b[t];
-            int t = 0, j = b[0];
-            for (int c = 0; c < total; ++c) {
-                while (j >= e[t]) {  // next non-empty run (t < W guaranteed while c < total)
-                    ++t;
-#pragma unroll
-                    for (int u = 1; u < W; ++u)
-                        if (t == u) j = b[u];
+            for (int t = 0; t < W; ++t) {
+                int j = b[t];
+                for (; j + 1 < e[t]; j += 2) {
+                    const float4 p0 = unpack4<P>(pos[j]), p1 = unpack4<P>(pos[j + 1]);
+                    pair(p0, j);
+                    pair(p1, j + 1);
                 }
-                pair(unpack4<P>(pos[j]), j);
-                ++j;
+                if (j < e[t]) pair(unpack4<P>(pos[j]), j);
             }
         }
         rho[perm ? perm[k] : k] = acc;

@@ -148,6 +148,16 @@ def density_with_ghosts(x, m, h, gx, gm, gh, slab: Slab, backend: DensityFn) -> 
     return backend(xc, mc, hc, slab, x.shape[0])
 
 
+PHASES: dict = {}  # optional CUDA-event phase log (bench instrumentation)
+
+
+def _mark(name):
+    if PHASES.get("_on"):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        PHASES.setdefault("_events", []).append((name, e))
+
+
 def gpu_density_backend(prec: int, refine: int = 2):
     """bin_particles + density_cells on the rank's local grid (own layers plus
     one ghost layer per side).  Binning cells are the slab cells split
@@ -160,10 +170,13 @@ def gpu_density_backend(prec: int, refine: int = 2):
         cell = slab.cell / refine
         dims = ((hi_layer - lo_layer) * refine, slab.nc * refine, slab.nc * refine)
         lo = (lo_layer * slab.cell, 0.0, 0.0)
+        _mark("bin")
         cs, perm = api.bin_particles(xc.float().contiguous(), lo, cell, dims)
         own = ((slab.x0 - lo_layer) * refine, (slab.x1 - lo_layer) * refine)
+        _mark("pairs")
         rho = api.density_cells(xc.contiguous(), mc.contiguous(), hc.contiguous(), cs, perm, lo, cell, dims,
                                 own=own, reach=refine, prec=prec)
+        _mark("store")
         return rho[:n_own]
 
     return run
@@ -250,10 +263,12 @@ class ShardedState:
 
     def density(self, group=None):
         x, m, h = self.stream("x"), self.stream("m"), self.stream("h")
+        _mark("halo")
         gx, gm, gh = exchange_halo(x, m, h, self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
         rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec))
         self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
+        _mark("end")
 
     def sort_by_cell(self, refine: int = 2):
         """Reorder every field into cell order (the density binning's order), so
