@@ -748,6 +748,62 @@ __global__ void __launch_bounds__(256) k_update_rec(uint8_t* __restrict__ buf, u
     }
 }
 
+// All ops of one kernel (kick: v/a and u/du) in a single per-record pass when
+// every lane shares one IEEE x format and one y format.
+template <int XB, int YB>
+__global__ void __launch_bounds__(256) k_update_rec_multi(uint8_t* __restrict__ buf, uint64_t n, uint32_t stride,
+                                                          const RecOps ops, double dt, uint8_t math) {
+    using TX = typename std::conditional<Ieee<XB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<XB>::w == 32, uint32_t, uint16_t>::type>::type;
+    using TY = typename std::conditional<Ieee<YB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<YB>::w == 32, uint32_t, uint16_t>::type>::type;
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
+        uint8_t* rec = buf + r * stride;
+        TX xv[2][3], out[2][3];
+        TY yv[2][3];
+#pragma unroll
+        for (int o = 0; o < 2; ++o)
+#pragma unroll
+            for (int l = 0; l < 3; ++l)
+                if (o < ops.n && l < ops.arity[o]) {
+                    xv[o][l] = reinterpret_cast<const TX*>(rec + ops.xoff[o])[l];
+                    yv[o][l] = reinterpret_cast<const TY*>(rec + ops.yoff[o])[l];
+                }
+        bool bad = false;
+#pragma unroll
+        for (int o = 0; o < 2; ++o)
+#pragma unroll
+            for (int l = 0; l < 3; ++l)
+                if (o < ops.n && l < ops.arity[o]) {
+                    bad |= Ieee<XB>::nan(xv[o][l]) | Ieee<YB>::nan(yv[o][l]);
+                    double v;
+                    if (math == MATH_FP64_EXACT)
+                        v = __dadd_rn(Ieee<XB>::f64(xv[o][l]), __dmul_rn(Ieee<YB>::f64(yv[o][l]), dt));
+                    else
+                        v = double(__fadd_rn(float(Ieee<XB>::f64(xv[o][l])),
+                                             __fmul_rn(float(Ieee<YB>::f64(yv[o][l])), float(dt))));
+                    bad |= isnan(v);
+                    if (ops.op[o] == OP_AXPY_CLAMP0 && v < 0.0) v = 0.0;
+                    out[o][l] = TX(Ieee<XB>::from(v));
+                }
+        if (bad) {
+            const LaneFmt fx = XB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<XB>::w);
+            const LaneFmt fy = YB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<YB>::w);
+            for (int o = 0; o < ops.n; ++o)
+                for (int l = 0; l < ops.arity[o]; ++l)
+                    out[o][l] = TX(axpy_lane(xv[o][l], fx, yv[o][l], fy, dt, ops.op[o], math));
+        }
+#pragma unroll
+        for (int o = 0; o < 2; ++o)
+#pragma unroll
+            for (int l = 0; l < 3; ++l)
+                if (o < ops.n && l < ops.arity[o]) reinterpret_cast<TX*>(rec + ops.xoff[o])[l] = out[o][l];
+    }
+}
+
+cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops,
+                                    double dt, uint8_t math, cudaStream_t st);
+
 // ----------------------------------------------------------------- force
 // dw_dr (sph.cpp:26-33), left-to-right binary64.
 __device__ __forceinline__ double dwdr_exact(double r, double h) {
@@ -904,6 +960,21 @@ cudaError_t launch_update_rec(int xb, int yb, int arity, void* buf, uint64_t n, 
     SFB_R(B_F64, B_F64) SFB_R(B_F64, B_F32) SFB_R(B_F32, B_F32) SFB_R(B_F32, B_F64)
     SFB_R(B_F16, B_F16) SFB_R(B_BF16, B_BF16)
 #undef SFB_R
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops,
+                                    double dt, uint8_t math, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    uint8_t* b = static_cast<uint8_t*>(buf);
+#define SFB_M(XB, YB)                                                                     \
+    if (xb == XB && yb == YB) {                                                           \
+        k_update_rec_multi<XB, YB><<<blocks, 256, 0, st>>>(b, n, stride, ops, dt, math); \
+        return cudaGetLastError();                                                        \
+    }
+    SFB_M(B_F64, B_F64) SFB_M(B_F32, B_F32) SFB_M(B_F16, B_F16) SFB_M(B_BF16, B_BF16) SFB_M(B_F64, B_F32)
+#undef SFB_M
     return cudaErrorInvalidValue;
 }
 

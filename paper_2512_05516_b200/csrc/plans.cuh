@@ -74,6 +74,13 @@ struct GatherPlan {
     GStream s[kMaxStreams];
 };
 
+// ---- in-place kick/drift on AoS records, all ops in one pass -----------------
+struct RecOps {
+    uint32_t xoff[2], yoff[2];  // byte offsets of the written field and its operand
+    uint8_t arity[2], op[2];
+    int n;
+};
+
 // ---- SPH density over 64-particle neighbour buffers (sph.cpp:176-199) -------
 struct DensityPlan {
     Lanes x, m, h, rho;

@@ -145,6 +145,24 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
                  c.aux.fmt.base != B_INT && c.dst.arity == c.aux.arity && al(c.dst) && al(c.aux) &&
                  (reinterpret_cast<uintptr_t>(p) & 7) == 0;
         }
+        bool same = ok && kp.n <= 2;
+        for (uint32_t i = 1; i < kp.n && same; ++i)
+            same = fmt_eq(kp.s[i].dst.fmt, kp.s[0].dst.fmt) && fmt_eq(kp.s[i].aux.fmt, kp.s[0].aux.fmt);
+        if (same) {  // every op of the kernel in one per-record pass
+            RecOps ops{};
+            ops.n = int(kp.n);
+            for (uint32_t i = 0; i < kp.n; ++i) {
+                ops.xoff[i] = uint32_t(kp.s[i].dst.base / 8);
+                ops.yoff[i] = uint32_t(kp.s[i].aux.base / 8);
+                ops.arity[i] = kp.s[i].dst.arity;
+                ops.op[i] = kp.s[i].op;
+            }
+            check_cuda(launch_update_rec_multi(kp.s[0].dst.fmt.base, kp.s[0].aux.fmt.base, p, v.count,
+                                               uint32_t(rb / 8), ops, dt, kp.math, st),
+                       "aos update launch");
+            count_launches(1);
+            return;
+        }
         if (ok) {
             for (uint32_t i = 0; i < kp.n; ++i) {
                 const CStream& c = kp.s[i];
