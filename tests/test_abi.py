@@ -156,3 +156,15 @@ def test_gpu_entry_points_fail_loudly_without_device():
     st = L.lib().sf_b200_gather(src.handle, C.cast(buf, C.c_void_p), dst.handle, C.cast(out, C.c_void_p), None)
     assert st == L.SF_ERROR
     assert "no CUDA device" in L.lib().sf_last_error().decode()
+
+
+def test_plain_c_consumer_links_and_runs(tmp_path):
+    """tests/c/capi_check.c: a C program built against include/soaforge_b200.h."""
+    import subprocess
+    exe = tmp_path / "capi_check"
+    libdir = os.path.dirname(L.LIB_PATH)
+    subprocess.run(["/usr/bin/gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "capi_check.c"), "-L", libdir, "-lsoaforge_b200",
+                    "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and "capi ok" in out.stdout, out.stdout
