@@ -113,6 +113,53 @@ def cpu_reference_rate(n_per_thread, threads, prec, seed=42):
     return n_per_thread * threads / secs, secs
 
 
+def _bench_kernels_csv(lib_path, particles, threads):
+    """Run a library's sf_run_bench_kernels (bench.cpp:269-316 semantics)."""
+    import ctypes as C
+    L = C.CDLL(lib_path)
+    L.sf_config_create.argtypes = [C.POINTER(C.c_void_p)]
+    L.sf_config_set_int.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+    L.sf_config_set_string.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
+    L.sf_run_bench_kernels.argtypes = [C.c_void_p, C.POINTER(C.c_char_p)]
+    L.sf_config_destroy.argtypes = [C.c_void_p]
+    L.sf_last_error.restype = C.c_char_p
+    cfg = C.c_void_p()
+    L.sf_config_create(C.byref(cfg))
+    L.sf_config_set_int(cfg, b"particles", particles)
+    L.sf_config_set_int(cfg, b"threads", threads)
+    L.sf_config_set_string(cfg, b"kernels", b"kick,drift,density")
+    L.sf_config_set_string(cfg, b"precision", b"64,32,16")
+    out = C.c_char_p()
+    st = L.sf_run_bench_kernels(cfg, C.byref(out))
+    text = out.value.decode() if out.value else ""
+    L.sf_config_destroy(cfg)
+    if st != 0:
+        raise RuntimeError(L.sf_last_error().decode())
+    rows = [l.split(",") for l in text.splitlines() if l and not l.startswith("#")]
+    head = rows[0]
+    return [dict(zip(head, r)) for r in rows[1:]]
+
+
+def kernels_table(particles):
+    """Reference CPU (all host cores) vs this GPU library, per kernel x layout x
+    precision, both through their own sf_run_bench_kernels on the same config:
+    particle updates/s and the checksum agreement (north_star: AoS and SoA, each
+    precision mode)."""
+    threads = os.cpu_count() or 1
+    ref = _bench_kernels_csv(os.path.join(ROOT, "oracle", "_ref", "libsoaforge_ref.so"), particles, threads)
+    from paper_2512_05516_b200 import _lib
+    gpu = _bench_kernels_csv(_lib.LIB_PATH, particles, threads)
+    table = {}
+    for r, g in zip(ref, gpu):
+        key = "%s/%s/T%s" % (r["kernel"], r["layout"], r["precision"])
+        cs, gs = float(r["compute_s"]), float(g["compute_s"])
+        table[key] = {"cpu_updates_per_s": particles / cs if cs > 0 else None,
+                      "gpu_updates_per_s": particles / gs if gs > 0 else None,
+                      "checksum_equal": r["checksum"] == g["checksum"]}
+    return {"particles": particles, "cpu_threads": threads, "rows": table,
+            "note": "density = 64-particle buffer mode (reference semantics, binary64); GPU time excludes transfers"}
+
+
 def dist_init():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -274,6 +321,10 @@ def b200_arm(args):
                        n_pt * threads, n_pt, secs)}
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "unavailable: %s" % ex}
+        try:
+            cpu["per_mode"] = kernels_table(args.table_particles)
+        except Exception as ex:
+            cpu["per_mode"] = {"unavailable": str(ex)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -343,6 +394,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--table-particles", type=int, default=1 << 16)
     ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c2",
                     help="BASELINE.json config (default c2 = configs[1], the headline)")
     ap.add_argument("--c4-n", type=int, default=1 << 26)
