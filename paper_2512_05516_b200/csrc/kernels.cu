@@ -807,100 +807,7 @@ __global__ void __launch_bounds__(256) k_update_rec_multi(uint8_t* __restrict__ 
 cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops,
                                     double dt, uint8_t math, cudaStream_t st);
 
-// Same update with the warp's 32 records staged through shared memory: the
-// record span is read with coalesced 16-B loads (the strided per-record lane
-// loads above cost ~22 L1 wavefronts per instruction), lanes update their
-// record in smem, and only the 16-B chunks holding written bytes go back.
-// Requires 32*stride % 16 == 0 and a 16-B aligned buffer (host checks).
-constexpr int kTileWarps = 8;
-constexpr int kTileMaxBytes = 32 * 256;  // records up to 256 B
 
-template <int XB, int YB>
-__global__ void __launch_bounds__(kTileWarps * 32) k_update_tile(uint8_t* __restrict__ buf, uint64_t n, uint32_t stride,
-                                                                const RecOps ops, double dt, uint8_t math) {
-    using TX = typename std::conditional<Ieee<XB>::w == 64, uint64_t,
-                                         typename std::conditional<Ieee<XB>::w == 32, uint32_t, uint16_t>::type>::type;
-    using TY = typename std::conditional<Ieee<YB>::w == 64, uint64_t,
-                                         typename std::conditional<Ieee<YB>::w == 32, uint32_t, uint16_t>::type>::type;
-    extern __shared__ __align__(16) uint8_t tsm[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* tile = tsm + warp * (32 * stride + 16);
-    // written byte ranges inside a record: [wlo[o], whi[o])
-    uint32_t wlo[2], whi[2];
-    for (int o = 0; o < 2; ++o) {
-        wlo[o] = ops.xoff[o];
-        whi[o] = o < ops.n ? ops.xoff[o] + ops.arity[o] * (Ieee<XB>::w / 8) : 0;
-    }
-    const uint64_t ntiles = (n + 31) / 32;
-    for (uint64_t t = blockIdx.x * uint64_t(kTileWarps) + warp; t < ntiles; t += uint64_t(gridDim.x) * kTileWarps) {
-        const uint64_t r0 = t * 32;
-        const uint32_t recs = n - r0 < 32 ? uint32_t(n - r0) : 32u;
-        const uint32_t bytes = recs * stride;
-        uint8_t* g = buf + r0 * stride;
-        const uint32_t chunks = bytes / 16;  // tail (< 16 B) handled bytewise
-        for (uint32_t c = lane; c < chunks; c += 32)
-            reinterpret_cast<uint4*>(tile)[c] = reinterpret_cast<const uint4*>(g)[c];
-        for (uint32_t b = chunks * 16 + lane; b < bytes; b += 32) tile[b] = g[b];
-        __syncwarp();
-        if (lane < recs) {
-            uint8_t* rec = tile + lane * stride;
-            bool bad = false;
-            TX xv[2][3], out[2][3];
-            TY yv[2][3];
-#pragma unroll
-            for (int o = 0; o < 2; ++o)
-#pragma unroll
-                for (int l = 0; l < 3; ++l)
-                    if (o < ops.n && l < ops.arity[o]) {
-                        memcpy(&xv[o][l], rec + ops.xoff[o] + l * sizeof(TX), sizeof(TX));
-                        memcpy(&yv[o][l], rec + ops.yoff[o] + l * sizeof(TY), sizeof(TY));
-                        bad |= Ieee<XB>::nan(xv[o][l]) | Ieee<YB>::nan(yv[o][l]);
-                        double v;
-                        if (math == MATH_FP64_EXACT)
-                            v = __dadd_rn(Ieee<XB>::f64(xv[o][l]), __dmul_rn(Ieee<YB>::f64(yv[o][l]), dt));
-                        else
-                            v = double(__fadd_rn(float(Ieee<XB>::f64(xv[o][l])),
-                                                 __fmul_rn(float(Ieee<YB>::f64(yv[o][l])), float(dt))));
-                        bad |= isnan(v);
-                        if (ops.op[o] == OP_AXPY_CLAMP0 && v < 0.0) v = 0.0;
-                        out[o][l] = TX(Ieee<XB>::from(v));
-                    }
-            if (bad) {
-                const LaneFmt fx = XB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<XB>::w);
-                const LaneFmt fy = YB == B_BF16 ? fmt_bf16() : fmt_native(Ieee<YB>::w);
-#pragma unroll
-                for (int o = 0; o < 2; ++o)
-#pragma unroll
-                    for (int l = 0; l < 3; ++l)
-                        if (o < ops.n && l < ops.arity[o])
-                            out[o][l] = TX(axpy_lane(xv[o][l], fx, yv[o][l], fy, dt, ops.op[o], math));
-            }
-#pragma unroll
-            for (int o = 0; o < 2; ++o)
-#pragma unroll
-                for (int l = 0; l < 3; ++l)
-                    if (o < ops.n && l < ops.arity[o]) memcpy(rec + ops.xoff[o] + l * sizeof(TX), &out[o][l], sizeof(TX));
-        }
-        __syncwarp();
-        // store back only the chunks that hold written bytes
-        for (uint32_t c = lane; c < chunks; c += 32) {
-            const uint32_t lo = c * 16, hi = lo + 16;
-            bool hit = false;
-            for (uint32_t r = lo / stride; r * stride < hi && r < recs; ++r)
-#pragma unroll
-                for (int o = 0; o < 2; ++o) {
-                    const uint32_t a = r * stride + wlo[o], b = r * stride + whi[o];
-                    hit |= o < ops.n && a < hi && b > lo;
-                }
-            if (hit) reinterpret_cast<uint4*>(g)[c] = reinterpret_cast<const uint4*>(tile)[c];
-        }
-        for (uint32_t b = chunks * 16 + lane; b < bytes; b += 32) g[b] = tile[b];
-        __syncwarp();
-    }
-}
-
-cudaError_t launch_update_tile(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops, double dt,
-                               uint8_t math, cudaStream_t st);
 
 // ----------------------------------------------------------------- force
 // dw_dr (sph.cpp:26-33), left-to-right binary64.
@@ -1073,26 +980,6 @@ cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint3
     }
     SFB_M(B_F64, B_F64) SFB_M(B_F32, B_F32) SFB_M(B_F16, B_F16) SFB_M(B_BF16, B_BF16) SFB_M(B_F64, B_F32)
 #undef SFB_M
-    return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_update_tile(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops, double dt,
-                               uint8_t math, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
-    if (stride > kTileMaxBytes / 32 || (32 * stride) % 16 || (reinterpret_cast<uintptr_t>(buf) & 15))
-        return cudaErrorInvalidValue;
-    const size_t smem = size_t(kTileWarps) * (32 * stride + 16);
-    const uint64_t ntiles = (n + 31) / 32;
-    const unsigned blocks = unsigned(std::min<uint64_t>((ntiles + kTileWarps - 1) / kTileWarps, uint64_t(num_sms()) * 8));
-    uint8_t* b = static_cast<uint8_t*>(buf);
-#define SFB_T(XB, YB)                                                                                    \
-    if (xb == XB && yb == YB) {                                                                          \
-        cudaFuncSetAttribute(k_update_tile<XB, YB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
-        k_update_tile<XB, YB><<<blocks, kTileWarps * 32, smem, st>>>(b, n, stride, ops, dt, math);       \
-        return cudaGetLastError();                                                                       \
-    }
-    SFB_T(B_F64, B_F64) SFB_T(B_F32, B_F32) SFB_T(B_F16, B_F16) SFB_T(B_BF16, B_BF16) SFB_T(B_F64, B_F32)
-#undef SFB_T
     return cudaErrorInvalidValue;
 }
 

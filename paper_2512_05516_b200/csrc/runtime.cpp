@@ -157,15 +157,9 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
                 ops.arity[i] = kp.s[i].dst.arity;
                 ops.op[i] = kp.s[i].op;
             }
-            const uint32_t stride = uint32_t(rb / 8);
-            if (stride <= 256 && (32 * stride) % 16 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0)
-                check_cuda(launch_update_tile(kp.s[0].dst.fmt.base, kp.s[0].aux.fmt.base, p, v.count, stride, ops, dt,
-                                              kp.math, st),
-                           "aos tile update launch");
-            else
-                check_cuda(launch_update_rec_multi(kp.s[0].dst.fmt.base, kp.s[0].aux.fmt.base, p, v.count, stride, ops,
-                                                   dt, kp.math, st),
-                           "aos update launch");
+            check_cuda(launch_update_rec_multi(kp.s[0].dst.fmt.base, kp.s[0].aux.fmt.base, p, v.count,
+                                               uint32_t(rb / 8), ops, dt, kp.math, st),
+                       "aos update launch");
             count_launches(1);
             return;
         }

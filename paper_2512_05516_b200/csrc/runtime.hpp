@@ -21,8 +21,6 @@ cudaError_t launch_update_rec(int xb, int yb, int arity, void* buf, uint64_t n, 
                               uint32_t yoff, double dt, uint8_t op, uint8_t math, cudaStream_t st);
 cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops,
                                     double dt, uint8_t math, cudaStream_t st);
-cudaError_t launch_update_tile(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops, double dt,
-                               uint8_t math, cudaStream_t st);
 cudaError_t launch_update_soa(int xb, int yb, void* x, const void* y, uint64_t n, double dt, uint8_t op, uint8_t math,
                               cudaStream_t st);
 cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate);

@@ -15,7 +15,8 @@ REF_SO = os.path.join(os.path.dirname(O.__file__), "_ref", "libsoaforge_ref.so")
 
 
 def _bind(lib):
-    for name in ["sf_run_bench_kernels", "sf_run_bench_pipeline", "sf_run_study_truncation", "sf_run_validate"]:
+    for name in ["sf_run_bench_kernels", "sf_run_bench_pipeline", "sf_run_study_truncation", "sf_run_validate",
+                 "sf_run_bench_transform"]:
         getattr(lib, name).argtypes = [C.c_void_p, C.POINTER(C.c_char_p)]
         getattr(lib, name).restype = C.c_int
     lib.sf_config_create.argtypes = [C.POINTER(C.c_void_p)]
@@ -99,3 +100,30 @@ def test_truncation_study(libs):  # test_capi.cpp:89-101
     assert text.startswith("# soaforge v") and "\n64,0,0\n" in text
     _, rtext = run(ref, "sf_run_study_truncation", **args)
     assert text == rtext  # binary64 density+force: every digit agrees
+
+
+def test_validate_dump_matches_reference(libs):
+    """validate --dump hex-dumps the first neighbour buffer of the stored state
+    (bench.cpp:193-202, :587-600): identical bytes on both libraries."""
+    ours, ref = libs
+    args = dict(ints=[("particles", 128), ("threads", 1), ("dump", 1)])
+    s1, r1 = run(ours, "sf_run_validate", **args)
+    s2, r2 = run(ref, "sf_run_validate", **args)
+    assert s1 == 0 and s2 == 0
+    hex1 = [l for l in r1.splitlines() if not l.startswith(("PASS", "FAIL"))]
+    hex2 = [l for l in r2.splitlines() if not l.startswith(("PASS", "FAIL"))]
+    assert hex1 and hex1 == hex2
+
+
+def test_bench_transform_rows(libs):
+    ours, ref = libs
+    args = dict(ints=[("particles", 1024)], strs=[("precision", "32,16"), ("kernels", "drift,kick")])
+    s1, t1 = run(ours, "sf_run_bench_transform", **args)
+    s2, t2 = run(ref, "sf_run_bench_transform", **args)
+    assert s1 == 0 and s2 == 0
+    r1, r2 = csv_rows(t1), csv_rows(t2)
+    assert [(a["kernel"], a["placement"], a["precision"]) for a in r1] == \
+           [(b["kernel"], b["placement"], b["precision"]) for b in r2]
+    for a, b in zip(r1, r2):  # the byte model column agrees; device rows carry a GPU time
+        if a["placement"] == "device":
+            assert a["bytes_moved"] == b["bytes_moved"] and float(a["convert_s"]) > 0
