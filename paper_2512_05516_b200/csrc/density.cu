@@ -155,9 +155,9 @@ __global__ void __launch_bounds__(256) k_pairs_r(const typename Pack<P>::T* __re
         auto pair = [&](const float4 pj, int j) {
             const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
             const float r2 = dx * dx + dy * dy + dz * dz;
-            const float hij = 0.5f * (pi.w + pj.w);
-            if (r2 < 4.0f * hij * hij) {
-                const float inv_h = __frcp_rn(hij);
+            const float s = pi.w + pj.w;  // 2 h_ij: the support radius
+            if (r2 < s * s) {             // == r2 < 4 h_ij^2 bit for bit (power-of-two rescale)
+                const float inv_h = 2.0f * __frcp_rn(s);
                 const float q = sqrtf(r2) * inv_h;
                 if (q < 2.0f) acc += __ldg(mass + j) * w_f32(q, inv_h);
             }
