@@ -303,8 +303,8 @@ def b200_arm(args):
         # parity of the e2e result with the device-resident result
         got = torch.from_numpy(hs.numpy()[: dst_v.nbytes].copy()).cuda()
         ok = bool(torch.equal(got, out.data[: dst_v.nbytes]))
-        e2e = {"value": n * world / float(s_t.item()), "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"],
-               "d2h_bytes_per_step": m["d2h_bytes"], "chunk_particles": args.chunk, "matches_device_result": ok,
+        e2e = {"value": n * world / float(s_t.item()), "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"] * world,
+               "d2h_bytes_per_step": m["d2h_bytes"] * world, "chunk_particles": args.chunk, "matches_device_result": ok,
                "path": "sf_b200_run_host(mode 2): pinned AoS, whole records H2D || k_gather_warp (fused drift) || "
                        "D2H SoA, 3-stream chunk pipeline"}
         hb.free()
