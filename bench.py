@@ -275,7 +275,7 @@ def b200_arm(args):
     peak, peak_kind = peaks()
     achieved = ALG_BYTES * n / (ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_kind": peak_kind, "kernel": "k_gather_tiled (fused gather+drift, %s)" % prec_name,
+                "peak_kind": peak_kind, "kernel": "k_gather_warp<ProcXV> (fused gather+drift, %s)" % prec_name,
                 "algorithmic_bytes_per_particle": ALG_BYTES,
                 "traffic": traffic_from_profiles("gather_drift_%s" % args.prec)}
 

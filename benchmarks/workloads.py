@@ -138,7 +138,7 @@ def c3(args, peak, peak_kind):
     ms = out["fp32"]["density_ms"]
     rl = {"bound": "compute (FP32 + MUFU)", "achieved": out["fp32"]["hbm_GBps_algorithmic"], "peak": peak,
           "unit": "GB/s", "frac": out["fp32"]["hbm_GBps_algorithmic"] / peak, "peak_kind": peak_kind,
-          "kernel": "k_density_cells (fp32)", "algorithmic_bytes_per_particle": 24, "traffic": None}
+          "kernel": "k_pairs_r (fp32, reach 2)", "algorithmic_bytes_per_particle": 24, "traffic": None}
     if out["fp32"]["pairs_in_support"]:
         rl["pairs_per_s"] = out["fp32"]["pairs_in_support"] / (ms * 1e-3)
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": rl,
@@ -238,7 +238,7 @@ def c5(args, peak, peak_kind, world, rank, group=None):
     phases["density_sub"] = [sub]
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
             "roofline": {"bound": "compute (density)", "achieved": None, "peak": peak, "unit": "GB/s",
-                         "frac": None, "kernel": "k_density_cells + k_convert(kick/drift)"},
+                         "frac": None, "kernel": "k_pairs_r + k_update_soa (kick/drift)"},
             "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + kick/drift sharded by cell "
                                    "with NCCL halo exchange" % (n >> 20), "particles_total": n,
                        "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},

@@ -290,6 +290,3 @@ ForcePlan plan_force(const View& v, uint64_t bs, int per_access) {
 
 }  // namespace sfb
 
-namespace sfb {
-
-}  // namespace sfb
