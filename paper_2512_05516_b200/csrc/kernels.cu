@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -295,7 +296,7 @@ __device__ __forceinline__ uint64_t axpy_ieee(uint64_t xq, uint64_t yq, double d
 // the shared-memory reads nearly conflict-free), writes each SoA stream's
 // slice into a per-warp staging area, and the warp stores the slice with
 // coalesced 16-B vector stores.
-constexpr int kWStages = 4;
+constexpr int kWStages = 4;  // default ring depth (GatherPlan::stages)
 
 // Fast path: every lane of stream g for this lane's records, IEEE formats
 // known at compile time (view.cpp fast_kind).
@@ -552,16 +553,16 @@ __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ 
                                                         uint64_t src_bytes) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * kWStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * int(P.stages);
     const uint32_t stage_bytes = (P.tile_bytes + 16 + 15) & ~15u;   // +16: funnel-shift overread pad
-    uint8_t* stages = smem + 128 * ((warps * kWStages * 8 + 127) / 128) +
-                      size_t(warp) * (kWStages * stage_bytes + P.out_bytes);
-    uint8_t* out = stages + kWStages * stage_bytes;
+    uint8_t* stages = smem + 128 * ((warps * int(P.stages) * 8 + 127) / 128) +
+                      size_t(warp) * (int(P.stages) * stage_bytes + P.out_bytes);
+    uint8_t* out = stages + int(P.stages) * stage_bytes;
     const uint64_t ntiles = (P.count + P.tile_recs - 1) / P.tile_recs;
     const uint64_t gw = uint64_t(blockIdx.x) * warps + warp, tw = uint64_t(gridDim.x) * warps;
 
     if (lane == 0) {
-        for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < int(P.stages); ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -574,14 +575,14 @@ __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ 
         if (bulk) tma_bulk_g2s(stages + s * stage_bytes, src + off, bulk, &bars[s]);
     };
     if (lane == 0)
-        for (int s = 0; s < kWStages; ++s)
+        for (int s = 0; s < int(P.stages); ++s)
             if (gw + s * tw < ntiles) issue(gw + s * tw, s);
 
     uint32_t k = 0;
     for (uint64_t t = gw; t < ntiles; t += tw, ++k) {
-        const int s = int(k % kWStages);
+        const int s = int(k % int(P.stages));
         uint8_t* tile = stages + s * stage_bytes;
-        mbar_wait(&bars[s], (k / kWStages) & 1);
+        mbar_wait(&bars[s], (k / int(P.stages)) & 1);
         const uint64_t rec0 = t * P.tile_recs;
         const uint32_t recs = uint32_t(min(uint64_t(P.tile_recs), P.count - rec0));
         if (recs < P.tile_recs) {  // the <16-byte tail the bulk copy skipped
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ 
         }
         Proc::tile(tile, P, lane, recs, rec0, out, dst);
         if (lane == 0) {
-            const uint64_t tn = t + uint64_t(kWStages) * tw;
+            const uint64_t tn = t + uint64_t(int(P.stages)) * tw;
             if (tn < ntiles) issue(tn, s);
         }
     }
@@ -904,17 +905,26 @@ cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cud
 }
 
 static size_t gather_warp_bytes(const GatherPlan& p) {
-    return size_t(kWStages) * ((p.tile_bytes + 16 + 15) & ~15u) + p.out_bytes;
+    return size_t(p.stages) * ((p.tile_bytes + 16 + 15) & ~15u) + p.out_bytes;
 }
 
-cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
                           int /*ctas_per_sm*/) {
-    if (p.count == 0 || p.n == 0) return cudaSuccess;
+    if (plan.count == 0 || plan.n == 0) return cudaSuccess;
+    GatherPlan p = plan;
+    // tuning overrides (ring depth per warp, warps per CTA) for sweeps
+    p.stages = uint8_t(std::min(8, std::max(2, env_int("SFB_GATHER_STAGES", kWStages))));
     const size_t per_warp = gather_warp_bytes(p);
     const size_t budget = 220 * 1024;
     int warps = int(std::min<size_t>(16, (budget - 1024) / per_warp));
+    warps = std::min(warps, std::max(1, env_int("SFB_GATHER_WARPS", warps)));
     if (warps < 1) return cudaErrorInvalidValue;
-    const size_t smem = 128 * ((size_t(warps) * kWStages * 8 + 127) / 128) + size_t(warps) * per_warp;
+    const size_t smem = 128 * ((size_t(warps) * p.stages * 8 + 127) / 128) + size_t(warps) * per_warp;
     const uint64_t ntiles = (p.count + p.tile_recs - 1) / p.tile_recs;
     const int ctas = int(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
     const uint64_t want = (ntiles + warps - 1) / warps;

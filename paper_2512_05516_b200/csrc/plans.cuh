@@ -69,6 +69,7 @@ struct GatherPlan {
     uint32_t tile_bytes = 0;  // tile_recs * record_bits / 8
     uint32_t out_bytes = 0;   // per-warp SoA staging (largest stream slice)
     uint8_t proc = 0;         // per-tile policy (PROC_*), chosen by view.cpp proc_kind
+    uint8_t stages = 4;       // TMA ring depth per warp (set at launch)
     uint8_t math = MATH_FP64_EXACT;
     double dt = 0;
     GStream s[kMaxStreams];
