@@ -168,3 +168,34 @@ def test_plain_c_consumer_links_and_runs(tmp_path):
                     "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0 and "capi ok" in out.stdout, out.stdout
+
+
+@pytest.mark.parametrize("prec,exclude,want", [
+    (api.SF_PREC_STORED, "", {"x": 64, "id": 64, "v": 32, "rho": 32}),
+    (api.SF_PREC_NATIVE, "", {"x": 64, "id": 64, "v": 32, "rho": 32}),
+    (16, "", {"x": 16, "id": 64, "v": 16, "rho": 16}),
+    (16, "x", {"x": 64, "id": 64, "v": 16, "rho": 16}),
+    (20, "", {"x": 32, "id": 64, "v": 32, "rho": 32}),           # truncated T held in its base width
+    (api.SF_PREC_PACKED + 20, "", {"x": 20, "id": 64, "v": 20, "rho": 20}),
+    (api.SF_PREC_PACKED + 40, "v", {"x": 40, "id": 64, "v": 32, "rho": 40}),
+    (api.SF_PREC_BF16, "x,rho", {"x": 64, "id": 64, "v": 16, "rho": 32}),
+])
+def test_view_precision_codes(prec, exclude, want):
+    """Lane widths chosen by each precision code (include/soaforge_b200.h)."""
+    v = api.View(api.Schema.default(), 10, "aos", None, prec, exclude)
+    for f, w in want.items():
+        assert v.lane(f)[2] == w, f
+
+
+def test_view_rejects_bad_arguments():
+    S = api.Schema.default()
+    for bad in [2, 6, 65, 999, 1006, 1065]:
+        with pytest.raises(L.SfInvalidArg):
+            api.View(S, 10, "aos", None, bad)
+    with pytest.raises(L.SfInvalidArg):
+        api.View(S, 10, "soa", "no_such_kernel")
+    h = C.c_void_p()
+    assert L.lib().sf_b200_view_create(S.handle, None, 7, 0, None, 10, C.byref(h)) == L.SF_INVALID_ARG
+    v = api.View(S, 10, "soa", "drift", 16)
+    with pytest.raises(L.SfInvalidArg):
+        v.lane("rho")  # not in the drift access set
