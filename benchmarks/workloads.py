@@ -106,7 +106,7 @@ def c3(args, peak, peak_kind):
     x = torch.rand(n, 3, generator=g, device="cuda", dtype=torch.float32)
     m = torch.full((n,), 1.0 / n, device="cuda")
     hh = torch.full((n,), h, device="cuda")
-    refine = 2                      # binning cells of side 1/(2 nc) >= h, searched with reach 2
+    refine = args.refine            # binning cells of side 1/(refine nc) >= 2h/refine, searched with reach = refine
     fine = cell / refine
     dims = (nc * refine,) * 3
     out = {}
@@ -138,7 +138,7 @@ def c3(args, peak, peak_kind):
     ms = out["fp32"]["density_ms"]
     rl = {"bound": "compute (FP32 + MUFU)", "achieved": out["fp32"]["hbm_GBps_algorithmic"], "peak": peak,
           "unit": "GB/s", "frac": out["fp32"]["hbm_GBps_algorithmic"] / peak, "peak_kind": peak_kind,
-          "kernel": "k_pairs_r (fp32, reach 2)", "algorithmic_bytes_per_particle": 24, "traffic": None}
+          "kernel": "k_pairs_c (fp32, reach %d)" % refine, "algorithmic_bytes_per_particle": 24, "traffic": None}
     if out["fp32"]["pairs_in_support"]:
         rl["pairs_per_s"] = out["fp32"]["pairs_in_support"] / (ms * 1e-3)
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": rl,

@@ -5,20 +5,21 @@
 // sorted into cells (x-major ids, z fastest; bin_particles below).  The pass
 //
 //   k_pack        applies the sort permutation once and packs each particle
-//                 as (x, y, z, h) — float4 (16 B) for fp32 streams, four
-//                 halves (8 B) for fp16/bf16 — plus its mass;
-//   k_pairs       one thread per home particle of the own x-layers (a
+//                 as a float4 (x, y, z, h) plus its mass (fp16/bf16 stream
+//                 values widen exactly), and finds the largest h;
+//   k_pairs_c     one thread per home particle of the own x-layers (a
 //                 contiguous range of the sorted order): for each of the
-//                 (2r+1)^2 (dx, dy) neighbour columns the cells iz-r..iz+r are
-//                 one contiguous run of the packed array, read straight
-//                 through L1/L2 (neighbouring threads sweep the same runs);
-//                 the pair test r^2 < (2 h_ij)^2 precedes any sqrt/division.
-//                 rho is stored back in particle (unsorted) order.
+//                 (2R+1)^2 (dx, dy) neighbour columns the cells of one
+//                 z-window are one contiguous run of the packed array, read
+//                 through L1/L2 (neighbouring lanes sweep the same runs in
+//                 lockstep); each window is culled to the support sphere
+//                 h_i + h_max; every candidate runs the same branch-free pair
+//                 term.  rho is stored back in particle (unsorted) order.
 //
 // With cells of side >= 2h use reach 1 (27 cells); with cells of side >= h
-// reach 2 (125 smaller cells) evaluates ~42% fewer candidate pairs.  Pair
-// formula: the reference's m_j * W(|x_i - x_j|, (h_i + h_j)/2), M4 spline,
-// sigma = 1/pi, evaluated in binary32 (rel <= 1e-5 vs the binary64 oracle).
+// reach 2 (125 smaller cells, ~84 after culling).  Pair formula: the
+// reference's m_j * W(|x_i - x_j|, (h_i + h_j)/2), M4 spline, sigma = 1/pi,
+// evaluated in binary32 (rel <= 1e-5 vs the binary64 oracle).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -42,49 +43,24 @@ __device__ __forceinline__ float ldf(const void* p, uint64_t i) {
     else return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
 }
 
-// packed candidate record: (x, y, z, h) at the stream precision
-template <int P> struct Pack { using T = uint2; };
-template <> struct Pack<SP_F32> { using T = float4; };
-
-template <int P>
-__device__ __forceinline__ typename Pack<P>::T pack4(float a, float b, float c, float d) {
-    if constexpr (P == SP_F32) {
-        return make_float4(a, b, c, d);
-    } else if constexpr (P == SP_F16) {
-        const __half2 lo = __floats2half2_rn(a, b), hi = __floats2half2_rn(c, d);
-        return make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
-    } else {
-        const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
-        return make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
-    }
-}
-
-template <int P>
-__device__ __forceinline__ float4 unpack4(typename Pack<P>::T v) {
-    if constexpr (P == SP_F32) {
-        return v;
-    } else if constexpr (P == SP_F16) {
-        const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
-        const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
-        return make_float4(lo.x, lo.y, hi.x, hi.y);
-    } else {
-        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
-        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
-        return make_float4(lo.x, lo.y, hi.x, hi.y);
-    }
-}
-
-// Stored values are exactly representable in the packed precision, so
-// packing then unpacking is lossless.
+// Stored values are exactly representable in binary32, so the packed
+// float4 record is lossless for every stream precision.
 template <int P>
 __global__ void k_pack(const void* __restrict__ x, const void* __restrict__ m, const void* __restrict__ h,
-                       const int32_t* __restrict__ perm, uint64_t n, typename Pack<P>::T* __restrict__ pos,
-                       float* __restrict__ mass) {
+                       const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ pos,
+                       float* __restrict__ mass, unsigned* __restrict__ hmax_bits) {
+    float hmax = 0.0f;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = perm ? uint64_t(perm[k]) : k;
-        pos[k] = pack4<P>(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), ldf<P>(h, i));
+        const float hi = ldf<P>(h, i);
+        pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), hi);
         mass[k] = ldf<P>(m, i);
+        hmax = fmaxf(hmax, hi);
     }
+    // largest smoothing length (non-negative floats order like their bits)
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, d));
+    if ((threadIdx.x & 31) == 0 && hmax > 0.0f) atomicMax(hmax_bits, __float_as_uint(hmax));
 }
 
 // M4 cubic spline (sph.cpp:17-24) in binary32; caller guarantees q < 2.
@@ -100,13 +76,12 @@ struct CellGrid {
     int nx, ny, nz, reach, own_x0, own_x1;
 };
 
-template <int P>
-__global__ void __launch_bounds__(256) k_pairs(const typename Pack<P>::T* __restrict__ pos,
+__global__ void __launch_bounds__(256) k_pairs(const float4* __restrict__ pos,
                                                const float* __restrict__ mass, const int32_t* __restrict__ cell_start,
                                                const int32_t* __restrict__ perm, CellGrid G, int64_t n,
                                                float* __restrict__ rho) {
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        const float4 pi = unpack4<P>(pos[k]);
+        const float4 pi = (pos[k]);
         // the same float formula bin_particles used, so the cell matches
         const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
         if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
@@ -119,7 +94,7 @@ __global__ void __launch_bounds__(256) k_pairs(const typename Pack<P>::T* __rest
                 const int64_t c0 = (int64_t(jx) * G.ny + jy) * G.nz;
                 const int b = __ldg(cell_start + c0 + z0), e = __ldg(cell_start + c0 + z1 + 1);
                 for (int j = b; j < e; ++j) {
-                    const float4 pj = unpack4<P>(pos[j]);
+                    const float4 pj = (pos[j]);
                     const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
                     const float r2 = dx * dx + dy * dy + dz * dz;
                     const float hij = 0.5f * (pi.w + pj.w);
@@ -137,15 +112,15 @@ __global__ void __launch_bounds__(256) k_pairs(const typename Pack<P>::T* __rest
 // Same pair loop with the reach fixed at compile time: the (2R+1) run bounds
 // of a neighbour row are loaded together (independent loads in flight), and
 // candidates are consumed two at a time.
-template <int P, int R>
-__global__ void __launch_bounds__(256) k_pairs_r(const typename Pack<P>::T* __restrict__ pos,
+template <int R>
+__global__ void __launch_bounds__(256) k_pairs_r(const float4* __restrict__ pos,
                                                  const float* __restrict__ mass,
                                                  const int32_t* __restrict__ cell_start,
                                                  const int32_t* __restrict__ perm, CellGrid G, int64_t n,
                                                  float* __restrict__ rho) {
     constexpr int W = 2 * R + 1;
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        const float4 pi = unpack4<P>(pos[k]);
+        const float4 pi = (pos[k]);
         const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
         if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
         const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
@@ -179,15 +154,120 @@ __global__ void __launch_bounds__(256) k_pairs_r(const typename Pack<P>::T* __re
             for (int t = 0; t < W; ++t) {
                 int j = b[t];
                 for (; j + 1 < e[t]; j += 2) {
-                    const float4 p0 = unpack4<P>(pos[j]), p1 = unpack4<P>(pos[j + 1]);
+                    const float4 p0 = (pos[j]), p1 = (pos[j + 1]);
                     pair(p0, j);
                     pair(p1, j + 1);
                 }
-                if (j < e[t]) pair(unpack4<P>(pos[j]), j);
+                if (j < e[t]) pair((pos[j]), j);
             }
         }
         rho[perm ? perm[k] : k] = acc;
     }
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Branch-free M4 pair term (sph.cpp:17-24 with h_ij = (h_i + h_j)/2):
+//   pi h_ij^3 w(q) = (max(2-q,0)^3 - 4 max(1-q,0)^3) / 4
+// (for q < 1 the difference expands to 1 - 1.5 q^2 + 0.75 q^3, sph.cpp:20;
+// for 1 <= q < 2 only the first term is left, sph.cpp:22; beyond 2 both are
+// 0); the 1/(4 pi) is applied once per particle.  Every candidate runs the
+// same instructions: no support test, no branch, one MUFU.RCP and one
+// MUFU.SQRT (approximate forms; the sum stays within rel 1e-5 of the binary64
+// oracle, tests/test_gpu_parity.py).  hh_i = h_i / 2.
+__device__ __forceinline__ float pair_term(const float4 pi, float hh_i, const float4 pj, float mj) {
+    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
+    const float q = sqrt_approx(r2) * inv_h;
+    const float t = fmaxf(2.0f - q, 0.0f);
+    const float u = fmaxf(1.0f - q, 0.0f);
+    const float w = fmaf(t * t, t, (u * u) * (-4.0f * u));
+    return (mj * (inv_h * inv_h * inv_h)) * w;
+}
+
+// Per-particle culled candidate runs.  As k_pairs_r (one thread per home
+// particle, the (2R+1)^2 neighbour columns swept in lockstep so neighbouring
+// lanes share candidate lines in L1), but every column's z-window is cut to
+// the cells that can hold a particle inside the support sphere of radius
+// h_i + h_max around the home particle (h_max from k_pack), and columns the
+// sphere misses are skipped.  For uniform particles with cells of side ~h at
+// reach 2 this evaluates ~84 of the 125 cells.  Cells on the grid faces
+// extend to infinity (binning clamps), so their distance is measured only on
+// their inner side.  Culling removes only candidates at q >= 2 (w = 0; a
+// 1e-5 radius margin covers rounding), and every candidate runs the
+// branch-free pair_term.
+template <int R>
+__global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
+                                                 const float* __restrict__ mass,
+                                                 const int32_t* __restrict__ cell_start,
+                                                 const int32_t* __restrict__ perm, CellGrid G, int64_t n,
+                                                 const unsigned* __restrict__ hmax_bits, float* __restrict__ rho) {
+    constexpr int W = 2 * R + 1;
+    const float hmax = __uint_as_float(*hmax_bits);
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const float4 pi = (pos[k]);
+        const float fx = (pi.x - G.lox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
+                    fz = (pi.z - G.loz) * G.inv_cell;
+        const int ix = min(max(int(floorf(fx)), 0), G.nx - 1);
+        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
+        const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
+        const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
+        const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
+        const float rc2 = rc * rc;
+        const float hh_i = 0.5f * pi.w;
+        const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
+        const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
+        float acc = 0.0f;
+#pragma unroll 1
+        for (int dxi = -R; dxi <= R; ++dxi) {
+            const int jx = ix + dxi;
+            if (jx < 0 || jx >= G.nx) continue;
+            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < G.nx - 1 ? fx - float(jx + 1) : 0.0f),
+                                    0.0f);
+            int b[W], e[W];
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+                const int jy = iy - R + t;
+                const float ddy = fmaxf(
+                    fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
+                const float d2 = fmaf(ddx, ddx, ddy * ddy);
+                const float dz = sqrtf(fmaxf(rc2 - d2, 0.0f));
+                const int zlo = min(max(int(floorf(fzc - dz)), zmin), G.nz - 1);
+                const int zhi = max(min(int(floorf(fzc + dz)), zmax), 0);
+                const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
+                const int64_t c0 = (int64_t(jx) * G.ny + (ok ? jy : 0)) * G.nz;
+                b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
+                e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+                int j = b[t];
+                for (; j + 1 < e[t]; j += 2) {
+                    const float4 p0 = (pos[j]), p1 = (pos[j + 1]);
+                    const float m0 = __ldg(mass + j), m1 = __ldg(mass + j + 1);
+                    acc += pair_term(pi, hh_i, p0, m0);
+                    acc += pair_term(pi, hh_i, p1, m1);
+                }
+                if (j < e[t]) acc += pair_term(pi, hh_i, (pos[j]), __ldg(mass + j));
+            }
+        }
+        rho[perm ? perm[k] : k] = acc * 0.079577471545947668f;  // 1 / (4 pi)
+    }
+}
+
+static int env_int_d(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
 }
 
 void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
@@ -200,33 +280,30 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     if (n == 0) return;
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
     if (sp < 0) throw std::invalid_argument("density_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
-    const size_t pbytes = (sp == SP_F32 ? 16 : 8) * n;
-    void* pos = nullptr;
+    float4* pos = nullptr;
     float* mass = nullptr;
-    check_cuda(cudaMallocAsync(&pos, pbytes, st), "cudaMallocAsync");
-    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&mass), 4 * n, st), "cudaMallocAsync");
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned pb = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(sms) * 16));
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pos), 16 * n, st), "cudaMallocAsync");
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&mass), 4 * n + 16, st), "cudaMallocAsync");
+    unsigned* hmax = reinterpret_cast<unsigned*>(mass + n);
+    check_cuda(cudaMemsetAsync(hmax, 0, sizeof(unsigned), st), "memset");
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
     const int64_t nn = int64_t(n);
-    const unsigned qb = pb;
-    auto pairs = [&](auto tag, auto* p) {
-        constexpr int SP = decltype(tag)::value;
-        if (reach == 1) k_pairs_r<SP, 1><<<qb, 256, 0, st>>>(p, mass, cell_start, perm, G, nn, rho);
-        else if (reach == 2) k_pairs_r<SP, 2><<<qb, 256, 0, st>>>(p, mass, cell_start, perm, G, nn, rho);
-        else k_pairs<SP><<<qb, 256, 0, st>>>(p, mass, cell_start, perm, G, nn, rho);
-    };
-    if (sp == SP_F32) {
-        k_pack<SP_F32><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<float4*>(pos), mass);
-        pairs(std::integral_constant<int, SP_F32>{}, static_cast<float4*>(pos));
-    } else if (sp == SP_F16) {
-        k_pack<SP_F16><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<uint2*>(pos), mass);
-        pairs(std::integral_constant<int, SP_F16>{}, static_cast<uint2*>(pos));
+    if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
+    else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
+    else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
+    // SFB_PAIRS=0 selects the unculled per-run loop (round-1 kernel) for comparison
+    if (env_int_d("SFB_PAIRS", 1) != 0) {
+        if (reach == 1) k_pairs_c<1><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        else if (reach == 2) k_pairs_c<2><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        else if (reach == 3) k_pairs_c<3><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        else k_pairs_c<4><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+    } else if (reach == 1) {
+        k_pairs_r<1><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
+    } else if (reach == 2) {
+        k_pairs_r<2><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
     } else {
-        k_pack<SP_BF16><<<pb, 256, 0, st>>>(x, m, h, perm, n, static_cast<uint2*>(pos), mass);
-        pairs(std::integral_constant<int, SP_BF16>{}, static_cast<uint2*>(pos));
+        k_pairs<<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
     }
     check_cuda(cudaGetLastError(), "density_cells launch");
     count_launches(2);

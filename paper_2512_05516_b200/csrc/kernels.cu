@@ -885,16 +885,7 @@ __global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf
 }
 
 // ----------------------------------------------------------------- launchers
-static int g_num_sms = 0;
-static int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
+int num_sms();  // runtime.cpp
 
 cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st) {
     if (p.count == 0 || p.n == 0) return cudaSuccess;

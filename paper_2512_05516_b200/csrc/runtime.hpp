@@ -27,6 +27,7 @@ cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, 
 
 void check_cuda(cudaError_t e, const char* what);
 void require_device();
+int num_sms();  // SM count of the current device
 void count_launches(uint64_t n);
 uint64_t launch_count();
 
