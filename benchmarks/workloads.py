@@ -238,7 +238,7 @@ def c5(args, peak, peak_kind, world, rank, group=None):
     phases["density_sub"] = [sub]
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
             "roofline": {"bound": "compute (density)", "achieved": None, "peak": peak, "unit": "GB/s",
-                         "frac": None, "kernel": "k_pairs_r + k_update_soa (kick/drift)"},
+                         "frac": None, "kernel": "k_pairs_c + k_update_soa (kick/drift)"},
             "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + kick/drift sharded by cell "
                                    "with NCCL halo exchange" % (n >> 20), "particles_total": n,
                        "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},

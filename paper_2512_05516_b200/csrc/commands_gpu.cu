@@ -83,6 +83,43 @@ State random_state(uint64_t n, uint64_t seed, double dt) {
     return s;
 }
 
+// load_initial_conditions_csv (sph.cpp:351-383): rows id,x0,x1,x2,v0,v1,v2,u,m,h;
+// blank lines, '#' comments and a header row starting with "id" are skipped;
+// rho = 1, P/cs from the EOS, a = du = 0, dt = the run's dt.  Same errors as
+// the reference: unreadable file / wrong column count -> runtime_error,
+// unparsable number -> std::stod's invalid_argument / out_of_range.
+State csv_state(const std::string& path, double dt) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open initial conditions file: " + path);
+    State s;
+    const double gamma = 5.0 / 3.0;
+    std::string line;
+    while (std::getline(in, line)) {
+        if (line.empty() || line[0] == '#') continue;
+        if (line.find_first_not_of(" \t") != std::string::npos && line.rfind("id", 0) == 0) continue;
+        std::istringstream row(line);
+        std::string cell;
+        std::vector<double> vals;
+        while (std::getline(row, cell, ',')) vals.push_back(std::stod(cell));
+        if (vals.size() != 10) throw std::runtime_error("initial conditions row must have 10 columns: " + line);
+        s.id.push_back(int64_t(vals[0]));
+        for (int l = 0; l < 3; ++l) s.x.push_back(vals[1 + l]);
+        for (int l = 0; l < 3; ++l) s.v.push_back(vals[4 + l]);
+        s.u.push_back(vals[7]);
+        s.m.push_back(vals[8]);
+        s.h.push_back(vals[9]);
+        s.rho.push_back(1.0);
+        const double P = (gamma - 1.0) * 1.0 * vals[7];  // eos(rho = 1, u), sph.cpp:42-46
+        s.P.push_back(P);
+        s.cs.push_back(std::sqrt(gamma * P / 1.0));
+        for (int l = 0; l < 3; ++l) s.a.push_back(0.0);
+        s.du.push_back(0.0);
+        s.dt.push_back(dt);
+        ++s.n;
+    }
+    return s;
+}
+
 const std::vector<double>* state_field(const State& s, const std::string& f) {
     if (f == "x") return &s.x;
     if (f == "v") return &s.v;
@@ -204,7 +241,6 @@ void validate_cfg(const RunConfig& c) {
         if (t < 7 || t > 64) throw std::invalid_argument("precision sweep value " + std::to_string(t) + " outside 7..64");
     if (!(c.latency_s >= 0) || !(c.bandwidth > 0))
         throw std::invalid_argument("interconnect model requires latency >= 0 and bandwidth > 0");
-    if (!c.ic_csv_path.empty()) throw std::invalid_argument("ic-csv initial conditions are not supported by the B200 build");
 }
 
 struct Population {
@@ -216,7 +252,8 @@ Population population(const RunConfig& c, int precision, bool all_fields = false
     validate_cfg(c);
     Population p;
     p.schema = load_schema(c, precision, all_fields);
-    p.ics = random_state(c.particles, c.seed, c.dt);
+    // bench.cpp:66-70: buffers are sized by the population, the CSV's row count when given
+    p.ics = c.ic_csv_path.empty() ? random_state(c.particles, c.seed, c.dt) : csv_state(c.ic_csv_path, c.dt);
     return p;
 }
 
@@ -231,7 +268,7 @@ std::string cmd_bench_kernels(const RunConfig& c) {
     out << header() << "kernel,layout,precision,particles,compute_s,speedup_vs_aos,checksum\n";
     for (int prec : sweep) {
         Population pop = population(c, prec);
-        const uint64_t n = c.particles;
+        const uint64_t n = pop.ics.n;
         View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, n);
         View nat = make_view(pop.schema, nullptr, Layout::AoS, kPrecNative, {}, n);
         View soa = make_view(pop.schema, nullptr, Layout::SoA, kPrecNative, {}, n);
@@ -247,8 +284,8 @@ std::string cmd_bench_kernels(const RunConfig& c) {
             const uint64_t sa = checksum_packed(nat, work_a.p);
             const double ts = gpu_seconds([&] { run_kernel(soa, work_s.p, k, c.dt, c.buffer_size, c.per_access, 0, nullptr); });
             const uint64_t ss = checksum_packed(soa, work_s.p);
-            out << k << ",aos," << prec << ',' << n << ',' << ta << ",1," << sa << '\n';
-            out << k << ",soa," << prec << ',' << n << ',' << ts << ',' << (ts > 0 ? ta / ts : 0.0) << ',' << ss << '\n';
+            out << k << ",aos," << prec << ',' << c.particles << ',' << ta << ",1," << sa << '\n';
+            out << k << ",soa," << prec << ',' << c.particles << ',' << ts << ',' << (ts > 0 ? ta / ts : 0.0) << ',' << ss << '\n';
         }
     }
     return out.str();
@@ -266,7 +303,7 @@ std::string cmd_bench_transform(const RunConfig& c) {
     out << header() << "kernel,placement,precision,particles,convert_s,bytes_moved,modeled_transfer_s,ratio\n";
     for (int prec : sweep) {
         Population pop = population(c, prec);
-        const uint64_t n = c.particles;
+        const uint64_t n = pop.ics.n;
         View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, n);
         DevBuf state(aos.total_bytes());
         store_state(pop.ics, aos, state.p);
@@ -280,8 +317,8 @@ std::string cmd_bench_transform(const RunConfig& c) {
             const double host_model = c.latency_s + double(host_bytes) / c.bandwidth;
             const double dev_model = c.latency_s + double(dev_bytes) / c.bandwidth;
             const std::string name = set.empty() ? "full" : set;
-            out << name << ",host," << prec << ',' << n << ",nan," << host_bytes << ',' << host_model << ",nan\n";
-            out << name << ",device," << prec << ',' << n << ',' << dev_convert << ',' << dev_bytes << ',' << dev_model
+            out << name << ",host," << prec << ',' << c.particles << ",nan," << host_bytes << ',' << host_model << ",nan\n";
+            out << name << ",device," << prec << ',' << c.particles << ',' << dev_convert << ',' << dev_bytes << ',' << dev_model
                 << ",nan\n";
         }
     }
@@ -314,7 +351,7 @@ struct VariantResult {
 // streaming moves each kernel's narrowed record set each way.
 VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const std::string& variant,
                               const std::string& mode, bool fault) {
-    const uint64_t n = c.particles;
+    const uint64_t n = pop.ics.n;
     View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, n);
     DevBuf state(aos.total_bytes());
     store_state(pop.ics, aos, state.p);
@@ -398,7 +435,7 @@ std::string cmd_study_truncation(const RunConfig& c) {
         if (t < 7 || t > 64) throw std::invalid_argument("sweep value " + std::to_string(t) + " outside 7..64");
     auto run_once = [&](int prec) {
         Population pop = population(c, prec);
-        View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, c.particles);
+        View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, pop.ics.n);
         DevBuf state(aos.total_bytes());
         store_state(pop.ics, aos, state.p);
         run_kernel(aos, state.p, "density", c.dt, c.buffer_size, c.per_access, 0, nullptr);
@@ -406,7 +443,7 @@ std::string cmd_study_truncation(const RunConfig& c) {
         return field_values(aos, download(aos, state.p), "a");
     };
     const std::vector<double> ref = run_once(64);
-    const uint64_t n = c.particles;
+    const uint64_t n = ref.size() / 3;
     double norm = 0;
     for (uint64_t i = 0; i < n; ++i)
         norm += std::sqrt(ref[3 * i] * ref[3 * i] + ref[3 * i + 1] * ref[3 * i + 1] + ref[3 * i + 2] * ref[3 * i + 2]);
@@ -514,7 +551,7 @@ std::string cmd_validate(const RunConfig& c, int& failures) {
         small.particles -= small.particles % small.buffer_size;
         if (small.particles == 0) small.particles = small.buffer_size;
         Population pop = population(small, 0);
-        const uint64_t n = small.particles;
+        const uint64_t n = pop.ics.n;
         View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, n);
         View soa = make_view(pop.schema, nullptr, Layout::SoA, kPrecStored, {}, n);
         View nat = make_view(pop.schema, nullptr, Layout::AoS, kPrecNative, {}, n);
@@ -537,7 +574,7 @@ std::string cmd_validate(const RunConfig& c, int& failures) {
         wide.particles -= wide.particles % wide.buffer_size;
         if (wide.particles == 0) wide.particles = wide.buffer_size;
         Population pop = population(wide, 64, true);
-        const uint64_t n = wide.particles, bs = wide.buffer_size;
+        const uint64_t n = pop.ics.n, bs = wide.buffer_size;
         View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, n);
         DevBuf st(aos.total_bytes());
         store_state(pop.ics, aos, st.p);
@@ -620,7 +657,7 @@ std::string cmd_validate(const RunConfig& c, int& failures) {
             }
         check("cross-variant-checksums", ok);
         if (c.dump) {
-            View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, small.particles);
+            View aos = make_view(pop.schema, nullptr, Layout::AoS, kPrecStored, {}, pop.ics.n);
             DevBuf st(aos.total_bytes());
             store_state(pop.ics, aos, st.p);
             const std::vector<uint8_t> b = download(aos, st.p);

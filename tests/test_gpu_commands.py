@@ -127,3 +127,58 @@ def test_bench_transform_rows(libs):
     for a, b in zip(r1, r2):  # the byte model column agrees; device rows carry a GPU time
         if a["placement"] == "device":
             assert a["bytes_moved"] == b["bytes_moved"] and float(a["convert_s"]) > 0
+
+
+def _write_ics_csv(path, n, seed=7):
+    """id,x0,x1,x2,v0,v1,v2,u,m,h rows (sph.cpp:351-383 format) with a comment,
+    a header and a blank line, values printed with 17 significant digits."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    with open(path, "w") as f:
+        f.write("# initial conditions\n")
+        f.write("id,x0,x1,x2,v0,v1,v2,u,m,h\n")
+        for i in range(n):
+            x, v = rng.random(3), rng.uniform(-1, 1, 3)
+            u, m, h = rng.uniform(0.5, 1.5), rng.uniform(0.5, 1.5) / 64, rng.uniform(0.3, 0.6)
+            f.write(",".join([str(i)] + ["%.17g" % t for t in (*x, *v, u, m, h)]) + "\n")
+            if i == n // 2:
+                f.write("\n")
+
+
+def test_ic_csv_bench_kernels_match_reference(libs, tmp_path):
+    """ic-csv initial conditions (bench.cpp:66-68): the population comes from the
+    file (row count sizes the buffers; the CSV's particles column stays the
+    configured count), identical checksums on both libraries."""
+    ours, ref = libs
+    path = str(tmp_path / "ics.csv")
+    _write_ics_csv(path, 192)
+    for cmd, prec in (("sf_run_bench_kernels", "64,32,16"), ("sf_run_bench_pipeline", "32")):
+        args = dict(ints=[("particles", 192), ("threads", 1)], strs=[("precision", prec), ("ic-csv", path)])
+        s1, t1 = run(ours, cmd, **args)
+        s2, t2 = run(ref, cmd, **args)
+        assert s1 == 0 and s2 == 0, (t1, t2)
+        r1, r2 = csv_rows(t1), csv_rows(t2)
+        assert len(r1) == len(r2) > 0
+        for a, b in zip(r1, r2):
+            assert a["checksum"] == b["checksum"], (cmd, a, b)
+            assert a["particles"] == b["particles"] == "192"
+    # the CSV overrides the random initial conditions
+    s, t_rand = run(ours, "sf_run_bench_kernels", ints=[("particles", 192)], strs=[("precision", "32")])
+    s, t_csv = run(ours, "sf_run_bench_kernels", ints=[("particles", 192)], strs=[("precision", "32"), ("ic-csv", path)])
+    assert [r["checksum"] for r in csv_rows(t_rand)] != [r["checksum"] for r in csv_rows(t_csv)]
+
+
+def test_ic_csv_errors_match_reference(libs, tmp_path):
+    ours, ref = libs
+    bad_cols = tmp_path / "cols.csv"
+    bad_cols.write_text("0,0.1,0.2,0.3,0,0,0,1.0,0.01\n")
+    bad_num = tmp_path / "num.csv"
+    bad_num.write_text("0,0.1,zz,0.3,0,0,0,1.0,0.01,0.5\n")
+    for path in (str(tmp_path / "missing.csv"), str(bad_cols), str(bad_num)):
+        args = dict(ints=[("particles", 64)], strs=[("precision", "32"), ("ic-csv", path)])
+        s1, _ = run(ours, "sf_run_bench_kernels", **args)
+        e1 = ours.sf_last_error()
+        s2, _ = run(ref, "sf_run_bench_kernels", **args)
+        e2 = ref.sf_last_error()
+        assert s1 == s2 != 0, (path, s1, s2)
+        assert e1 == e2, (e1, e2)
