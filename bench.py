@@ -278,6 +278,12 @@ def b200_arm(args):
                 "peak_kind": peak_kind, "kernel": "k_gather_warp<ProcXV> (fused gather+drift, %s)" % prec_name,
                 "algorithmic_bytes_per_particle": ALG_BYTES,
                 "traffic": traffic_from_profiles("gather_drift_%s" % args.prec)}
+    if roofline["traffic"]:  # the DRAM bytes ncu measured per launch, over the same launch time
+        roofline["dram_achieved"] = roofline["traffic"] / (ms * 1e-3) / 1e9
+        roofline["dram_frac"] = roofline["dram_achieved"] / peak
+        roofline["note"] = ("frac counts the 48 algorithmic B/particle; the 88-B AoS record crosses HBM whole "
+                            "(DRAM fetch granularity >= 64 B, profiles/r01_sector_probe.md), so frac <= 0.48 "
+                            "by format; dram_frac is the measured-bytes fraction of the copy peak")
 
     # end to end through the C ABI: pinned host AoS in, host SoA out
     e2e = None

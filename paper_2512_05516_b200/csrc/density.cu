@@ -235,17 +235,18 @@ __global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
             const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < G.nx - 1 ? fx - float(jx + 1) : 0.0f),
                                     0.0f);
             int b[W], e[W];
+            const int cx = jx * G.ny;  // cell ids fit in int32 (bin_particles checks ncell < 2^31)
 #pragma unroll
             for (int t = 0; t < W; ++t) {
                 const int jy = iy - R + t;
                 const float ddy = fmaxf(
                     fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
                 const float d2 = fmaf(ddx, ddx, ddy * ddy);
-                const float dz = sqrtf(fmaxf(rc2 - d2, 0.0f));
+                const float dz = sqrt_approx(fmaxf(rc2 - d2, 0.0f));  // rel err ~1e-7, inside the margin
                 const int zlo = min(max(int(floorf(fzc - dz)), zmin), G.nz - 1);
                 const int zhi = max(min(int(floorf(fzc + dz)), zmax), 0);
                 const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
-                const int64_t c0 = (int64_t(jx) * G.ny + (ok ? jy : 0)) * G.nz;
+                const int c0 = (cx + (ok ? jy : 0)) * G.nz;
                 b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
                 e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
             }
@@ -277,6 +278,7 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     if (nx <= 0 || ny <= 0 || nz <= 0 || own_x0 < 0 || own_x1 > nx || own_x0 > own_x1 || reach < 1 || reach > 4)
         throw std::invalid_argument("bad cell grid");
     if (n >= (1ull << 31)) throw std::invalid_argument("density_cells: n must be < 2^31 per device");
+    if (int64_t(nx) * ny * nz >= (1ll << 31)) throw std::invalid_argument("bad cell grid");
     if (n == 0) return;
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
     if (sp < 0) throw std::invalid_argument("density_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
