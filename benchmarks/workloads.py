@@ -135,6 +135,22 @@ def c3(args, peak, peak_kind):
         out[name] = {"density_ms": msd, "bin_ms": msb, "value": n / (msd * 1e-3),
                      "hbm_GBps_algorithmic": bytes_pp * n / (msd * 1e-3) / 1e9,
                      "pairs_in_support": pairs}
+        if name == "fp32":
+            # cell-linked force on the same particles: rho from the density
+            # just computed, P from the EOS at u = 1 (P = (gamma - 1) rho u), random velocities
+            vel = torch.rand(n, 3, generator=g, device="cuda") * 2 - 1
+            pres = rho * (2.0 / 3.0)
+            acc, dudt = torch.empty(n, 3, device="cuda"), torch.empty(n, device="cuda")
+            ff = lambda: api.force_cells(xs, vel, ms_, hs, rho, pres, cs, perm, (0, 0, 0), fine, dims,  # noqa: E731
+                                         reach=refine, prec=prec, a=acc, du=dudt)
+            for _ in range(args.warmup):
+                ff()
+            tf = timed_each(ff, max(3, args.steps // 5))
+            msf = sum(tf) / len(tf)
+            out["force_fp32"] = {"force_ms": msf, "value": n / (msf * 1e-3),
+                                 "pairs_in_support_per_s": pairs / (msf * 1e-3),
+                                 "note": "pack (x,h | v,m | P/rho^2) + k_force_c; includes the rho == 0 check "
+                                         "(one stream sync)"}
     ms = out["fp32"]["density_ms"]
     rl = {"bound": "compute (FP32 + MUFU)", "achieved": out["fp32"]["hbm_GBps_algorithmic"], "peak": peak,
           "unit": "GB/s", "frac": out["fp32"]["hbm_GBps_algorithmic"] / peak, "peak_kind": peak_kind,

@@ -136,6 +136,18 @@ SF_API sf_status sf_b200_density_cells(const void* x, const void* m, const void*
                                        uint64_t n, const int32_t* perm, const int32_t* cell_start,
                                        const float* lo, float cell, int nx, int ny, int nz, int reach,
                                        int own_x0, int own_x1, float* rho_out, void* stream);
+/* Cell-linked force (the reference's force_kernel, sph.cpp:201-245, over
+ * cell neighbours instead of 64-particle buffers): x, v: 3*n lanes; m, h,
+ * rho, P: n lanes, all in `prec` and particle order; grid, perm and
+ * cell_start as for sf_b200_density_cells.  Writes a_out[3*i+l] and
+ * du_out[i] (fp32, particle order) for particles of the own x-layers.  Any
+ * rho == 0 returns SF_ERROR "force: degenerate state, rho == 0" (the
+ * reference's std::domain_error); synchronizes `stream` to check it. */
+SF_API sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const void* h,
+                                     const void* rho, const void* P, int prec, uint64_t n,
+                                     const int32_t* perm, const int32_t* cell_start, const float* lo,
+                                     float cell, int nx, int ny, int nz, int reach, int own_x0,
+                                     int own_x1, float* a_out, float* du_out, void* stream);
 /* Counting sort of particles into cells (x-major cell id), stable in
  * particle index: writes perm[n] (sorted position -> original index) and
  * cell_start[ncell+1].  scratch must hold sf_b200_bin_scratch_bytes(). */

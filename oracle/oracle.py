@@ -68,6 +68,8 @@ def lib():
             ("or_w", d, [d, d]),
             ("or_density_buffer", None, [P, P, P, u64, u64, i, P]),
             ("or_density_cells", None, [P, P, P, u64, d, d, d, P]),
+            ("or_force_cells", i, [P] * 6 + [u64, d, d, d] + [P] * 4),
+            ("or_dw_dr", d, [d, d]),
             ("or_random_ics", None, [u64, u64, u64, d] + [P] * 12),
             ("or_fmt_width", i, [i]),
         ]:
@@ -429,6 +431,19 @@ def density_cells(x, m, h, lo: float, hi: float, cell: float) -> np.ndarray:
     rho = np.zeros(len(m), np.float64)
     lib().or_density_cells(_p(x), _p(m), _p(h), len(m), lo, hi, cell, _p(rho))
     return rho
+
+
+def force_cells(x, v, m, h, rho, P, lo: float, hi: float, cell: float):
+    """Cell-linked restatement of force_kernel (sph.cpp:201-245): returns
+    (a[n,3], du[n], a_scale[n], du_scale[n]); raises on rho == 0 like the
+    reference's domain_error."""
+    x, v, m, h, rho, P = (np.ascontiguousarray(t, np.float64) for t in (x, v, m, h, rho, P))
+    n = len(m)
+    a = np.zeros(3 * n); du = np.zeros(n); sa = np.zeros(n); sd = np.zeros(n)
+    if lib().or_force_cells(_p(x), _p(v), _p(m), _p(h), _p(rho), _p(P), n, lo, hi, cell,
+                            _p(a), _p(du), _p(sa), _p(sd)) != 0:
+        raise ArithmeticError("force: degenerate state, rho == 0")
+    return a.reshape(n, 3), du, sa, sd
 
 
 def w(r: float, h: float) -> float:

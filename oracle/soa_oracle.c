@@ -241,46 +241,134 @@ static int cmp_u64(const void* a, const void* b) {
     return x < y ? -1 : x > y;
 }
 
-void or_density_cells(const double* x, const double* m, const double* h, uint64_t n,
-                      double lo, double hi, double cell, double* rho) {
-    int nc = (int)ceil((hi - lo) / cell);
-    if (nc < 1) nc = 1;
+/* Cell list of a cubic grid [lo, hi)^3 with cells of side `cell` (particles
+ * outside clamp to the face cells), each cell's members in ascending index. */
+typedef struct {
+    int nc;
+    uint64_t *start, *idx;
+    int* cid;
+} CellList;
+
+static CellList cells_build(const double* x, uint64_t n, double lo, double hi, double cell) {
+    CellList L;
+    L.nc = (int)ceil((hi - lo) / cell);
+    if (L.nc < 1) L.nc = 1;
+    const int nc = L.nc;
     uint64_t ncell = (uint64_t)nc * nc * nc;
-    uint64_t* start = calloc(ncell + 1, sizeof(uint64_t));
-    uint64_t* idx = malloc(n * sizeof(uint64_t));
-    int* cid = malloc(n * sizeof(int) * 3);
+    L.start = calloc(ncell + 1, sizeof(uint64_t));
+    L.idx = malloc((n ? n : 1) * sizeof(uint64_t));
+    L.cid = malloc((n ? n : 1) * sizeof(int) * 3);
     for (uint64_t i = 0; i < n; ++i)
         for (int d = 0; d < 3; ++d) {
             int c = (int)floor((x[3 * i + d] - lo) / cell);
-            cid[3 * i + d] = c < 0 ? 0 : c >= nc ? nc - 1 : c;
+            L.cid[3 * i + d] = c < 0 ? 0 : c >= nc ? nc - 1 : c;
         }
     for (uint64_t i = 0; i < n; ++i)
-        start[((uint64_t)cid[3 * i] * nc + cid[3 * i + 1]) * nc + cid[3 * i + 2] + 1]++;
-    for (uint64_t c = 0; c < ncell; ++c) start[c + 1] += start[c];
+        L.start[((uint64_t)L.cid[3 * i] * nc + L.cid[3 * i + 1]) * nc + L.cid[3 * i + 2] + 1]++;
+    for (uint64_t c = 0; c < ncell; ++c) L.start[c + 1] += L.start[c];
     uint64_t* fill = malloc(ncell * sizeof(uint64_t));
-    memcpy(fill, start, ncell * sizeof(uint64_t));
+    memcpy(fill, L.start, ncell * sizeof(uint64_t));
     for (uint64_t i = 0; i < n; ++i)  /* ascending i -> each cell list is sorted */
-        idx[fill[((uint64_t)cid[3 * i] * nc + cid[3 * i + 1]) * nc + cid[3 * i + 2]]++] = i;
+        L.idx[fill[((uint64_t)L.cid[3 * i] * nc + L.cid[3 * i + 1]) * nc + L.cid[3 * i + 2]]++] = i;
+    free(fill);
+    return L;
+}
+
+static void cells_free(CellList* L) { free(L->start); free(L->idx); free(L->cid); }
+
+/* the members of the 27 cells around particle i, ascending index */
+static uint64_t cells_candidates(const CellList* L, uint64_t i, uint64_t** cand, uint64_t* cap) {
+    const int nc = L->nc;
+    uint64_t nn = 0;
+    for (int a = -1; a <= 1; ++a)
+        for (int b = -1; b <= 1; ++b)
+            for (int c = -1; c <= 1; ++c) {
+                int p = L->cid[3 * i] + a, q = L->cid[3 * i + 1] + b, s = L->cid[3 * i + 2] + c;
+                if (p < 0 || q < 0 || s < 0 || p >= nc || q >= nc || s >= nc) continue;
+                uint64_t k = ((uint64_t)p * nc + q) * nc + s;
+                for (uint64_t t = L->start[k]; t < L->start[k + 1]; ++t) {
+                    if (nn == *cap) { *cap *= 2; *cand = realloc(*cand, *cap * sizeof(uint64_t)); }
+                    (*cand)[nn++] = L->idx[t];
+                }
+            }
+    qsort(*cand, nn, sizeof(uint64_t), cmp_u64);
+    return nn;
+}
+
+/* Cell-linked density: density_kernel's sum (sph.cpp:176-199) over every
+ * particle of the 27 cells (side >= 2 h_max) in ascending index — the terms
+ * beyond the support are exactly +0.0, so this equals the all-pairs sum. */
+void or_density_cells(const double* x, const double* m, const double* h, uint64_t n,
+                      double lo, double hi, double cell, double* rho) {
+    CellList L = cells_build(x, n, lo, hi, cell);
     uint64_t cap = 1024, *cand = malloc(cap * sizeof(uint64_t));
     for (uint64_t i = 0; i < n; ++i) {
-        uint64_t nn = 0;
-        for (int a = -1; a <= 1; ++a)
-            for (int b = -1; b <= 1; ++b)
-                for (int c = -1; c <= 1; ++c) {
-                    int p = cid[3 * i] + a, q = cid[3 * i + 1] + b, s = cid[3 * i + 2] + c;
-                    if (p < 0 || q < 0 || s < 0 || p >= nc || q >= nc || s >= nc) continue;
-                    uint64_t k = ((uint64_t)p * nc + q) * nc + s;
-                    for (uint64_t t = start[k]; t < start[k + 1]; ++t) {
-                        if (nn == cap) { cap *= 2; cand = realloc(cand, cap * sizeof(uint64_t)); }
-                        cand[nn++] = idx[t];
-                    }
-                }
-        qsort(cand, nn, sizeof(uint64_t), cmp_u64);
+        uint64_t nn = cells_candidates(&L, i, &cand, &cap);
         double acc = 0.0;
         for (uint64_t t = 0; t < nn; ++t) acc += pair_term(x, m, h, i, cand[t]);
         rho[i] = acc;
     }
-    free(cand); free(fill); free(cid); free(idx); free(start);
+    free(cand);
+    cells_free(&L);
+}
+
+/* sph.cpp:26-33 */
+double or_dw_dr(double r, double h) {
+    double q = r / h;
+    if (q >= 2.0) return 0.0;
+    double norm = (1.0 / 3.14159265358979323846) / (h * h * h * h);
+    if (q < 1.0) return norm * (-3.0 * q + 2.25 * q * q);
+    double t = 2.0 - q;
+    return norm * (-0.75 * t * t);
+}
+
+/* Cell-linked force: force_kernel (sph.cpp:201-245, Deferred writeback) over
+ * the 27-cell candidates in ascending index, j == i skipped, grad_w
+ * (sph.cpp:35-40) zero at r == 0.  a[3n] and du[n] as the reference writes
+ * them; a_scale[n] = sum_j |m_j pf_ij grad W_ij| and du_scale[n] =
+ * |P_i/rho_i^2| sum_j |m_j (v_i - v_j) . grad W_ij| are the magnitudes the
+ * sums cancel from (the scale a floating-point tolerance is relative to).
+ * Returns -1 when some rho is 0 (the reference's domain_error), else 0. */
+int or_force_cells(const double* x, const double* v, const double* m, const double* h, const double* rho,
+                   const double* P, uint64_t n, double lo, double hi, double cell, double* a, double* du,
+                   double* a_scale, double* du_scale) {
+    for (uint64_t i = 0; i < n; ++i)
+        if (rho[i] == 0.0) return -1;
+    CellList L = cells_build(x, n, lo, hi, cell);
+    uint64_t cap = 1024, *cand = malloc(cap * sizeof(uint64_t));
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t nn = cells_candidates(&L, i, &cand, &cap);
+        const double pi = P[i] / (rho[i] * rho[i]);
+        double acc[3] = {0.0, 0.0, 0.0}, compr = 0.0, sa = 0.0, sd = 0.0;
+        for (uint64_t t = 0; t < nn; ++t) {
+            const uint64_t j = cand[t];
+            if (j == i) continue;
+            const double d0 = x[3 * i] - x[3 * j], d1 = x[3 * i + 1] - x[3 * j + 1], d2 = x[3 * i + 2] - x[3 * j + 2];
+            const double hij = 0.5 * (h[i] + h[j]);
+            const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+            if (r != 0.0) {
+                const double sc = or_dw_dr(r, hij) / r;
+                g0 = sc * d0; g1 = sc * d1; g2 = sc * d2;
+            }
+            const double pf = pi + P[j] / (rho[j] * rho[j]);
+            acc[0] -= m[j] * pf * g0;
+            acc[1] -= m[j] * pf * g1;
+            acc[2] -= m[j] * pf * g2;
+            const double dv = (v[3 * i] - v[3 * j]) * g0 + (v[3 * i + 1] - v[3 * j + 1]) * g1 +
+                              (v[3 * i + 2] - v[3 * j + 2]) * g2;
+            compr += m[j] * dv;
+            sa += fabs(m[j] * pf) * sqrt(g0 * g0 + g1 * g1 + g2 * g2);
+            sd += fabs(m[j] * dv);
+        }
+        for (int l = 0; l < 3; ++l) a[3 * i + l] = acc[l];
+        du[i] = pi * compr;
+        a_scale[i] = sa;
+        du_scale[i] = fabs(pi) * sd;
+    }
+    free(cand);
+    cells_free(&L);
+    return 0;
 }
 
 /* ---- std::mt19937_64 (the C++ standard's parameters) -------------------- */

@@ -265,6 +265,19 @@ sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int
     });
 }
 
+sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho,
+                              const void* P, int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start,
+                              const float* lo, float cell, int nx, int ny, int nz, int reach, int own_x0, int own_x1,
+                              float* a_out, float* du_out, void* stream) {
+    if (!x || !v || !m || !h || !rho || !P || !cell_start || !lo || !a_out || !du_out)
+        return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        force_cells(x, v, m, h, rho, P, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, own_x0, own_x1, a_out,
+                    du_out, static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
 uint64_t sf_b200_bin_scratch_bytes(uint64_t n, int nx, int ny, int nz) { return bin_scratch_bytes(n, nx, ny, nz); }
 
 sf_status sf_b200_bin_particles(const float* x, uint64_t n, const float* lo, float cell, int nx, int ny, int nz,

@@ -313,6 +313,169 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     check_cuda(cudaFreeAsync(mass, st), "cudaFreeAsync");
 }
 
+// ------------------------------------------------------------------ force
+// Cell-linked force (sph.cpp:201-245 restated over cell neighbours; the
+// reference evaluates it inside 64-particle buffers).  k_pack_force packs per
+// sorted particle (x, y, z, h), (vx, vy, vz, m) and P/rho^2, flags rho == 0
+// (the reference's domain_error) and reduces h_max; k_force_c sweeps the same
+// culled column runs as k_pairs_c and accumulates, per home particle i,
+//   a_i  = -sum_j m_j (P_i/rho_i^2 + P_j/rho_j^2) dW/dr(r, h_ij) dx/r
+//   du_i =  P_i/rho_i^2 sum_j m_j (v_i - v_j) . dx dW/dr(r, h_ij) / r
+// with the branch-free M4 derivative
+//   pi h_ij^4 dW/dr = 3 max(1-q,0)^2 - 0.75 max(2-q,0)^2
+// (q < 1: -3q + 2.25q^2, sph.cpp:30; 1 <= q < 2: -0.75 (2-q)^2, sph.cpp:32),
+// which is exactly 0 at r = 0, so the self term vanishes as in grad_w
+// (sph.cpp:35-40) without a j != i test.  binary32 arithmetic; tolerance
+// relative to sum_j |term| (tests/test_gpu_parity.py).
+template <int P>
+__global__ void k_pack_force(const void* __restrict__ x, const void* __restrict__ v, const void* __restrict__ m,
+                             const void* __restrict__ h, const void* __restrict__ rho, const void* __restrict__ pr,
+                             const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ pos,
+                             float4* __restrict__ vel, float* __restrict__ pf, unsigned* __restrict__ hmax_bits,
+                             unsigned* __restrict__ degenerate) {
+    float hmax = 0.0f;
+    bool zero = false;
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = perm ? uint64_t(perm[k]) : k;
+        const float hi = ldf<P>(h, i), ri = ldf<P>(rho, i);
+        pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), hi);
+        vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(m, i));
+        pf[k] = ldf<P>(pr, i) / (ri * ri);
+        hmax = fmaxf(hmax, hi);
+        zero |= ri == 0.0f;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, d));
+    if ((threadIdx.x & 31) == 0 && hmax > 0.0f) atomicMax(hmax_bits, __float_as_uint(hmax));
+    if (__any_sync(0xffffffffu, zero) && (threadIdx.x & 31) == 0) atomicOr(degenerate, 1u);
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos, const float4* __restrict__ vel,
+                                                 const float* __restrict__ pf, const int32_t* __restrict__ cell_start,
+                                                 const int32_t* __restrict__ perm, CellGrid G, int64_t n,
+                                                 const unsigned* __restrict__ hmax_bits, float* __restrict__ a_out,
+                                                 float* __restrict__ du_out) {
+    constexpr int W = 2 * R + 1;
+    const float hmax = __uint_as_float(*hmax_bits);
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const float4 pi = pos[k];
+        const float fx = (pi.x - G.lox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
+                    fz = (pi.z - G.loz) * G.inv_cell;
+        const int ix = min(max(int(floorf(fx)), 0), G.nx - 1);
+        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
+        const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
+        const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
+        const float4 vi = vel[k];
+        const float pfi = pf[k];
+        const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;
+        const float rc2 = rc * rc;
+        const float hh_i = 0.5f * pi.w;
+        const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
+        const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
+        float ax = 0.0f, ay = 0.0f, az = 0.0f, cp = 0.0f;
+        auto pair = [&](int j) {
+            const float4 pj = pos[j];
+            const float4 vj = vel[j];
+            const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
+            const float inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
+            const float q = (r2 * inv_r) * inv_h;
+            const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
+            const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
+            const float ih2 = inv_h * inv_h;
+            const float sc = dw * (ih2 * ih2) * inv_r;           // pi dW/dr / r
+            const float f = vj.w * (pfi + __ldg(pf + j)) * sc;
+            ax = fmaf(f, dx, ax);
+            ay = fmaf(f, dy, ay);
+            az = fmaf(f, dz, az);
+            const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
+            cp = fmaf(vj.w * sc, dvx, cp);
+        };
+#pragma unroll 1
+        for (int dxi = -R; dxi <= R; ++dxi) {
+            const int jx = ix + dxi;
+            if (jx < 0 || jx >= G.nx) continue;
+            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < G.nx - 1 ? fx - float(jx + 1) : 0.0f),
+                                    0.0f);
+            int b[W], e[W];
+            const int cx = jx * G.ny;
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+                const int jy = iy - R + t;
+                const float ddy = fmaxf(
+                    fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
+                const float d2 = fmaf(ddx, ddx, ddy * ddy);
+                const float dzr = sqrt_approx(fmaxf(rc2 - d2, 0.0f));
+                const int zlo = min(max(int(floorf(fzc - dzr)), zmin), G.nz - 1);
+                const int zhi = max(min(int(floorf(fzc + dzr)), zmax), 0);
+                const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
+                const int c0 = (cx + (ok ? jy : 0)) * G.nz;
+                b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
+                e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < W; ++t)
+                for (int j = b[t]; j < e[t]; ++j) pair(j);
+        }
+        constexpr float kInvPi = 0.31830988618379067f;
+        const int64_t i = perm ? perm[k] : k;
+        a_out[3 * i] = -kInvPi * ax;
+        a_out[3 * i + 1] = -kInvPi * ay;
+        a_out[3 * i + 2] = -kInvPi * az;
+        du_out[i] = pfi * (kInvPi * cp);
+    }
+}
+
+void force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho, const void* pr,
+                 int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
+                 int nx, int ny, int nz, int reach, int own_x0, int own_x1, float* a, float* du, cudaStream_t st) {
+    require_device();
+    if (nx <= 0 || ny <= 0 || nz <= 0 || own_x0 < 0 || own_x1 > nx || own_x0 > own_x1 || reach < 1 || reach > 4)
+        throw std::invalid_argument("bad cell grid");
+    if (n >= (1ull << 31)) throw std::invalid_argument("force_cells: n must be < 2^31 per device");
+    if (int64_t(nx) * ny * nz >= (1ll << 31)) throw std::invalid_argument("bad cell grid");
+    if (n == 0) return;
+    const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
+    if (sp < 0) throw std::invalid_argument("force_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
+    float4 *pos = nullptr, *vel = nullptr;
+    float* pf = nullptr;
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pos), 32 * n, st), "cudaMallocAsync");
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pf), 4 * n + 16, st), "cudaMallocAsync");
+    vel = pos + n;
+    unsigned* words = reinterpret_cast<unsigned*>(pf + n);  // [0] h_max bits, [1] rho == 0 flag
+    check_cuda(cudaMemsetAsync(words, 0, 2 * sizeof(unsigned), st), "memset");
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    if (sp == SP_F32) k_pack_force<SP_F32><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 1);
+    else if (sp == SP_F16) k_pack_force<SP_F16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 1);
+    else k_pack_force<SP_BF16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 1);
+    unsigned flag = 0;
+    check_cuda(cudaMemcpyAsync(&flag, words + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    if (flag) {
+        cudaFreeAsync(pos, st);
+        cudaFreeAsync(pf, st);
+        throw std::domain_error("force: degenerate state, rho == 0");
+    }
+    CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
+    const int64_t nn = int64_t(n);
+    if (reach == 1) k_force_c<1><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+    else if (reach == 2) k_force_c<2><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+    else if (reach == 3) k_force_c<3><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+    else k_force_c<4><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+    check_cuda(cudaGetLastError(), "force_cells launch");
+    count_launches(2);
+    check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
+    check_cuda(cudaFreeAsync(pf, st), "cudaFreeAsync");
+}
+
 // ------------------------------------------------------------------ binning
 __global__ void k_cell_ids(const float* __restrict__ x, uint64_t n, float lox, float loy, float loz, float inv_cell,
                            int nx, int ny, int nz, int32_t* __restrict__ cid, int32_t* __restrict__ counts) {

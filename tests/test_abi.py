@@ -199,3 +199,23 @@ def test_view_rejects_bad_arguments():
     v = api.View(S, 10, "soa", "drift", 16)
     with pytest.raises(L.SfInvalidArg):
         v.lane("rho")  # not in the drift access set
+
+
+def test_cell_entry_points_fail_loudly_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    n = 64
+    f = (C.c_float * (3 * n))()
+    i32 = (C.c_int32 * (n + 8))()
+    lo = (C.c_float * 3)(0, 0, 0)
+    p = lambda a: C.cast(a, C.c_void_p)  # noqa: E731
+    st = L.lib().sf_b200_density_cells(p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2, 1, 0, 2, p(f),
+                                       None)
+    assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
+    st = L.lib().sf_b200_force_cells(p(f), p(f), p(f), p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2,
+                                     1, 0, 2, p(f), p(f), None)
+    assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
+    st = L.lib().sf_b200_force_cells(None, p(f), p(f), p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2,
+                                     1, 0, 2, p(f), p(f), None)
+    assert st == L.SF_INVALID_ARG

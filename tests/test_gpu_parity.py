@@ -307,6 +307,64 @@ def test_density_cells_own_layers_and_ghosts():
     assert np.all(rho[~mine] == 0)
 
 
+# ----------------------------------------------------------- cell force
+def _force_case(n, seed, prec):
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, 3))
+    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3)) * rng.uniform(0.8, 1.2, n)
+    m = rng.uniform(0.5, 1.5, n) / n
+    v = rng.uniform(-1, 1, (n, 3))
+    rho = rng.uniform(0.5, 1.5, n)
+    P = rng.uniform(0.2, 1.2, n)
+    dt = {api.SF_PREC_NATIVE: torch.float32, 16: torch.float16, api.SF_PREC_BF16: torch.bfloat16}[prec]
+    ts = [torch.tensor(a, device="cuda").to(dt) for a in (x, v, m, h, rho, P)]
+    return ts, [t.double().cpu().numpy() for t in ts]
+
+
+# Tolerance: binary32 sums of binary32 terms (approximate rcp/rsqrt) vs the
+# binary64 oracle on the identical stored inputs.  Forces cancel (a_i is a sum
+# of terms of both signs), so the error is bounded relative to the sum of the
+# term magnitudes the oracle reports: |a - a_ref| <= 2e-5 * sum_j |a_ij|.
+FORCE_TOL = 2e-5
+
+
+@pytest.mark.parametrize("prec", [api.SF_PREC_NATIVE, 16, api.SF_PREC_BF16])
+@pytest.mark.parametrize("refine", [1, 2])
+def test_force_cells_vs_oracle(prec, refine):
+    n = 1 << 15
+    ts, (xd, vd, md, hd, rd, Pd) = _force_case(n, 5, prec)
+    nc = int(np.floor(1.0 / float(2 * ts[3].float().max())))
+    cell = 1.0 / nc / refine
+    dims = (nc * refine,) * 3
+    cs, perm = api.bin_particles(ts[0].float().contiguous(), (0, 0, 0), cell, dims)
+    a, du = api.force_cells(*ts, cs, perm, (0, 0, 0), cell, dims, reach=refine, prec=prec)
+    want_a, want_du, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rd, Pd, 0.0, 1.0, 1.0 / nc)
+    err_a = np.linalg.norm(a.double().cpu().numpy() - want_a, axis=1)
+    err_du = np.abs(du.double().cpu().numpy() - want_du)
+    assert np.all(err_a <= FORCE_TOL * sa), (err_a / sa).max()
+    assert np.all(err_du <= FORCE_TOL * sd + 1e-30), (err_du / np.maximum(sd, 1e-300)).max()
+    # not trivially zero: the accelerations are of the order of their scale
+    assert np.median(np.linalg.norm(want_a, axis=1) / sa) > 1e-3
+
+
+def test_force_cells_own_layers_and_degenerate():
+    n = 1 << 14
+    ts, (xd, vd, md, hd, rd, Pd) = _force_case(n, 6, api.SF_PREC_NATIVE)
+    nc = int(np.floor(1.0 / float(2 * ts[3].max())))
+    cs, perm = api.bin_particles(ts[0].contiguous(), (0, 0, 0), 1.0 / nc, (nc, nc, nc))
+    own = (2, nc - 3)
+    a, du = api.force_cells(*ts, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc), own=own)
+    want_a, want_du, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rd, Pd, 0.0, 1.0, 1.0 / nc)
+    layer = np.minimum(np.floor(xd[:, 0] * nc).astype(int), nc - 1)
+    mine = (layer >= own[0]) & (layer < own[1])
+    err = np.linalg.norm(a.double().cpu().numpy() - want_a, axis=1)
+    assert np.all(err[mine] <= FORCE_TOL * sa[mine])
+    assert np.all(a.cpu().numpy()[~mine] == 0) and np.all(du.cpu().numpy()[~mine] == 0)
+    ts[4][17] = 0.0  # rho == 0 anywhere: the reference's domain_error
+    with pytest.raises(api.L.SfError, match="rho == 0"):
+        api.force_cells(*ts, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc))
+
+
 def test_force_degenerate_state_is_an_error():
     """force with rho == 0 raises like the reference's std::domain_error."""
     n = 128

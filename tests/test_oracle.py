@@ -2,6 +2,7 @@
 vectors (tests/golden/, generated from the unmodified reference by
 tests/golden/make_golden.py) and, when oracle/_ref is built, against the
 reference library itself on random inputs."""
+import ctypes as C
 import struct
 
 import numpy as np
@@ -164,3 +165,54 @@ def test_random_values_against_live_reference():
     want = np.zeros(x.size, np.uint64)
     R.L.ref_narrow_array(O._p(x), x.size, 8, 7, O._p(want))
     np.testing.assert_array_equal(O.encode(x, O.OR_BF16), want)
+
+
+def _t64_records(x, v, m, h, rho, P):
+    """The default schema at T=64, x included (every field binary64, id i64):
+    144-B records in declaration order x3 id v3 u m h rho P cs a3 du dt."""
+    n = len(m)
+    rec = np.zeros((n, 18), np.float64)
+    rec[:, 0:3] = x
+    rec[:, 3] = np.arange(n, dtype=np.int64).view(np.float64)
+    rec[:, 4:7] = v
+    rec[:, 7] = 1.0
+    rec[:, 8], rec[:, 9], rec[:, 10], rec[:, 11] = m, h, rho, P
+    rec[:, 12] = 1.0
+    return rec
+
+
+def _cells_case(n, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, 3))
+    h0 = 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3)
+    h = h0 * rng.uniform(0.8, 1.2, n)
+    m = rng.uniform(0.5, 1.5, n) / n
+    v = rng.uniform(-1, 1, (n, 3))
+    nc = int(np.floor(1.0 / (2 * h.max())))
+    return x, v, m, h, 1.0 / nc
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+def test_cell_oracles_pinned_to_reference_all_pairs():
+    """The cell-linked restatements (27 cells of side >= 2 h_max, ascending j)
+    equal the reference's own density_kernel / force_kernel run over ONE buffer
+    holding every particle (all pairs, sph.cpp:176-245): the terms beyond the
+    support are exact zeros, so the sums agree bit for bit."""
+    R = O.RefLib()
+    n = 2048
+    x, v, m, h, cell = _cells_case(n, 11)
+    rng = np.random.default_rng(12)
+    P = rng.uniform(0.5, 1.5, n)
+    rec = _t64_records(x, v, m, h, np.ones(n), P)
+    hb = R._chk(R.L.ref_buf_from_bytes(None, 64, b"", n, rec.ctypes.data_as(C.c_void_p), rec.nbytes))
+    R.run_kernel(hb, "density", bs=n)
+    out = R.bytes(hb).view(np.float64).reshape(n, 18)
+    rho = O.density_cells(x.reshape(-1), m, h, 0.0, 1.0, cell)
+    assert np.array_equal(out[:, 10], rho)
+    # force on the reference's own densities
+    R.run_kernel(hb, "force", bs=n)
+    out = R.bytes(hb).view(np.float64).reshape(n, 18)
+    a, du, sa, sd = O.force_cells(x.reshape(-1), v.reshape(-1), m, h, rho, P, 0.0, 1.0, cell)
+    assert np.array_equal(out[:, 13:16], a) and np.array_equal(out[:, 16], du)
+    assert np.all(sa > 0) and np.all(sd >= 0)
+    R.free(hb)
