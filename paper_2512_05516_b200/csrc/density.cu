@@ -356,7 +356,7 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     return r;
 }
 
-template <int R>
+template <int R, int U>
 __global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos, const float4* __restrict__ vel,
                                                  const float* __restrict__ pf, const int32_t* __restrict__ cell_start,
                                                  const int32_t* __restrict__ perm, CellGrid G, int64_t n,
@@ -422,8 +422,16 @@ __global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos,
                 e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
             }
 #pragma unroll
-            for (int t = 0; t < W; ++t)
-                for (int j = b[t]; j < e[t]; ++j) pair(j);
+            for (int t = 0; t < W; ++t) {
+                int j = b[t];
+                if constexpr (U == 2) {
+                    for (; j + 1 < e[t]; j += 2) {
+                        pair(j);
+                        pair(j + 1);
+                    }
+                }
+                for (; j < e[t]; ++j) pair(j);
+            }
         }
         constexpr float kInvPi = 0.31830988618379067f;
         const int64_t i = perm ? perm[k] : k;
@@ -466,10 +474,15 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
     }
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
     const int64_t nn = int64_t(n);
-    if (reach == 1) k_force_c<1><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-    else if (reach == 2) k_force_c<2><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-    else if (reach == 3) k_force_c<3><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-    else k_force_c<4><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+    auto go = [&](auto u) {
+        constexpr int U = decltype(u)::value;
+        if (reach == 1) k_force_c<1, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        else if (reach == 2) k_force_c<2, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        else if (reach == 3) k_force_c<3, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        else k_force_c<4, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+    };
+    if (env_int_d("SFB_FORCE_UNROLL", 2) == 2) go(std::integral_constant<int, 2>{});
+    else go(std::integral_constant<int, 1>{});
     check_cuda(cudaGetLastError(), "force_cells launch");
     count_launches(2);
     check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
