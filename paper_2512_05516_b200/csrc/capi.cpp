@@ -257,7 +257,7 @@ sf_status sf_b200_run_kernel(const sf_view* v, void* p, const char* k, double dt
 sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n,
                                 const int32_t* perm, const int32_t* cell_start, const float* lo, float cell, int nx,
                                 int ny, int nz, int reach, int own_x0, int own_x1, float* rho, void* stream) {
-    if (!x || !m || !h || !cell_start || !rho || !lo) return fail(SF_INVALID_ARG, "null argument");
+    if ((n && (!x || !m || !h || !rho)) || !cell_start || !lo) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
         density_cells(x, m, h, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, own_x0, own_x1, rho,
                       static_cast<cudaStream_t>(stream));
@@ -269,7 +269,7 @@ sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const
                               const void* P, int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start,
                               const float* lo, float cell, int nx, int ny, int nz, int reach, int own_x0, int own_x1,
                               float* a_out, float* du_out, void* stream) {
-    if (!x || !v || !m || !h || !rho || !P || !cell_start || !lo || !a_out || !du_out)
+    if ((n && (!x || !v || !m || !h || !rho || !P || !a_out || !du_out)) || !cell_start || !lo)
         return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
         force_cells(x, v, m, h, rho, P, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, own_x0, own_x1, a_out,
@@ -283,7 +283,8 @@ uint64_t sf_b200_bin_scratch_bytes(uint64_t n, int nx, int ny, int nz) { return 
 sf_status sf_b200_bin_particles(const float* x, uint64_t n, const float* lo, float cell, int nx, int ny, int nz,
                                 int32_t* cell_start, int32_t* perm, void* scratch, uint64_t scratch_bytes,
                                 void* stream) {
-    if (!x || !lo || !cell_start || !perm || !scratch) return fail(SF_INVALID_ARG, "null argument");
+    // per-particle arrays may be NULL when there are no particles
+    if ((n && (!x || !perm)) || !lo || !cell_start || !scratch) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
         bin_particles(x, n, lo, cell, nx, ny, nz, cell_start, perm, scratch, scratch_bytes,
                       static_cast<cudaStream_t>(stream));

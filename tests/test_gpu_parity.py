@@ -365,6 +365,44 @@ def test_force_cells_own_layers_and_degenerate():
         api.force_cells(*ts, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc))
 
 
+def test_cells_outside_grid_offset_origin_and_empty():
+    """Particles beyond the grid clamp into the face cells (binning), whose
+    extent the culled windows treat as unbounded; a non-zero origin; n = 0."""
+    n = 1 << 14
+    rng = np.random.default_rng(9)
+    lo, hi = -0.5, 0.5
+    x = rng.random((n, 3)) - 0.5
+    out = rng.random(n) < 0.05           # 5% pushed up to 0.02 beyond a face
+    ax = rng.integers(0, 3, n)
+    x[out, ax[out]] = np.where(x[out, ax[out]] > 0, hi, lo) + np.sign(x[out, ax[out]]) * rng.random(out.sum()) * 0.02
+    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3)) * rng.uniform(0.9, 1.1, n)
+    m = rng.uniform(0.5, 1.5, n) / n
+    nc = int(np.floor((hi - lo) / (2 * h.max())))
+    cell = (hi - lo) / nc
+    xt, mt, ht = (torch.tensor(a, device="cuda", dtype=torch.float32) for a in (x, m, h))
+    xd, md, hd = (t.double().cpu().numpy() for t in (xt, mt, ht))
+    for refine in (1, 2):
+        dims = (nc * refine,) * 3
+        cs, perm = api.bin_particles(xt, (lo, lo, lo), cell / refine, dims)
+        rho = api.density_cells(xt, mt, ht, cs, perm, (lo, lo, lo), cell / refine, dims, reach=refine)
+        want = O.density_cells(xd.reshape(-1), md, hd, lo, hi, (hi - lo) / nc)
+        np.testing.assert_allclose(rho.double().cpu().numpy(), want, rtol=1e-5, atol=0)
+        v = torch.rand(n, 3, device="cuda") - 0.5
+        r32, P = rho.clone(), rho * 0.7
+        a, du = api.force_cells(xt, v, mt, ht, r32, P, cs, perm, (lo, lo, lo), cell / refine, dims, reach=refine)
+        wa, wdu, sa, sd = O.force_cells(xd.reshape(-1), v.double().cpu().numpy().reshape(-1), md, hd,
+                                        r32.double().cpu().numpy(), P.double().cpu().numpy(), lo, hi, (hi - lo) / nc)
+        assert np.all(np.linalg.norm(a.double().cpu().numpy() - wa, axis=1) <= FORCE_TOL * sa)
+        assert np.all(np.abs(du.double().cpu().numpy() - wdu) <= FORCE_TOL * sd + 1e-30)
+    # n = 0: nothing launched, nothing written
+    e = torch.zeros(0, 3, device="cuda")
+    z = torch.zeros(0, device="cuda")
+    cs, perm = api.bin_particles(e, (0, 0, 0), 0.25, (4, 4, 4))
+    assert int(cs.cpu()[-1]) == 0
+    api.density_cells(e, z, z, cs, perm, (0, 0, 0), 0.25, (4, 4, 4))
+    api.force_cells(e, e, z, z, z, z, cs, perm, (0, 0, 0), 0.25, (4, 4, 4))
+
+
 def test_force_degenerate_state_is_an_error():
     """force with rho == 0 raises like the reference's std::domain_error."""
     n = 128
