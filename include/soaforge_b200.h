@@ -129,25 +129,26 @@ SF_API sf_status sf_b200_run_kernel(const sf_view* view, void* dev, const char* 
  * bf16), in particle order; perm[n] / cell_start[ncell+1] from
  * sf_b200_bin_particles over the same grid (lo[3] host floats, cell side,
  * nx*ny*nz cells, x-major).  reach = neighbour cells per side searched
- * (1 when cell >= 2h, 2 when cell >= h).  Only particles in x-layers
- * [own_x0, own_x1) are computed (layers outside are ghosts, multi-GPU);
- * rho_out[i] (fp32, particle order) is written for those particles. */
+ * (1 when cell >= 2h, 2 when cell >= h).  Only the first n_home particles
+ * (particle order) are computed; particles [n_home, n) are neighbours only
+ * (ghosts received from other ranks, multi-GPU).  rho_out[i] (fp32,
+ * particle order) is written for i < n_home. */
 SF_API sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int prec,
                                        uint64_t n, const int32_t* perm, const int32_t* cell_start,
                                        const float* lo, float cell, int nx, int ny, int nz, int reach,
-                                       int own_x0, int own_x1, float* rho_out, void* stream);
+                                       uint64_t n_home, float* rho_out, void* stream);
 /* Cell-linked force (the reference's force_kernel, sph.cpp:201-245, over
  * cell neighbours instead of 64-particle buffers): x, v: 3*n lanes; m, h,
  * rho, P: n lanes, all in `prec` and particle order; grid, perm and
  * cell_start as for sf_b200_density_cells.  Writes a_out[3*i+l] and
- * du_out[i] (fp32, particle order) for particles of the own x-layers.  Any
+ * du_out[i] (fp32, particle order) for i < n_home (the rest are ghosts).  Any
  * rho == 0 returns SF_ERROR "force: degenerate state, rho == 0" (the
  * reference's std::domain_error); synchronizes `stream` to check it. */
 SF_API sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const void* h,
                                      const void* rho, const void* P, int prec, uint64_t n,
                                      const int32_t* perm, const int32_t* cell_start, const float* lo,
-                                     float cell, int nx, int ny, int nz, int reach, int own_x0,
-                                     int own_x1, float* a_out, float* du_out, void* stream);
+                                     float cell, int nx, int ny, int nz, int reach, uint64_t n_home,
+                                     float* a_out, float* du_out, void* stream);
 /* Counting sort of particles into cells (x-major cell id), stable in
  * particle index: writes perm[n] (sorted position -> original index) and
  * cell_start[ncell+1].  scratch must hold sf_b200_bin_scratch_bytes(). */

@@ -240,41 +240,43 @@ def bin_particles(x, lo, cell: float, dims, cell_start=None, perm=None):
     return cell_start, perm
 
 
-def density_cells(x, m, h, cell_start, perm, lo, cell: float, dims, own=None, reach: int = 1,
+def density_cells(x, m, h, cell_start, perm, lo, cell: float, dims, n_home=None, reach: int = 1,
                   prec: int = SF_PREC_NATIVE, rho=None):
     """Cell-linked density.  x: (n,3), m, h: (n,) in particle order stored
     as fp32 (SF_PREC_NATIVE), fp16 (16) or bf16 (SF_PREC_BF16); cell_start /
     perm from bin_particles on the same grid.  Returns rho (fp32, particle
-    order; only own x-layers are written)."""
+    order); only the first n_home particles (default all) are computed, the
+    rest are neighbours only (ghosts)."""
     import torch
     nx, ny, nz = dims
-    own = own or (0, nx)
     n = m.shape[0]
+    n_home = n if n_home is None else n_home
     rho = rho if rho is not None else torch.zeros(max(n, 1), dtype=torch.float32, device=m.device)
     lo_arr = (C.c_float * 3)(*[float(v) for v in lo])
     check(lib().sf_b200_density_cells(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
                                       _ptr(cell_start), C.cast(lo_arr, C.c_void_p), float(cell), nx, ny, nz, reach,
-                                      own[0], own[1], _ptr(rho), _stream()))
+                                      n_home, _ptr(rho), _stream()))
     return rho
 
 
-def force_cells(x, v, m, h, rho, P, cell_start, perm, lo, cell: float, dims, own=None, reach: int = 1,
+def force_cells(x, v, m, h, rho, P, cell_start, perm, lo, cell: float, dims, n_home=None, reach: int = 1,
                 prec: int = SF_PREC_NATIVE, a=None, du=None):
     """Cell-linked force (force_kernel, sph.cpp:201-245, over cell
     neighbours).  x, v: (n,3); m, h, rho, P: (n,), particle order, stored as
     fp32 / fp16 / bf16 per `prec`; grid as for density_cells.  Returns
-    (a (n,3) fp32, du (n,) fp32); only own x-layers are written.  rho == 0
-    raises SfError (the reference's domain_error)."""
+    (a (n,3) fp32, du (n,) fp32) for the first n_home particles (default
+    all; the rest are ghosts).  rho == 0 raises SfError (the reference's
+    domain_error)."""
     import torch
     nx, ny, nz = dims
-    own = own or (0, nx)
     n = m.shape[0]
+    n_home = n if n_home is None else n_home
     a = a if a is not None else torch.zeros((max(n, 1), 3), dtype=torch.float32, device=m.device)
     du = du if du is not None else torch.zeros(max(n, 1), dtype=torch.float32, device=m.device)
     lo_arr = (C.c_float * 3)(*[float(t) for t in lo])
     check(lib().sf_b200_force_cells(_ptr(x), _ptr(v), _ptr(m), _ptr(h), _ptr(rho), _ptr(P), prec, n,
                                     _ptr(perm) if perm is not None else None, _ptr(cell_start),
-                                    C.cast(lo_arr, C.c_void_p), float(cell), nx, ny, nz, reach, own[0], own[1],
+                                    C.cast(lo_arr, C.c_void_p), float(cell), nx, ny, nz, reach, n_home,
                                     _ptr(a), _ptr(du), _stream()))
     return a, du
 

@@ -256,10 +256,10 @@ sf_status sf_b200_run_kernel(const sf_view* v, void* p, const char* k, double dt
 
 sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n,
                                 const int32_t* perm, const int32_t* cell_start, const float* lo, float cell, int nx,
-                                int ny, int nz, int reach, int own_x0, int own_x1, float* rho, void* stream) {
+                                int ny, int nz, int reach, uint64_t n_home, float* rho, void* stream) {
     if ((n && (!x || !m || !h || !rho)) || !cell_start || !lo) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
-        density_cells(x, m, h, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, own_x0, own_x1, rho,
+        density_cells(x, m, h, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, n_home, rho,
                       static_cast<cudaStream_t>(stream));
         return SF_OK;
     });
@@ -267,12 +267,12 @@ sf_status sf_b200_density_cells(const void* x, const void* m, const void* h, int
 
 sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho,
                               const void* P, int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start,
-                              const float* lo, float cell, int nx, int ny, int nz, int reach, int own_x0, int own_x1,
+                              const float* lo, float cell, int nx, int ny, int nz, int reach, uint64_t n_home,
                               float* a_out, float* du_out, void* stream) {
     if ((n && (!x || !v || !m || !h || !rho || !P || !a_out || !du_out)) || !cell_start || !lo)
         return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
-        force_cells(x, v, m, h, rho, P, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, own_x0, own_x1, a_out,
+        force_cells(x, v, m, h, rho, P, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, n_home, a_out,
                     du_out, static_cast<cudaStream_t>(stream));
         return SF_OK;
     });

@@ -73,7 +73,8 @@ __device__ __forceinline__ float w_f32(float q, float inv_h) {
 
 struct CellGrid {
     float lox, loy, loz, inv_cell;
-    int nx, ny, nz, reach, own_x0, own_x1;
+    int nx, ny, nz, reach;
+    int64_t n_home;  // particles [0, n_home) (particle order) are homes; the rest neighbours only
 };
 
 __global__ void __launch_bounds__(256) k_pairs(const float4* __restrict__ pos,
@@ -81,10 +82,11 @@ __global__ void __launch_bounds__(256) k_pairs(const float4* __restrict__ pos,
                                                const int32_t* __restrict__ perm, CellGrid G, int64_t n,
                                                float* __restrict__ rho) {
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i_home = perm ? perm[k] : k;
+        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
         const float4 pi = (pos[k]);
         // the same float formula bin_particles used, so the cell matches
         const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
-        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
         const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
         const int iz = min(max(int(floorf((pi.z - G.loz) * G.inv_cell)), 0), G.nz - 1);
         const int z0 = max(iz - G.reach, 0), z1 = min(iz + G.reach, G.nz - 1);
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(256) k_pairs(const float4* __restrict__ pos,
                     }
                 }
             }
-        rho[perm ? perm[k] : k] = acc;
+        rho[i_home] = acc;
     }
 }
 
@@ -120,9 +122,10 @@ __global__ void __launch_bounds__(256) k_pairs_r(const float4* __restrict__ pos,
                                                  float* __restrict__ rho) {
     constexpr int W = 2 * R + 1;
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i_home = perm ? perm[k] : k;
+        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
         const float4 pi = (pos[k]);
         const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
-        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
         const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
         const int iz = min(max(int(floorf((pi.z - G.loz) * G.inv_cell)), 0), G.nz - 1);
         const int z0 = max(iz - R, 0), z1 = min(iz + R, G.nz - 1);
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(256) k_pairs_r(const float4* __restrict__ pos,
                 if (j < e[t]) pair((pos[j]), j);
             }
         }
-        rho[perm ? perm[k] : k] = acc;
+        rho[i_home] = acc;
     }
 }
 
@@ -215,11 +218,12 @@ __global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
     constexpr int W = 2 * R + 1;
     const float hmax = __uint_as_float(*hmax_bits);
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i_home = perm ? perm[k] : k;
+        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
         const float4 pi = (pos[k]);
         const float fx = (pi.x - G.lox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
                     fz = (pi.z - G.loz) * G.inv_cell;
         const int ix = min(max(int(floorf(fx)), 0), G.nx - 1);
-        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
         const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
         const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
         const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
                 if (j < e[t]) acc += pair_term(pi, hh_i, (pos[j]), __ldg(mass + j));
             }
         }
-        rho[perm ? perm[k] : k] = acc * 0.079577471545947668f;  // 1 / (4 pi)
+        rho[i_home] = acc * 0.079577471545947668f;  // 1 / (4 pi)
     }
 }
 
@@ -273,9 +277,9 @@ static int env_int_d(const char* name, int dflt) {
 
 void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
                    const int32_t* cell_start, const float* lo, float cell, int nx, int ny, int nz, int reach,
-                   int own_x0, int own_x1, float* rho, cudaStream_t st) {
+                   uint64_t n_home, float* rho, cudaStream_t st) {
     require_device();
-    if (nx <= 0 || ny <= 0 || nz <= 0 || own_x0 < 0 || own_x1 > nx || own_x0 > own_x1 || reach < 1 || reach > 4)
+    if (nx <= 0 || ny <= 0 || nz <= 0 || n_home > n || reach < 1 || reach > 4)
         throw std::invalid_argument("bad cell grid");
     if (n >= (1ull << 31)) throw std::invalid_argument("density_cells: n must be < 2^31 per device");
     if (int64_t(nx) * ny * nz >= (1ll << 31)) throw std::invalid_argument("bad cell grid");
@@ -289,7 +293,7 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     unsigned* hmax = reinterpret_cast<unsigned*>(mass + n);
     check_cuda(cudaMemsetAsync(hmax, 0, sizeof(unsigned), st), "memset");
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
+    CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
     const int64_t nn = int64_t(n);
     if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
     else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
@@ -365,11 +369,12 @@ __global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos,
     constexpr int W = 2 * R + 1;
     const float hmax = __uint_as_float(*hmax_bits);
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i_home = perm ? perm[k] : k;
+        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
         const float4 pi = pos[k];
         const float fx = (pi.x - G.lox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
                     fz = (pi.z - G.loz) * G.inv_cell;
         const int ix = min(max(int(floorf(fx)), 0), G.nx - 1);
-        if (ix < G.own_x0 || ix >= G.own_x1) continue;  // ghost layers: neighbours only
         const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
         const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
         const float4 vi = vel[k];
@@ -434,19 +439,18 @@ __global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos,
             }
         }
         constexpr float kInvPi = 0.31830988618379067f;
-        const int64_t i = perm ? perm[k] : k;
-        a_out[3 * i] = -kInvPi * ax;
-        a_out[3 * i + 1] = -kInvPi * ay;
-        a_out[3 * i + 2] = -kInvPi * az;
-        du_out[i] = pfi * (kInvPi * cp);
+        a_out[3 * i_home] = -kInvPi * ax;
+        a_out[3 * i_home + 1] = -kInvPi * ay;
+        a_out[3 * i_home + 2] = -kInvPi * az;
+        du_out[i_home] = pfi * (kInvPi * cp);
     }
 }
 
 void force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho, const void* pr,
                  int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
-                 int nx, int ny, int nz, int reach, int own_x0, int own_x1, float* a, float* du, cudaStream_t st) {
+                 int nx, int ny, int nz, int reach, uint64_t n_home, float* a, float* du, cudaStream_t st) {
     require_device();
-    if (nx <= 0 || ny <= 0 || nz <= 0 || own_x0 < 0 || own_x1 > nx || own_x0 > own_x1 || reach < 1 || reach > 4)
+    if (nx <= 0 || ny <= 0 || nz <= 0 || n_home > n || reach < 1 || reach > 4)
         throw std::invalid_argument("bad cell grid");
     if (n >= (1ull << 31)) throw std::invalid_argument("force_cells: n must be < 2^31 per device");
     if (int64_t(nx) * ny * nz >= (1ll << 31)) throw std::invalid_argument("bad cell grid");
@@ -472,7 +476,7 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
         cudaFreeAsync(pf, st);
         throw std::domain_error("force: degenerate state, rho == 0");
     }
-    CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, own_x0, own_x1};
+    CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
     const int64_t nn = int64_t(n);
     auto go = [&](auto u) {
         constexpr int U = decltype(u)::value;

@@ -42,10 +42,10 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
 // density.cu
 void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
                    const int32_t* cell_start, const float* lo, float cell, int nx, int ny, int nz, int reach,
-                   int own_x0, int own_x1, float* rho, cudaStream_t st);
+                   uint64_t n_home, float* rho, cudaStream_t st);
 void force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho, const void* pr,
                  int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
-                 int nx, int ny, int nz, int reach, int own_x0, int own_x1, float* a, float* du, cudaStream_t st);
+                 int nx, int ny, int nz, int reach, uint64_t n_home, float* a, float* du, cudaStream_t st);
 uint64_t bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
 void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int nx, int ny, int nz,
                    int32_t* cell_start, int32_t* perm, void* scratch, uint64_t scratch_bytes, cudaStream_t st);

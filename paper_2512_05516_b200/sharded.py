@@ -14,6 +14,9 @@ Rank r owns layers [x0, x1).  One step:
                           grid (own layers + one ghost layer each side), then
                           the cell-linked density over the own layers only
 
+`full_step` runs the reference's timestep order instead: density, a second
+halo of (x, v, m, h, rho, P), the cell-linked force, kick, drift, migrate.
+
 NVSwitch makes every peer equidistant, so slab r simply maps to rank r.  The
 exchange uses only neighbour point-to-point traffic; there is no collective
 on the data path.  The same code runs with gloo on CPU tensors (tests) with
@@ -134,7 +137,29 @@ def migrate_rows(rows: torch.Tensor, xcol: torch.Tensor, slab: Slab, group=None)
     return torch.cat([rows[keep], rl, rr], dim=0)
 
 
+def exchange_ghost_fields(fields: List[torch.Tensor], xcol: torch.Tensor, slab: Slab, group=None) -> List[torch.Tensor]:
+    """Ghost copies of per-particle fields ((n,) or (n,k), one dtype) of the
+    neighbours' boundary layers — the force step's halo (x, v, m, h, rho, P
+    after the density step has produced rho on every rank)."""
+    cols = [f.reshape(f.shape[0], -1) for f in fields]
+    if slab.world == 1:
+        return [f[:0] for f in fields]
+    rows = torch.cat(cols, dim=1)
+    ix = slab.layer(xcol)
+    left = rows[ix == slab.x0] if slab.rank > 0 else rows[:0]
+    right = rows[ix == slab.x1 - 1] if slab.rank < slab.world - 1 else rows[:0]
+    gl, gr = neighbour_exchange(left, right, slab.rank, slab.world, group)
+    g = torch.cat([gl, gr], dim=0)
+    out, c = [], 0
+    for f, col in zip(fields, cols):
+        k = col.shape[1]
+        out.append(g[:, c:c + k].reshape((g.shape[0],) + tuple(f.shape[1:])).contiguous())
+        c += k
+    return out
+
+
 DensityFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor, Slab, int], torch.Tensor]
+ForceFn = Callable[..., Tuple[torch.Tensor, torch.Tensor]]
 
 
 def density_with_ghosts(x, m, h, gx, gm, gh, slab: Slab, backend: DensityFn) -> torch.Tensor:
@@ -172,12 +197,39 @@ def gpu_density_backend(prec: int, refine: int = 2):
         lo = (lo_layer * slab.cell, 0.0, 0.0)
         _mark("bin")
         cs, perm = api.bin_particles(xc.float().contiguous(), lo, cell, dims)
-        own = ((slab.x0 - lo_layer) * refine, (slab.x1 - lo_layer) * refine)
         _mark("pairs")
         rho = api.density_cells(xc.contiguous(), mc.contiguous(), hc.contiguous(), cs, perm, lo, cell, dims,
-                                own=own, reach=refine, prec=prec)
+                                n_home=n_own, reach=refine, prec=prec)
         _mark("store")
         return rho[:n_own]
+
+    return run
+
+
+def force_with_ghosts(own: List[torch.Tensor], ghosts: List[torch.Tensor], slab: Slab,
+                      backend: ForceFn) -> Tuple[torch.Tensor, torch.Tensor]:
+    """(a, du) of the own particles: own rows first, ghosts after;
+    backend(x, v, m, h, rho, P, slab, n_own) -> (a[n_own,3], du[n_own])."""
+    n_own = own[0].shape[0]
+    if ghosts[2].shape[0] == 0:
+        return backend(*own, slab, n_own)
+    comb = [torch.cat([o, g.to(o.dtype)], dim=0) for o, g in zip(own, ghosts)]
+    return backend(*comb, slab, n_own)
+
+
+def gpu_force_backend(prec: int, refine: int = 2):
+    """bin_particles + force_cells on the rank's local grid (as the density)."""
+    from . import api
+
+    def run(x, v, m, h, rho, P, slab: Slab, n_own: int):
+        lo_layer, hi_layer = slab.local_lo, slab.local_hi
+        cell = slab.cell / refine
+        dims = ((hi_layer - lo_layer) * refine, slab.nc * refine, slab.nc * refine)
+        lo = (lo_layer * slab.cell, 0.0, 0.0)
+        cs, perm = api.bin_particles(x.float().contiguous(), lo, cell, dims)
+        a, du = api.force_cells(x.contiguous(), v.contiguous(), m.contiguous(), h.contiguous(), rho.contiguous(),
+                                P.contiguous(), cs, perm, lo, cell, dims, n_home=n_own, reach=refine, prec=prec)
+        return a[:n_own], du[:n_own]
 
     return run
 
@@ -269,6 +321,27 @@ class ShardedState:
         rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec))
         self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
         _mark("end")
+
+    def force(self, group=None):
+        """Cell-linked force with the neighbours' (x, v, m, h, rho, P) as
+        ghosts (second halo, after every rank has its rho)."""
+        names = ["x", "v", "m", "h", "rho", "P"]
+        own = [self.stream(k) for k in names]
+        _mark("halo2")
+        ghosts = exchange_ghost_fields(own, own[0][:, 0], self.slab, group)
+        prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
+        a, du = force_with_ghosts(own, ghosts, self.slab, gpu_force_backend(prec))
+        self.stream("a").copy_(a.to(self.stream("a").dtype))
+        self.stream("du").copy_(du.to(self.stream("du").dtype))
+        _mark("end2")
+
+    def full_step(self, dt=1e-3, group=None):
+        """The reference timestep order (density -> force -> kick -> drift,
+        pipelines.cpp / bench.cpp kernel lists), then migration."""
+        self.density(group)
+        self.force(group)
+        self.kick_drift(dt)
+        self.migrate(group)
 
     def sort_by_cell(self, refine: int = 2):
         """Reorder every field into cell order (the density binning's order), so

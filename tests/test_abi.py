@@ -210,12 +210,11 @@ def test_cell_entry_points_fail_loudly_without_device():
     i32 = (C.c_int32 * (n + 8))()
     lo = (C.c_float * 3)(0, 0, 0)
     p = lambda a: C.cast(a, C.c_void_p)  # noqa: E731
-    st = L.lib().sf_b200_density_cells(p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2, 1, 0, 2, p(f),
-                                       None)
+    st = L.lib().sf_b200_density_cells(p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2, 1, n, p(f), None)
     assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
     st = L.lib().sf_b200_force_cells(p(f), p(f), p(f), p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2,
-                                     1, 0, 2, p(f), p(f), None)
+                                     1, n, p(f), p(f), None)
     assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
     st = L.lib().sf_b200_force_cells(None, p(f), p(f), p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2,
-                                     1, 0, 2, p(f), p(f), None)
+                                     1, n, p(f), p(f), None)
     assert st == L.SF_INVALID_ARG

@@ -288,23 +288,24 @@ def test_density_cells_vs_oracle(prec, refine):
         assert np.all(np.diff(perm_h[cs_h[c]:cs_h[c + 1]]) > 0)
 
 
-def test_density_cells_own_layers_and_ghosts():
-    """Only own x-layers are computed; ghost layers feed neighbours only."""
+def test_density_cells_homes_and_ghosts():
+    """Only the first n_home particles are computed; the rest (ghosts) feed
+    their neighbours only and keep rho untouched."""
     n = 1 << 14
     rng = np.random.default_rng(4)
     x = rng.random((n, 3))
     h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3))
     m = np.full(n, 1.0 / n)
     nc = int(np.floor(1.0 / (2 * h[0])))
+    n_home = n - 3000
     xt, mt, ht = (torch.tensor(a, device="cuda", dtype=torch.float32) for a in (x, m, h))
     cs, perm = api.bin_particles(xt, (0, 0, 0), 1.0 / nc, (nc, nc, nc))
-    own = (2, nc - 3)
-    rho = api.density_cells(xt, mt, ht, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc), own=own).cpu().numpy()
+    rho = torch.full((n,), -1.0, device="cuda")
+    api.density_cells(xt, mt, ht, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc), n_home=n_home, rho=rho)
+    rho = rho.cpu().numpy()
     want = O.density_cells(x.reshape(-1), m, h, 0.0, 1.0, 1.0 / nc)
-    layer = np.minimum(np.floor(x[:, 0] * nc).astype(int), nc - 1)
-    mine = (layer >= own[0]) & (layer < own[1])
-    np.testing.assert_allclose(rho[mine], want[mine], rtol=1e-5)
-    assert np.all(rho[~mine] == 0)
+    np.testing.assert_allclose(rho[:n_home], want[:n_home], rtol=1e-5)
+    assert np.all(rho[n_home:] == -1.0)
 
 
 # ----------------------------------------------------------- cell force
@@ -347,19 +348,17 @@ def test_force_cells_vs_oracle(prec, refine):
     assert np.median(np.linalg.norm(want_a, axis=1) / sa) > 1e-3
 
 
-def test_force_cells_own_layers_and_degenerate():
+def test_force_cells_homes_and_degenerate():
     n = 1 << 14
     ts, (xd, vd, md, hd, rd, Pd) = _force_case(n, 6, api.SF_PREC_NATIVE)
     nc = int(np.floor(1.0 / float(2 * ts[3].max())))
     cs, perm = api.bin_particles(ts[0].contiguous(), (0, 0, 0), 1.0 / nc, (nc, nc, nc))
-    own = (2, nc - 3)
-    a, du = api.force_cells(*ts, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc), own=own)
+    n_home = n // 2
+    a, du = api.force_cells(*ts, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc), n_home=n_home)
     want_a, want_du, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rd, Pd, 0.0, 1.0, 1.0 / nc)
-    layer = np.minimum(np.floor(xd[:, 0] * nc).astype(int), nc - 1)
-    mine = (layer >= own[0]) & (layer < own[1])
     err = np.linalg.norm(a.double().cpu().numpy() - want_a, axis=1)
-    assert np.all(err[mine] <= FORCE_TOL * sa[mine])
-    assert np.all(a.cpu().numpy()[~mine] == 0) and np.all(du.cpu().numpy()[~mine] == 0)
+    assert np.all(err[:n_home] <= FORCE_TOL * sa[:n_home])
+    assert np.all(a.cpu().numpy()[n_home:] == 0) and np.all(du.cpu().numpy()[n_home:] == 0)
     ts[4][17] = 0.0  # rho == 0 anywhere: the reference's domain_error
     with pytest.raises(api.L.SfError, match="rho == 0"):
         api.force_cells(*ts, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc))

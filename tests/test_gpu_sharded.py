@@ -54,3 +54,58 @@ def test_rank_density_with_ghost_layers(world):
         np.testing.assert_allclose(rho.double().cpu().numpy(), want[own], rtol=1e-5)
         seen |= own
     assert seen.all()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_rank_force_with_ghost_layers(world):
+    """Per-rank cell-linked force over own + ghost (x, v, m, h, rho, P) rows
+    (simulated splits of one population) against the global oracle force."""
+    from paper_2512_05516_b200.sharded import force_with_ghosts, gpu_force_backend
+    n = 1 << 15
+    rng = np.random.default_rng(10)
+    x = rng.random((n, 3))
+    v = rng.uniform(-1, 1, (n, 3))
+    h, nc, cell = grid_for(n)
+    hh, m = np.full(n, h), np.full(n, 1.0 / n)
+    rho, P = rng.uniform(0.5, 1.5, n), rng.uniform(0.2, 1.2, n)
+    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+    dec = lambda a: t(a).double().cpu().numpy()  # noqa: E731  (the stored binary32 values)
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(hh), dec(rho), dec(P),
+                                    0.0, 1.0, cell)
+    layer = np.minimum(np.floor(x[:, 0] / cell).astype(int), nc - 1)
+    seen = np.zeros(n, bool)
+    for r in range(world):
+        slab = Slab(nc, cell, r, world)
+        own = (layer >= slab.x0) & (layer < slab.x1)
+        ghost = ((layer == slab.x0 - 1) | (layer == slab.x1)) & ~own
+        a, du = force_with_ghosts([t(f[own]) for f in (x, v, m, hh, rho, P)],
+                                  [t(f[ghost]) for f in (x, v, m, hh, rho, P)], slab,
+                                  gpu_force_backend(api.SF_PREC_NATIVE))
+        assert np.all(np.linalg.norm(a.double().cpu().numpy() - wa[own], axis=1) <= 2e-5 * sa[own])
+        assert np.all(np.abs(du.double().cpu().numpy() - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
+        seen |= own
+    assert seen.all()
+
+
+def test_single_rank_full_step_runs_reference_order():
+    """density -> force -> kick -> drift on one rank: a/du come from the force
+    on the fresh rho, then kick/drift use them (checked against the oracle)."""
+    n = 1 << 15
+    h, nc, cell = grid_for(n)
+    st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h)
+    st.sort_by_cell()
+    st.stream("P").copy_(torch.rand(st.n, device="cuda") + 0.2)
+    before = {k: st.stream(k).double().cpu().numpy().copy() for k in ["x", "v", "u", "m", "h", "P"]}
+    st.full_step(1e-3)
+    torch.cuda.synchronize()
+    rho = st.stream("rho").double().cpu().numpy()
+    want_rho = O.density_cells(before["x"].reshape(-1), before["m"], before["h"], 0.0, 1.0, cell)
+    np.testing.assert_allclose(rho, want_rho.astype(np.float32), rtol=2e-5)
+    wa, wdu, sa, sd = O.force_cells(before["x"].reshape(-1), before["v"].reshape(-1), before["m"], before["h"], rho,
+                                    before["P"], 0.0, 1.0, cell)
+    a = st.stream("a").double().cpu().numpy()
+    assert np.all(np.linalg.norm(a - wa, axis=1) <= 2e-5 * sa + 1e-6 * np.abs(wa).max())
+    # kick used the stored a/du
+    du = st.stream("du").double().cpu().numpy()
+    v2, u2 = O.kick(before["v"], before["u"], a, du, 1e-3)
+    np.testing.assert_array_equal(st.stream("v").double().cpu().numpy(), v2.astype(np.float32).astype(np.float64))
