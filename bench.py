@@ -405,6 +405,8 @@ def main():
                     help="BASELINE.json config (default c2 = configs[1], the headline)")
     ap.add_argument("--c4-n", type=int, default=1 << 26)
     ap.add_argument("--c5-n", type=int, default=1 << 27)
+    ap.add_argument("--c5-full", action="store_true",
+                    help="C5 with the full reference timestep (density, force, kick, drift)")
     ap.add_argument("--refine", type=int, default=2,
                     help="C3/C5 binning cells per density cell side (searched with reach = refine)")
     args = ap.parse_args()

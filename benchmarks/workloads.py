@@ -226,29 +226,45 @@ def c5(args, peak, peak_kind, world, rank, group=None):
     st = ShardedState(n, slab, prec=32, h=h)
     st.sort_by_cell()  # particles kept in cell order (re-sorted every few steps in a long run)
     for _ in range(max(1, min(args.warmup, 2))):
-        st.step(group=group)
+        st.full_step(group=group) if args.c5_full else st.step(group=group)
     torch.cuda.synchronize()
     phases = {"kick_drift": [], "migrate": [], "density": []}
+    if args.c5_full:
+        phases["force"] = []
     times = []
     for _ in range(max(2, min(args.steps, 5))):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
-        c = torch.cuda.Event(enable_timing=True); d = torch.cuda.Event(enable_timing=True)
-        a.record()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        if args.c5_full:  # the reference's timestep order: density, force, kick+drift, migrate
+            st.density(group)
+            ev[1].record()
+            st.force(group)
+            ev[2].record()
+            st.kick_drift()
+            ev[3].record()
+            st.migrate(group)
+            ev[4].record()
+            ev[4].synchronize()
+            phases["density"].append(ev[0].elapsed_time(ev[1]))
+            phases["force"].append(ev[1].elapsed_time(ev[2]))
+            phases["kick_drift"].append(ev[2].elapsed_time(ev[3]))
+            phases["migrate"].append(ev[3].elapsed_time(ev[4]))
+            times.append(ev[0].elapsed_time(ev[4]))
+            continue
         st.kick_drift()
-        b.record()
+        ev[1].record()
         st.migrate(group)
-        c.record()
+        ev[2].record()
         st.density(group)
-        d.record()
-        d.synchronize()
-        phases["kick_drift"].append(a.elapsed_time(b))
-        phases["migrate"].append(b.elapsed_time(c))
-        phases["density"].append(c.elapsed_time(d))
-        times.append(a.elapsed_time(d))
+        ev[3].record()
+        ev[3].synchronize()
+        phases["kick_drift"].append(ev[0].elapsed_time(ev[1]))
+        phases["migrate"].append(ev[1].elapsed_time(ev[2]))
+        phases["density"].append(ev[2].elapsed_time(ev[3]))
+        times.append(ev[0].elapsed_time(ev[3]))
     ms = sum(times) / len(times)
     # one more step with sub-phase events (not part of the timed mean)
     import paper_2512_05516_b200.sharded as SH
@@ -265,8 +281,10 @@ def c5(args, peak, peak_kind, world, rank, group=None):
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
             "roofline": {"bound": "compute (density)", "achieved": None, "peak": peak, "unit": "GB/s",
                          "frac": None, "kernel": "k_pairs_c + k_update_soa (kick/drift)"},
-            "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + kick/drift sharded by cell "
-                                   "with NCCL halo exchange" % (n >> 20), "particles_total": n,
+            "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + %skick/drift sharded by cell "
+                                   "with NCCL halo exchange" % (n >> 20, "force + " if args.c5_full else ""),
+                       "particles_total": n, "step": "full (density, force, kick, drift, migrate)" if args.c5_full
+                       else "kick, drift, migrate, density",
                        "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},
             "phases_ms": {k: (sum(v) / len(v) if k != "density_sub" else v[0]) for k, v in phases.items()},
             "particles_local": st.n}

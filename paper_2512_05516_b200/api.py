@@ -97,9 +97,12 @@ class Schema:
         return out.value.decode()
 
     def __del__(self):
-        if getattr(self, "_h", None) and L._lib is not None:
-            L._lib.sf_schema_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and L._lib is not None:
+                L._lib.sf_schema_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: module globals already gone
+            pass
 
 
 class View:
@@ -140,9 +143,12 @@ class View:
                     self.exclude if exclude is None else exclude)
 
     def __del__(self):
-        if getattr(self, "_h", None) and L._lib is not None:
-            L._lib.sf_b200_view_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and L._lib is not None:
+                L._lib.sf_b200_view_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: module globals already gone
+            pass
 
 
 def _stream():

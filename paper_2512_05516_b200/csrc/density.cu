@@ -77,6 +77,15 @@ struct CellGrid {
     int64_t n_home;  // particles [0, n_home) (particle order) are homes; the rest neighbours only
 };
 
+// The home kernels run one thread per home over a grid of ceil(n/256) CTAs
+// (not a capped grid-stride loop): the block scheduler hands out CTAs in
+// index order, so the CTAs in flight always cover one compact range of the
+// cell-sorted homes and their candidate columns stay in L2.  With the grid
+// capped at 16 CTAs/SM, each resident CTA strode through the whole range,
+// the in-flight set scattered across it and the L2 hit rate of k_pairs_c
+// at C5 (128M) fell to 46% (91% uncapped; 54 -> 46 ms).
+static unsigned home_grid(uint64_t n) { return unsigned((n + 255) / 256); }
+
 __global__ void __launch_bounds__(256) k_pairs(const float4* __restrict__ pos,
                                                const float* __restrict__ mass, const int32_t* __restrict__ cell_start,
                                                const int32_t* __restrict__ perm, CellGrid G, int64_t n,
@@ -299,11 +308,12 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
     else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
     // SFB_PAIRS=0 selects the unculled per-run loop (round-1 kernel) for comparison
+    const unsigned hgrid = home_grid(n);
     if (env_int_d("SFB_PAIRS", 1) != 0) {
-        if (reach == 1) k_pairs_c<1><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
-        else if (reach == 2) k_pairs_c<2><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
-        else if (reach == 3) k_pairs_c<3><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
-        else k_pairs_c<4><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        if (reach == 1) k_pairs_c<1><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        else if (reach == 2) k_pairs_c<2><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        else if (reach == 3) k_pairs_c<3><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        else k_pairs_c<4><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
     } else if (reach == 1) {
         k_pairs_r<1><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
     } else if (reach == 2) {
@@ -478,12 +488,13 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
     }
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
     const int64_t nn = int64_t(n);
+    const unsigned hgrid = home_grid(n);
     auto go = [&](auto u) {
         constexpr int U = decltype(u)::value;
-        if (reach == 1) k_force_c<1, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-        else if (reach == 2) k_force_c<2, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-        else if (reach == 3) k_force_c<3, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-        else k_force_c<4, U><<<blocks, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        if (reach == 1) k_force_c<1, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        else if (reach == 2) k_force_c<2, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        else if (reach == 3) k_force_c<3, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
+        else k_force_c<4, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
     };
     if (env_int_d("SFB_FORCE_UNROLL", 2) == 2) go(std::integral_constant<int, 2>{});
     else go(std::integral_constant<int, 1>{});

@@ -183,20 +183,30 @@ def _mark(name):
         PHASES.setdefault("_events", []).append((name, e))
 
 
-def gpu_density_backend(prec: int, refine: int = 2):
+def local_grid(slab: Slab, refine: int):
+    """Binning grid of a rank: own layers plus one ghost layer per side, the
+    slab cells split `refine` times per axis."""
+    lo_layer, hi_layer = slab.local_lo, slab.local_hi
+    cell = slab.cell / refine
+    dims = ((hi_layer - lo_layer) * refine, slab.nc * refine, slab.nc * refine)
+    return (lo_layer * slab.cell, 0.0, 0.0), cell, dims
+
+
+def gpu_density_backend(prec: int, refine: int = 2, keep: Optional[dict] = None):
     """bin_particles + density_cells on the rank's local grid (own layers plus
     one ghost layer per side).  Binning cells are the slab cells split
     `refine` times per axis (side >= 2h/refine), searched with reach=refine:
-    ~42% fewer candidate pairs at refine 2 than 27 cells of side 2h."""
+    ~42% fewer candidate pairs at refine 2 than 27 cells of side 2h.  With
+    `keep`, the binning is left there for a following force on the same
+    own+ghost rows."""
     from . import api
 
     def run(xc, mc, hc, slab: Slab, n_own: int) -> torch.Tensor:
-        lo_layer, hi_layer = slab.local_lo, slab.local_hi
-        cell = slab.cell / refine
-        dims = ((hi_layer - lo_layer) * refine, slab.nc * refine, slab.nc * refine)
-        lo = (lo_layer * slab.cell, 0.0, 0.0)
+        lo, cell, dims = local_grid(slab, refine)
         _mark("bin")
         cs, perm = api.bin_particles(xc.float().contiguous(), lo, cell, dims)
+        if keep is not None:
+            keep.update(cs=cs, perm=perm, n=xc.shape[0])
         _mark("pairs")
         rho = api.density_cells(xc.contiguous(), mc.contiguous(), hc.contiguous(), cs, perm, lo, cell, dims,
                                 n_home=n_own, reach=refine, prec=prec)
@@ -217,16 +227,18 @@ def force_with_ghosts(own: List[torch.Tensor], ghosts: List[torch.Tensor], slab:
     return backend(*comb, slab, n_own)
 
 
-def gpu_force_backend(prec: int, refine: int = 2):
-    """bin_particles + force_cells on the rank's local grid (as the density)."""
+def gpu_force_backend(prec: int, refine: int = 2, binning: Optional[dict] = None):
+    """bin_particles + force_cells on the rank's local grid (as the density).
+    `binning` from the density of the same rows (same positions, same ghost
+    rows in the same order) skips the second counting sort."""
     from . import api
 
     def run(x, v, m, h, rho, P, slab: Slab, n_own: int):
-        lo_layer, hi_layer = slab.local_lo, slab.local_hi
-        cell = slab.cell / refine
-        dims = ((hi_layer - lo_layer) * refine, slab.nc * refine, slab.nc * refine)
-        lo = (lo_layer * slab.cell, 0.0, 0.0)
-        cs, perm = api.bin_particles(x.float().contiguous(), lo, cell, dims)
+        lo, cell, dims = local_grid(slab, refine)
+        if binning and binning.get("n") == x.shape[0]:
+            cs, perm = binning["cs"], binning["perm"]
+        else:
+            cs, perm = api.bin_particles(x.float().contiguous(), lo, cell, dims)
         a, du = api.force_cells(x.contiguous(), v.contiguous(), m.contiguous(), h.contiguous(), rho.contiguous(),
                                 P.contiguous(), cs, perm, lo, cell, dims, n_home=n_own, reach=refine, prec=prec)
         return a[:n_own], du[:n_own]
@@ -268,6 +280,7 @@ class ShardedState:
         return self.api.View(self.schema, n, "soa", None, self.prec)
 
     def set_fields(self, fields):
+        self._binning = None
         n = fields["id"].shape[0]
         self.n = n
         self.buf = self.api.PackedBuffer.empty(self.view(n), self.device)
@@ -304,6 +317,7 @@ class ShardedState:
 
     # -- the step ---------------------------------------------------------------
     def kick_drift(self, dt=1e-3):
+        self._binning = None  # positions change
         self.api.run_kernel(self.buf, "kick", dt, buffer_size=1)
         self.api.run_kernel(self.buf, "drift", dt, buffer_size=1)
 
@@ -318,7 +332,8 @@ class ShardedState:
         _mark("halo")
         gx, gm, gh = exchange_halo(x, m, h, self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
-        rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec))
+        self._binning = {}
+        rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec, keep=self._binning))
         self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
         _mark("end")
 
@@ -330,7 +345,7 @@ class ShardedState:
         _mark("halo2")
         ghosts = exchange_ghost_fields(own, own[0][:, 0], self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
-        a, du = force_with_ghosts(own, ghosts, self.slab, gpu_force_backend(prec))
+        a, du = force_with_ghosts(own, ghosts, self.slab, gpu_force_backend(prec, binning=self._binning))
         self.stream("a").copy_(a.to(self.stream("a").dtype))
         self.stream("du").copy_(du.to(self.stream("du").dtype))
         _mark("end2")
