@@ -131,8 +131,9 @@ def c3(args, peak, peak_kind):
         for _ in range(args.warmup):
             fn()
         t = timed_each(fn, max(3, args.steps // 5))
-        tb = timed_each(lambda: api.bin_particles(xf, (0, 0, 0), fine, dims, cell_start=cs, perm=perm),
-                        max(3, args.steps // 5))
+        fb = lambda: api.bin_particles(xf, (0, 0, 0), fine, dims, cell_start=cs, perm=perm)  # noqa: E731
+        fb()  # scratch allocation outside the timed launches
+        tb = timed_each(fb, max(3, args.steps // 5))
         msd, msb = sum(t) / len(t), sum(tb) / len(tb)
         # pairs inside the support, for pairs/s
         pairs = None

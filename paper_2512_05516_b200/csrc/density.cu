@@ -516,7 +516,9 @@ __global__ void k_cell_ids(const float* __restrict__ x, uint64_t n, float lox, f
         cz = min(max(cz, 0), nz - 1);
         const int c = (cx * ny + cy) * nz + cz;
         cid[i] = c;
-        atomicAdd(&counts[c], 1);
+        // lanes of one cell (cell-sorted input: most of a warp) share one atomic
+        const unsigned peers = __match_any_sync(__activemask(), c);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[c], __popc(peers));
     }
 }
 
@@ -578,9 +580,16 @@ static void exclusive_scan(int32_t* a, int64_t n, int32_t* scratch, cudaStream_t
 
 __global__ void k_place(const int32_t* __restrict__ cid, uint64_t n, const int32_t* __restrict__ start,
                         int32_t* __restrict__ fill, int32_t* __restrict__ perm) {
+    const int lane = threadIdx.x & 31;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const int c = cid[i];
-        perm[start[c] + atomicAdd(&fill[c], 1)] = int32_t(i);
+        // one atomic per (warp, cell); lanes take consecutive slots in lane order
+        const unsigned peers = __match_any_sync(__activemask(), c);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&fill[c], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        perm[start[c] + base + __popc(peers & ((1u << lane) - 1))] = int32_t(i);
     }
 }
 
@@ -639,7 +648,9 @@ void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int 
     int32_t* scan_tmp = fill + ncell;
     check_cuda(cudaMemsetAsync(cell_start, 0, sizeof(int32_t) * (ncell + 1), st), "memset");
     check_cuda(cudaMemsetAsync(fill, 0, sizeof(int32_t) * ncell, st), "memset");
-    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256 + 1, 148ull * 32));
+    // uncapped grids: the CTAs in flight touch one compact range of particles
+    // (and, for cell-sorted input, of cells)
+    const unsigned blocks = unsigned((n + 255) / 256);
     if (n) {
         k_cell_ids<<<blocks, 256, 0, st>>>(x, n, lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, cid, cell_start);
         count_launches(1);
@@ -647,7 +658,7 @@ void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int 
     exclusive_scan(cell_start, ncell + 1, scan_tmp, st);  // counts -> starts (last entry = n)
     if (n) {
         k_place<<<blocks, 256, 0, st>>>(cid, n, cell_start, fill, perm);
-        k_sort_runs<<<unsigned(std::min<int64_t>((ncell + 255) / 256, 148ll * 32)), 256, 0, st>>>(cell_start, ncell, perm);
+        k_sort_runs<<<unsigned((ncell + 255) / 256), 256, 0, st>>>(cell_start, ncell, perm);
         count_launches(2);
     }
     check_cuda(cudaGetLastError(), "bin launch");
