@@ -137,6 +137,42 @@ SF_API sf_status sf_b200_density_cells(const void* x, const void* m, const void*
                                        uint64_t n, const int32_t* perm, const int32_t* cell_start,
                                        const float* lo, float cell, int nx, int ny, int nz, int reach,
                                        uint64_t n_home, float* rho_out, void* stream);
+/* Multi-block cell-linked density: the homes' own block plus up to two
+ * neighbouring slabs' blocks read in place (multi-GPU: peer pointers over
+ * NVLink from sf_b200_ipc_open — the halo is never copied).  Every block is
+ * one x-slab [x0, x0 + nx) of a global grid (cell side, nx_global x-layers,
+ * ny, nz; y/z origin lo_yz[2]) with its own cell list (sf_b200_bin_particles
+ * over its layers with lo = {x_origin, lo_yz[0], lo_yz[1]}) and packed
+ * particles (sf_b200_cells_pack). */
+typedef struct sf_cell_block {
+    const void* pos;            /* float4 (x, y, z, h) per particle, cell-sorted */
+    const float* mass;          /* cell-sorted masses */
+    const int32_t* cell_start;  /* nx*ny*nz + 1 entries */
+    const uint32_t* hmax;       /* the block's largest h (float bits) */
+    int32_t x0, nx;             /* global x-layers held by the block */
+    float x_origin;             /* the lo[0] its binning used (layer x0 starts there) */
+    int32_t reserved;           /* 0 */
+} sf_cell_block;
+#define SF_IPC_HANDLE_BYTES 64
+/* Packs x (3n), m, h (n) in `prec` through perm (sorted position -> particle)
+ * into caller-owned pos_out (16*n bytes, 16-B aligned), mass_out (4*n) and
+ * hmax_out (one word). */
+SF_API sf_status sf_b200_cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n,
+                                    const int32_t* perm, void* pos_out, float* mass_out,
+                                    uint32_t* hmax_out, void* stream);
+/* rho of the first n_home particles (particle order) of blocks[0] (n particles,
+ * perm from its binning); candidates from every block. */
+SF_API sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int nblocks, uint64_t n,
+                                              const int32_t* perm, uint64_t n_home, const float* lo_yz,
+                                              float cell, int nx_global, int ny, int nz, int reach,
+                                              float* rho_out, void* stream);
+/* Device memory that another process can map (cudaMalloc base), and CUDA IPC
+ * handles for it (same node; NVLink/NVSwitch peers or the same device). */
+SF_API sf_status sf_b200_dev_alloc(uint64_t bytes, void** ptr);
+SF_API sf_status sf_b200_dev_free(void* ptr);
+SF_API sf_status sf_b200_ipc_handle(const void* dev_ptr, uint8_t handle[SF_IPC_HANDLE_BYTES]);
+SF_API sf_status sf_b200_ipc_open(const uint8_t handle[SF_IPC_HANDLE_BYTES], void** dev_ptr);
+SF_API sf_status sf_b200_ipc_close(void* dev_ptr);
 /* Cell-linked force (the reference's force_kernel, sph.cpp:201-245, over
  * cell neighbours instead of 64-particle buffers): x, v: 3*n lanes; m, h,
  * rho, P: n lanes, all in `prec` and particle order; grid, perm and

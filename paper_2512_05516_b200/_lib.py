@@ -17,6 +17,15 @@ SF_MATH_FP64_EXACT, SF_MATH_FP32 = 0, 1
 SF_MODE_STREAMED, SF_MODE_MANAGED, SF_MODE_INPLACE = 0, 1, 2
 
 
+class SfCellBlock(C.Structure):
+    """sf_cell_block (include/soaforge_b200.h)."""
+    _fields_ = [("pos", C.c_void_p), ("mass", C.c_void_p), ("cell_start", C.c_void_p), ("hmax", C.c_void_p),
+                ("x0", C.c_int32), ("nx", C.c_int32), ("x_origin", C.c_float), ("reserved", C.c_int32)]
+
+
+SF_IPC_HANDLE_BYTES = 64
+
+
 class SfError(RuntimeError):
     """SF_ERROR (generic failure, including CUDA errors / missing device)."""
 
@@ -75,6 +84,13 @@ SYMBOLS = [
     ("sf_b200_run_kernel", i32, [P, P, s, f64, u64, i32, i32, P]),
     ("sf_b200_density_cells", i32, [P, P, P, i32, u64, P, P, P, C.c_float, i32, i32, i32, i32, u64, P, P]),
     ("sf_b200_force_cells", i32, [P] * 6 + [i32, u64, P, P, P, C.c_float] + [i32] * 4 + [u64, P, P, P]),
+    ("sf_b200_cells_pack", i32, [P, P, P, i32, u64, P, P, P, P, P]),
+    ("sf_b200_density_cells_blocks", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P]),
+    ("sf_b200_dev_alloc", i32, [u64, PP]),
+    ("sf_b200_dev_free", i32, [P]),
+    ("sf_b200_ipc_handle", i32, [P, P]),
+    ("sf_b200_ipc_open", i32, [P, PP]),
+    ("sf_b200_ipc_close", i32, [P]),
     ("sf_b200_bin_particles", i32, [P, u64, P, C.c_float, i32, i32, i32, P, P, P, u64, P]),
     ("sf_b200_bin_scratch_bytes", u64, [u64, i32, i32, i32]),
     ("sf_b200_run_host", i32, [P, P, P, s, f64, i32, i32, u64, P, C.POINTER(C.c_double)]),

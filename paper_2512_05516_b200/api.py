@@ -287,6 +287,86 @@ def force_cells(x, v, m, h, rho, P, cell_start, perm, lo, cell: float, dims, n_h
     return a, du
 
 
+def cells_pack(x, m, h, perm, pos, mass, hmax, prec: int = SF_PREC_NATIVE):
+    """Pack x (n,3), m, h (n,) through perm (sorted position -> particle) into
+    caller-owned float4 pos (n,4), mass (n,) and hmax (1 int32 word)."""
+    n = m.shape[0]
+    check(lib().sf_b200_cells_pack(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
+                                   _ptr(pos), _ptr(mass), _ptr(hmax), _stream()))
+
+
+def cell_block(pos, mass, cell_start, hmax, x0: int, nx: int, x_origin: float) -> "L.SfCellBlock":
+    """One sf_cell_block from device tensors or raw device addresses (ints);
+    x_origin = the lo[0] the block's bin_particles used."""
+    addr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
+    return L.SfCellBlock(addr(pos), addr(mass), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
+
+
+def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,
+                         reach: int = 1, rho=None):
+    """Cell-linked density of blocks[0]'s first n_home particles with
+    candidates from every block (own slab + neighbouring slabs in place)."""
+    import torch
+    n_home = n if n_home is None else n_home
+    rho = rho if rho is not None else torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+    arr = (L.SfCellBlock * len(blocks))(*blocks)
+    lo_arr = (C.c_float * 2)(*[float(t) for t in lo_yz])
+    check(lib().sf_b200_density_cells_blocks(C.cast(arr, C.c_void_p), len(blocks), n,
+                                             _ptr(perm) if perm is not None else None, n_home,
+                                             C.cast(lo_arr, C.c_void_p), float(cell), nx_global, ny, nz, reach,
+                                             _ptr(rho), _stream()))
+    return rho
+
+
+class DeviceBuffer:
+    """cudaMalloc'd device memory (an IPC-shareable allocation base), or a
+    mapping of another process's buffer opened from its IPC handle."""
+
+    def __init__(self, nbytes: int = 0, handle: Optional[bytes] = None):
+        p = C.c_void_p()
+        if handle is not None:
+            h = (C.c_uint8 * L.SF_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+            check(lib().sf_b200_ipc_open(C.cast(h, C.c_void_p), C.byref(p)))
+            self.opened = True
+        else:
+            check(lib().sf_b200_dev_alloc(nbytes, C.byref(p)))
+            self.opened = False
+        self.ptr, self.nbytes = p.value, nbytes
+
+    def ipc_handle(self) -> bytes:
+        h = (C.c_uint8 * L.SF_IPC_HANDLE_BYTES)()
+        check(lib().sf_b200_ipc_handle(C.c_void_p(self.ptr), C.cast(h, C.c_void_p)))
+        return bytes(h)
+
+    def tensor(self, offset: int, shape, dtype):
+        """A torch view of [offset, offset + size) of this buffer (no copy)."""
+        import torch
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.float64: "<f8", torch.uint8: "|u1"}[dtype]
+        shape = tuple(shape)
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (self.ptr + offset, False),
+                                        "version": 3, "strides": None}
+        t = torch.as_tensor(_Iface(), device="cuda")
+        assert t.data_ptr() == self.ptr + offset and t.element_size() == itemsize
+        return t
+
+    def free(self):
+        if self.ptr:
+            if self.opened:
+                check(lib().sf_b200_ipc_close(C.c_void_p(self.ptr)))
+            else:
+                check(lib().sf_b200_dev_free(C.c_void_p(self.ptr)))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class HostBuffer:
     """Pinned (mode 0) or managed (mode 1) host memory for run_host."""
 

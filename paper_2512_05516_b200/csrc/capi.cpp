@@ -12,6 +12,7 @@
 #include <cmath>
 #include <memory>
 #include <sstream>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -274,6 +275,80 @@ sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const
     return guarded([&] {
         force_cells(x, v, m, h, rho, P, prec, n, perm, cell_start, lo, cell, nx, ny, nz, reach, n_home, a_out,
                     du_out, static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
+static_assert(sizeof(sf_cell_block) == sizeof(CellBlockDesc), "sf_cell_block layout");
+
+sf_status sf_b200_cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
+                             void* pos_out, float* mass_out, uint32_t* hmax_out, void* stream) {
+    if ((n && (!x || !m || !h || !pos_out || !mass_out)) || !hmax_out) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        cells_pack(x, m, h, prec, n, perm, pos_out, mass_out, hmax_out, static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int nblocks, uint64_t n, const int32_t* perm,
+                                       uint64_t n_home, const float* lo_yz, float cell, int nx_global, int ny, int nz,
+                                       int reach, float* rho_out, void* stream) {
+    if (!blocks || !lo_yz || (n && !rho_out)) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        std::vector<CellBlockDesc> d(size_t(std::max(nblocks, 0)));
+        for (int g = 0; g < nblocks; ++g)
+            d[g] = CellBlockDesc{blocks[g].pos,    blocks[g].mass,     blocks[g].cell_start, blocks[g].hmax,
+                                 blocks[g].x0,     blocks[g].nx,       blocks[g].x_origin,   0};
+        density_cells_blocks(d.data(), nblocks, n, perm, n_home, lo_yz, cell, nx_global, ny, nz, reach, rho_out,
+                             static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_dev_alloc(uint64_t bytes, void** out) {
+    if (!out) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        require_device();
+        *out = nullptr;
+        check_cuda(cudaMalloc(out, bytes ? bytes : 1), "cudaMalloc");
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_dev_free(void* p) {
+    return guarded([&] {
+        if (p) check_cuda(cudaFree(p), "cudaFree");
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_ipc_handle(const void* p, uint8_t* handle) {
+    if (!p || !handle) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        require_device();
+        cudaIpcMemHandle_t hd;
+        check_cuda(cudaIpcGetMemHandle(&hd, const_cast<void*>(p)), "cudaIpcGetMemHandle");
+        static_assert(sizeof(hd) == SF_IPC_HANDLE_BYTES, "IPC handle size");
+        memcpy(handle, &hd, sizeof(hd));
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_ipc_open(const uint8_t* handle, void** out) {
+    if (!handle || !out) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        require_device();
+        cudaIpcMemHandle_t hd;
+        memcpy(&hd, handle, sizeof(hd));
+        check_cuda(cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_ipc_close(void* p) {
+    if (!p) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        check_cuda(cudaIpcCloseMemHandle(p), "cudaIpcCloseMemHandle");
         return SF_OK;
     });
 }

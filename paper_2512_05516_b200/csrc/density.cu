@@ -218,21 +218,41 @@ __device__ __forceinline__ float pair_term(const float4 pi, float hh_i, const fl
 // their inner side.  Culling removes only candidates at q >= 2 (w = 0; a
 // 1e-5 radius margin covers rounding), and every candidate runs the
 // branch-free pair_term.
+// Candidate blocks: the homes' own cell-sorted block [0] plus up to two
+// neighbouring slabs' blocks [1], [2] (multi-GPU: their packed arrays read in
+// place over NVLink through peer pointers, no ghost copy).  Each block covers
+// global x-layers [x0, x0 + nx) of one grid (shared origin, cell, ny, nz).
+struct CellBlock {
+    const float4* pos;
+    const float* mass;
+    const int32_t* cs;
+    const unsigned* hmax;
+    int x0, nx;
+    float lox;  // x origin the block was binned with (its layer x0 starts there)
+};
+struct BlockSet {
+    CellBlock b[3];
+    int nb, NX;  // blocks in use; global x-layers (faces at 0 and NX)
+};
+
 template <int R>
-__global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
-                                                 const float* __restrict__ mass,
-                                                 const int32_t* __restrict__ cell_start,
-                                                 const int32_t* __restrict__ perm, CellGrid G, int64_t n,
-                                                 const unsigned* __restrict__ hmax_bits, float* __restrict__ rho) {
+__global__ void __launch_bounds__(256) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+                                                 int64_t n, float* __restrict__ rho) {
     constexpr int W = 2 * R + 1;
-    const float hmax = __uint_as_float(*hmax_bits);
+    float hmax = 0.0f;
+    for (int g = 0; g < B.nb; ++g) hmax = fmaxf(hmax, __uint_as_float(*B.b[g].hmax));
+    const float4* __restrict__ hpos = B.b[0].pos;
+    const int hx0 = B.b[0].x0, hnx = B.b[0].nx;
+    const float hlox = B.b[0].lox;
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i_home = perm ? perm[k] : k;
         if (i_home >= G.n_home) continue;  // ghosts: neighbours only
-        const float4 pi = (pos[k]);
-        const float fx = (pi.x - G.lox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
+        const float4 pi = hpos[k];
+        // the binning formula of the own block (same origin, same rounding), then global layers
+        const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
                     fz = (pi.z - G.loz) * G.inv_cell;
-        const int ix = min(max(int(floorf(fx)), 0), G.nx - 1);
+        const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
+        const float fx = fxl + float(hx0);
         const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
         const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
         const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
@@ -244,11 +264,18 @@ __global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
 #pragma unroll 1
         for (int dxi = -R; dxi <= R; ++dxi) {
             const int jx = ix + dxi;
-            if (jx < 0 || jx >= G.nx) continue;
-            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < G.nx - 1 ? fx - float(jx + 1) : 0.0f),
+            if (jx < 0 || jx >= B.NX) continue;
+            int g = 0;
+            while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
+            if (g == B.nb) continue;  // layer held by no block
+            const float4* __restrict__ pos = B.b[g].pos;
+            const float* __restrict__ mass = B.b[g].mass;
+            const int32_t* __restrict__ cell_start = B.b[g].cs;
+            // faces of the global grid extend to infinity (binning clamps)
+            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
                                     0.0f);
             int b[W], e[W];
-            const int cx = jx * G.ny;  // cell ids fit in int32 (bin_particles checks ncell < 2^31)
+            const int cx = (jx - B.b[g].x0) * G.ny;  // cell ids fit in int32 (checked on the host)
 #pragma unroll
             for (int t = 0; t < W; ++t) {
                 const int jy = iy - R + t;
@@ -277,6 +304,15 @@ __global__ void __launch_bounds__(256) k_pairs_c(const float4* __restrict__ pos,
         }
         rho[i_home] = acc * 0.079577471545947668f;  // 1 / (4 pi)
     }
+}
+
+static void launch_pairs(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach, float* rho,
+                         cudaStream_t st) {
+    const unsigned grid = home_grid(uint64_t(n));
+    if (reach == 1) k_pairs_c<1><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
+    else if (reach == 2) k_pairs_c<2><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
+    else if (reach == 3) k_pairs_c<3><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
+    else k_pairs_c<4><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
 }
 
 static int env_int_d(const char* name, int dflt) {
@@ -310,10 +346,11 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     // SFB_PAIRS=0 selects the unculled per-run loop (round-1 kernel) for comparison
     const unsigned hgrid = home_grid(n);
     if (env_int_d("SFB_PAIRS", 1) != 0) {
-        if (reach == 1) k_pairs_c<1><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
-        else if (reach == 2) k_pairs_c<2><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
-        else if (reach == 3) k_pairs_c<3><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
-        else k_pairs_c<4><<<hgrid, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, hmax, rho);
+        BlockSet B{};
+        B.b[0] = CellBlock{pos, mass, cell_start, hmax, 0, nx, lo[0]};
+        B.nb = 1;
+        B.NX = nx;
+        launch_pairs(B, perm, G, nn, reach, rho, st);
     } else if (reach == 1) {
         k_pairs_r<1><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
     } else if (reach == 2) {
@@ -325,6 +362,50 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     count_launches(2);
     check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
     check_cuda(cudaFreeAsync(mass, st), "cudaFreeAsync");
+}
+
+// Pack for the block API: caller-owned, persistent outputs (so that other
+// ranks can read them in place through peer pointers).
+void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm, void* pos,
+                float* mass, unsigned* hmax, cudaStream_t st) {
+    require_device();
+    if (n >= (1ull << 31)) throw std::invalid_argument("cells_pack: n must be < 2^31 per device");
+    const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
+    if (sp < 0) throw std::invalid_argument("cells_pack precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
+    check_cuda(cudaMemsetAsync(hmax, 0, sizeof(unsigned), st), "memset");
+    if (n == 0) return;
+    if (reinterpret_cast<uintptr_t>(pos) & 15) throw std::invalid_argument("pos must be 16-byte aligned");
+    float4* p4 = static_cast<float4*>(pos);
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, mass, hmax);
+    else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, mass, hmax);
+    else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, mass, hmax);
+    check_cuda(cudaGetLastError(), "cells_pack launch");
+    count_launches(1);
+}
+
+void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
+                          const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* rho,
+                          cudaStream_t st) {
+    require_device();
+    if (nb < 1 || nb > 3 || NX <= 0 || ny <= 0 || nz <= 0 || n_home > n || reach < 1 || reach > 4 || !(cell > 0))
+        throw std::invalid_argument("bad cell grid");
+    if (n >= (1ull << 31)) throw std::invalid_argument("density_cells: n must be < 2^31 per device");
+    BlockSet B{};
+    B.nb = nb;
+    B.NX = NX;
+    for (int g = 0; g < nb; ++g) {
+        const CellBlockDesc& d = blocks[g];
+        if (!d.pos || !d.mass || !d.cell_start || !d.hmax) throw std::invalid_argument("null block pointer");
+        if (d.nx <= 0 || d.x0 < 0 || d.x0 + d.nx > NX || int64_t(d.nx) * ny * nz >= (1ll << 31))
+            throw std::invalid_argument("block layers outside the grid");
+        B.b[g] = CellBlock{static_cast<const float4*>(d.pos), d.mass, d.cell_start, d.hmax, d.x0, d.nx, d.x_origin};
+    }
+    if (n == 0) return;
+    CellGrid G{blocks[0].x_origin, lo_yz[0], lo_yz[1], 1.0f / cell, NX, ny, nz, reach, int64_t(n_home)};
+    launch_pairs(B, perm, G, int64_t(n), reach, rho, st);
+    check_cuda(cudaGetLastError(), "density_cells_blocks launch");
+    count_launches(1);
 }
 
 // ------------------------------------------------------------------ force
