@@ -246,14 +246,129 @@ def gpu_force_backend(prec: int, refine: int = 2, binning: Optional[dict] = None
     return run
 
 
+def _align(v: int, a: int = 256) -> int:
+    return (v + a - 1) // a * a
+
+
+class PeerBlocks:
+    """Density across ranks with no ghost copy (the fused halo).
+
+    Every rank bins and packs its own particles into ONE persistent device
+    allocation [cell_start | pos (float4) | mass | hmax] and exposes it to
+    its +-1 neighbours by CUDA IPC handle (exchanged over the process group
+    when a buffer is (re)allocated).  The density kernel then reads the
+    neighbours' boundary columns in place through the mapped peer pointers —
+    NVLink loads issued by the pair loop itself, overlapping its arithmetic —
+    so the step has no send/recv and no staging copy.  Two barriers order the
+    ranks: after every rank has packed (its block is complete before a
+    neighbour reads it) and before a rank overwrites its block (every
+    neighbour has finished reading the previous one).  The same code serves
+    ranks on one device (CUDA IPC between processes of one GPU, the tests)."""
+
+    def __init__(self, slab: Slab, refine: int = 2, prec: Optional[int] = None, group=None):
+        from . import api
+        self.api, self.slab, self.refine, self.group = api, slab, refine, group
+        self.prec = api.SF_PREC_NATIVE if prec is None else prec
+        self.NX = self.ny = self.nz = slab.nc * refine
+        self.cell = slab.cell / refine
+        self.x0, self.nx = slab.x0 * refine, (slab.x1 - slab.x0) * refine
+        self.x_origin = self.x0 * self.cell
+        self.ncell = self.nx * self.ny * self.nz
+        self.cap, self.buf, self.peers, self.perm = 0, None, {}, None
+
+    @staticmethod
+    def layout(ncell: int, cap: int):
+        pos = _align(4 * (ncell + 1))
+        mass = pos + 16 * cap
+        hmax = _align(mass + 4 * cap)
+        return pos, mass, hmax, hmax + 256
+
+    def _barrier(self):
+        if self.slab.world > 1:
+            import torch.distributed as dist
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def _ensure(self, n: int):
+        import torch.distributed as dist
+        grow = n > self.cap
+        if grow:
+            if self.buf is not None:
+                self.buf.free()
+            self.cap = max(int(n * 1.2) + 1024, 1024)
+            self.buf = self.api.DeviceBuffer(self.layout(self.ncell, self.cap)[3])
+        if self.slab.world == 1:
+            return
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        flag = torch.tensor([int(grow)], device=dev)
+        dist.all_reduce(flag, group=self.group)
+        if int(flag.item()) == 0:
+            return
+        info = (self.buf.ipc_handle(), self.cap, self.x0, self.nx, self.ncell, self.x_origin)
+        every = [None] * self.slab.world
+        dist.all_gather_object(every, info, group=self.group)
+        for r, old in list(self.peers.items()):
+            old[0].free()
+        self.peers = {}
+        for r in (self.slab.rank - 1, self.slab.rank + 1):
+            if 0 <= r < self.slab.world:
+                hd, cap, x0, nx, ncell, xo = every[r]
+                self.peers[r] = (self.api.DeviceBuffer(handle=hd), cap, x0, nx, ncell, xo)
+
+    def _peer_block(self, r):
+        mapped, cap, x0, nx, ncell, xo = self.peers[r]
+        pos, mass, hmax, _ = self.layout(ncell, cap)
+        base = mapped.ptr
+        return self.api.cell_block(base + pos, base + mass, base, base + hmax, x0, nx, xo)
+
+    def __call__(self, x, m, h) -> torch.Tensor:
+        """rho of this rank's particles (x, m, h in particle order)."""
+        api = self.api
+        n = m.shape[0]
+        self._barrier()  # the neighbours are done reading the previous block
+        self._ensure(n)
+        posb, massb, hmaxb, _ = self.layout(self.ncell, self.cap)
+        cs = self.buf.tensor(0, (self.ncell + 1,), torch.int32)
+        pos = self.buf.tensor(posb, (self.cap, 4), torch.float32)[:n]
+        mass = self.buf.tensor(massb, (self.cap,), torch.float32)[:n]
+        hmax = self.buf.tensor(hmaxb, (4,), torch.int32)
+        if self.perm is None or self.perm.shape[0] < n:
+            self.perm = torch.empty(max(self.cap, 1), dtype=torch.int32, device="cuda")
+        _mark("bin")
+        api.bin_particles(x.float().contiguous(), (self.x_origin, 0.0, 0.0), self.cell, (self.nx, self.ny, self.nz),
+                          cell_start=cs, perm=self.perm[:max(n, 1)])
+        api.cells_pack(x.contiguous(), m.contiguous(), h.contiguous(), self.perm, pos, mass, hmax, self.prec)
+        self._barrier()  # every block of this step is complete
+        _mark("pairs")
+        blocks = [api.cell_block(pos, mass, cs, hmax, self.x0, self.nx, self.x_origin)]
+        blocks += [self._peer_block(r) for r in sorted(self.peers)]
+        rho = api.density_cells_blocks(blocks, n, self.perm, (0.0, 0.0), self.cell, self.NX, self.ny, self.nz,
+                                       reach=self.refine)
+        self.last = {"cs": cs, "perm": self.perm[:max(n, 1)], "n": n}  # valid until the next call
+        _mark("store")
+        return rho[:n]
+
+    def close(self):
+        for old in self.peers.values():
+            old[0].free()
+        self.peers = {}
+        if self.buf is not None:
+            self.buf.free()
+            self.buf = None
+
+
 class ShardedState:
     """One rank's particles: SoA buffer of the reference's default schema at
     uniform storage precision `prec` (32 or 16; positions included)."""
 
     def __init__(self, n_global: int, slab: Slab, prec: int = 32, seed: int = 7, device="cuda",
-                 h: Optional[float] = None):
+                 h: Optional[float] = None, halo: str = "peer", group=None):
         from . import api
         self.api, self.slab, self.prec, self.device = api, slab, prec, device
+        if halo not in ("peer", "nccl"):
+            raise ValueError("halo must be 'peer' (neighbour blocks read in place) or 'nccl' (ghost rows sent)")
+        self.halo = halo
+        self._peer = PeerBlocks(slab, 2, {32: api.SF_PREC_NATIVE, 16: 16}[prec], group) if halo == "peer" else None
         self.schema = api.Schema.default()
         self.h = h if h is not None else grid_for(n_global)[0]
         n = n_global // slab.world
@@ -329,6 +444,15 @@ class ShardedState:
 
     def density(self, group=None):
         x, m, h = self.stream("x"), self.stream("m"), self.stream("h")
+        if self._peer is not None:  # fused halo: the neighbours' blocks are read in place
+            _mark("halo")
+            self._peer.group = group
+            rho = self._peer(x, m, h)
+            # at world 1 the own-block grid is the force's local grid: its binning is reusable
+            self._binning = self._peer.last if self.slab.world == 1 else None
+            self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
+            _mark("end")
+            return
         _mark("halo")
         gx, gm, gh = exchange_halo(x, m, h, self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]

@@ -156,3 +156,63 @@ def test_density_blocks_read_neighbours_in_place(world, refine):
         np.testing.assert_allclose(rho[: S[r]["n"]].double().cpu().numpy(), want[S[r]["own"]], rtol=1e-5)
         seen |= S[r]["own"]
     assert seen.all()
+
+
+def _peer_worker(rank, world, port, outdir, n):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    import torch.distributed as dist
+    from paper_2512_05516_b200.sharded import PeerBlocks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # every rank on the one device: CUDA IPC between processes of one GPU
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(31)
+    x = rng.random((n, 3))
+    h, nc, cell = grid_for(n)
+    m = rng.uniform(0.5, 1.5, n) / n
+    layer = np.minimum(np.floor(x[:, 0] / cell).astype(int), nc - 1)
+    slab = Slab(nc, cell, rank, world)
+    own = (layer >= slab.x0) & (layer < slab.x1)
+    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+    pb = PeerBlocks(slab, 2)
+    rho = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))
+    rho2 = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))  # second step: buffers reused, no new handles
+    np.savez(os.path.join(outdir, f"p{rank}.npz"), own=own, rho=rho.cpu().numpy(), rho2=rho2.cpu().numpy(),
+             npeers=len(pb.peers))
+    torch.cuda.synchronize()
+    dist.barrier()
+    pb.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_blocks_across_processes_cuda_ipc(tmp_path, world):
+    """PeerBlocks in `world` processes sharing one GPU: every rank maps its
+    neighbours' blocks by CUDA IPC handle (the multi-GPU mechanism) and the
+    per-rank densities equal the global oracle's."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    n = 1 << 15
+    mp.spawn(_peer_worker, args=(world, port, str(tmp_path), n), nprocs=world, join=True)
+    rng = np.random.default_rng(31)
+    x = rng.random((n, 3))
+    h, nc, cell = grid_for(n)
+    m = rng.uniform(0.5, 1.5, n) / n
+    dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
+    want = O.density_cells(dec(x).reshape(-1), dec(m), dec(np.full(n, h)), 0.0, 1.0, cell)
+    seen = np.zeros(n, bool)
+    for r in range(world):
+        d = np.load(tmp_path / f"p{r}.npz")
+        np.testing.assert_allclose(d["rho"], want[d["own"]], rtol=1e-5)
+        assert np.array_equal(d["rho"], d["rho2"])
+        assert int(d["npeers"]) == (1 if r in (0, world - 1) else 2)
+        seen |= d["own"]
+    assert seen.all()
