@@ -166,6 +166,26 @@ SF_API sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int n
                                               const int32_t* perm, uint64_t n_home, const float* lo_yz,
                                               float cell, int nx_global, int ny, int nz, int reach,
                                               float* rho_out, void* stream);
+/* The force over the same blocks: a density block plus the same particles'
+ * (v, m) as float4 and P/rho^2, packed in its cell-sorted order by
+ * sf_b200_force_pack (rho == 0 -> SF_ERROR domain error; synchronizes). */
+typedef struct sf_force_block {
+    const void* pos;            /* the density block's float4 (x, y, z, h) */
+    const void* vel;            /* float4 (vx, vy, vz, m) */
+    const float* pf;            /* P / rho^2 */
+    const int32_t* cell_start;
+    const uint32_t* hmax;
+    int32_t x0, nx;
+    float x_origin;
+    int32_t reserved;
+} sf_force_block;
+SF_API sf_status sf_b200_force_pack(const void* v, const void* m, const void* rho, const void* P, int prec,
+                                    uint64_t n, const int32_t* perm, void* vel_out, float* pf_out,
+                                    void* stream);
+SF_API sf_status sf_b200_force_cells_blocks(const sf_force_block* blocks, int nblocks, uint64_t n,
+                                            const int32_t* perm, uint64_t n_home, const float* lo_yz,
+                                            float cell, int nx_global, int ny, int nz, int reach,
+                                            float* a_out, float* du_out, void* stream);
 /* Device memory that another process can map (cudaMalloc base), and CUDA IPC
  * handles for it (same node; NVLink/NVSwitch peers or the same device). */
 SF_API sf_status sf_b200_dev_alloc(uint64_t bytes, void** ptr);

@@ -318,6 +318,36 @@ def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: in
     return rho
 
 
+def force_pack(v, m, rho, P, perm, vel, pf, prec: int = SF_PREC_NATIVE):
+    """(v, m) -> float4 vel (n,4) and P/rho^2 -> pf (n,) in perm's order;
+    rho == 0 raises SfError (domain error)."""
+    n = m.shape[0]
+    check(lib().sf_b200_force_pack(_ptr(v), _ptr(m), _ptr(rho), _ptr(P), prec, n,
+                                   _ptr(perm) if perm is not None else None, _ptr(vel), _ptr(pf), _stream()))
+
+
+def force_block(pos, vel, pf, cell_start, hmax, x0: int, nx: int, x_origin: float) -> "L.SfForceBlock":
+    addr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
+    return L.SfForceBlock(addr(pos), addr(vel), addr(pf), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
+
+
+def force_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,
+                       reach: int = 1, a=None, du=None):
+    """Cell-linked force of blocks[0]'s first n_home particles with
+    candidates from every block; returns (a (n,3), du (n,))."""
+    import torch
+    n_home = n if n_home is None else n_home
+    a = a if a is not None else torch.zeros((max(n, 1), 3), dtype=torch.float32, device="cuda")
+    du = du if du is not None else torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+    arr = (L.SfForceBlock * len(blocks))(*blocks)
+    lo_arr = (C.c_float * 2)(*[float(t) for t in lo_yz])
+    check(lib().sf_b200_force_cells_blocks(C.cast(arr, C.c_void_p), len(blocks), n,
+                                           _ptr(perm) if perm is not None else None, n_home,
+                                           C.cast(lo_arr, C.c_void_p), float(cell), nx_global, ny, nz, reach,
+                                           _ptr(a), _ptr(du), _stream()))
+    return a, du
+
+
 class DeviceBuffer:
     """cudaMalloc'd device memory (an IPC-shareable allocation base), or a
     mapping of another process's buffer opened from its IPC handle."""

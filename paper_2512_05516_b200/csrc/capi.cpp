@@ -305,6 +305,33 @@ sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int nblocks,
     });
 }
 
+static_assert(sizeof(sf_force_block) == sizeof(ForceBlockDesc), "sf_force_block layout");
+
+sf_status sf_b200_force_pack(const void* v, const void* m, const void* rho, const void* P, int prec, uint64_t n,
+                             const int32_t* perm, void* vel_out, float* pf_out, void* stream) {
+    if (n && (!v || !m || !rho || !P || !vel_out || !pf_out)) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        force_pack(v, m, rho, P, prec, n, perm, vel_out, pf_out, static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_force_cells_blocks(const sf_force_block* blocks, int nblocks, uint64_t n, const int32_t* perm,
+                                     uint64_t n_home, const float* lo_yz, float cell, int nx_global, int ny, int nz,
+                                     int reach, float* a_out, float* du_out, void* stream) {
+    if (!blocks || !lo_yz || (n && (!a_out || !du_out))) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        std::vector<ForceBlockDesc> d(size_t(std::max(nblocks, 0)));
+        for (int g = 0; g < nblocks; ++g)
+            d[g] = ForceBlockDesc{blocks[g].pos,  blocks[g].vel, blocks[g].pf,       blocks[g].cell_start,
+                                  blocks[g].hmax, blocks[g].x0,  blocks[g].nx,       blocks[g].x_origin,
+                                  0};
+        force_cells_blocks(d.data(), nblocks, n, perm, n_home, lo_yz, cell, nx_global, ny, nz, reach, a_out, du_out,
+                           static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
 sf_status sf_b200_dev_alloc(uint64_t bytes, void** out) {
     if (!out) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {

@@ -451,58 +451,82 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     return r;
 }
 
+// Candidate blocks of the force: a density block's (x,y,z,h) plus the same
+// particles' (v, m) and P/rho^2, all in the block's cell-sorted order.
+struct ForceBlock {
+    const float4* pos;
+    const float4* vel;
+    const float* pf;
+    const int32_t* cs;
+    const unsigned* hmax;
+    int x0, nx;
+    float lox;
+};
+struct ForceBlockSet {
+    ForceBlock b[3];
+    int nb, NX;
+};
+
 template <int R, int U>
-__global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos, const float4* __restrict__ vel,
-                                                 const float* __restrict__ pf, const int32_t* __restrict__ cell_start,
-                                                 const int32_t* __restrict__ perm, CellGrid G, int64_t n,
-                                                 const unsigned* __restrict__ hmax_bits, float* __restrict__ a_out,
-                                                 float* __restrict__ du_out) {
+__global__ void __launch_bounds__(256) k_force_c(const ForceBlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+                                                 int64_t n, float* __restrict__ a_out, float* __restrict__ du_out) {
     constexpr int W = 2 * R + 1;
-    const float hmax = __uint_as_float(*hmax_bits);
+    float hmax = 0.0f;
+    for (int g = 0; g < B.nb; ++g) hmax = fmaxf(hmax, __uint_as_float(*B.b[g].hmax));
+    const int hx0 = B.b[0].x0, hnx = B.b[0].nx;
+    const float hlox = B.b[0].lox;
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i_home = perm ? perm[k] : k;
         if (i_home >= G.n_home) continue;  // ghosts: neighbours only
-        const float4 pi = pos[k];
-        const float fx = (pi.x - G.lox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
+        const float4 pi = B.b[0].pos[k];
+        const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
                     fz = (pi.z - G.loz) * G.inv_cell;
-        const int ix = min(max(int(floorf(fx)), 0), G.nx - 1);
+        const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
+        const float fx = fxl + float(hx0);
         const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
         const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
-        const float4 vi = vel[k];
-        const float pfi = pf[k];
+        const float4 vi = B.b[0].vel[k];
+        const float pfi = B.b[0].pf[k];
         const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;
         const float rc2 = rc * rc;
         const float hh_i = 0.5f * pi.w;
         const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
         const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
         float ax = 0.0f, ay = 0.0f, az = 0.0f, cp = 0.0f;
-        auto pair = [&](int j) {
-            const float4 pj = pos[j];
-            const float4 vj = vel[j];
-            const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
-            const float inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
-            const float q = (r2 * inv_r) * inv_h;
-            const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
-            const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
-            const float ih2 = inv_h * inv_h;
-            const float sc = dw * (ih2 * ih2) * inv_r;           // pi dW/dr / r
-            const float f = vj.w * (pfi + __ldg(pf + j)) * sc;
-            ax = fmaf(f, dx, ax);
-            ay = fmaf(f, dy, ay);
-            az = fmaf(f, dz, az);
-            const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
-            cp = fmaf(vj.w * sc, dvx, cp);
-        };
 #pragma unroll 1
         for (int dxi = -R; dxi <= R; ++dxi) {
             const int jx = ix + dxi;
-            if (jx < 0 || jx >= G.nx) continue;
-            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < G.nx - 1 ? fx - float(jx + 1) : 0.0f),
+            if (jx < 0 || jx >= B.NX) continue;
+            int g = 0;
+            while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
+            if (g == B.nb) continue;  // layer held by no block
+            const float4* __restrict__ pos = B.b[g].pos;
+            const float4* __restrict__ vel = B.b[g].vel;
+            const float* __restrict__ pf = B.b[g].pf;
+            const int32_t* __restrict__ cell_start = B.b[g].cs;
+            auto pair = [&](int j) {
+                const float4 pj = pos[j];
+                const float4 vj = vel[j];
+                const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
+                const float inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
+                const float q = (r2 * inv_r) * inv_h;
+                const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
+                const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
+                const float ih2 = inv_h * inv_h;
+                const float sc = dw * (ih2 * ih2) * inv_r;           // pi dW/dr / r
+                const float f = vj.w * (pfi + __ldg(pf + j)) * sc;
+                ax = fmaf(f, dx, ax);
+                ay = fmaf(f, dy, ay);
+                az = fmaf(f, dz, az);
+                const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
+                cp = fmaf(vj.w * sc, dvx, cp);
+            };
+            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
                                     0.0f);
             int b[W], e[W];
-            const int cx = jx * G.ny;
+            const int cx = (jx - B.b[g].x0) * G.ny;
 #pragma unroll
             for (int t = 0; t < W; ++t) {
                 const int jy = iy - R + t;
@@ -537,6 +561,36 @@ __global__ void __launch_bounds__(256) k_force_c(const float4* __restrict__ pos,
     }
 }
 
+static void launch_force(const ForceBlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
+                         float* a, float* du, cudaStream_t st) {
+    const unsigned grid = home_grid(uint64_t(n));
+    auto go = [&](auto u) {
+        constexpr int U = decltype(u)::value;
+        if (reach == 1) k_force_c<1, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+        else if (reach == 2) k_force_c<2, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+        else if (reach == 3) k_force_c<3, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+        else k_force_c<4, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+    };
+    if (env_int_d("SFB_FORCE_UNROLL", 2) == 2) go(std::integral_constant<int, 2>{});
+    else go(std::integral_constant<int, 1>{});
+}
+
+// (v, m) and P/rho^2 of a packed block, in its cell-sorted order; rho == 0 sets *zero
+template <int P>
+__global__ void k_pack_vel(const void* __restrict__ v, const void* __restrict__ m, const void* __restrict__ rho,
+                           const void* __restrict__ pr, const int32_t* __restrict__ perm, uint64_t n,
+                           float4* __restrict__ vel, float* __restrict__ pf, unsigned* __restrict__ zero) {
+    bool z = false;
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = perm ? uint64_t(perm[k]) : k;
+        const float ri = ldf<P>(rho, i);
+        vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(m, i));
+        pf[k] = ldf<P>(pr, i) / (ri * ri);
+        z |= ri == 0.0f;
+    }
+    if (__any_sync(0xffffffffu, z) && (threadIdx.x & 31) == 0) atomicOr(zero, 1u);
+}
+
 void force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho, const void* pr,
                  int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
                  int nx, int ny, int nz, int reach, uint64_t n_home, float* a, float* du, cudaStream_t st) {
@@ -568,21 +622,64 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
         throw std::domain_error("force: degenerate state, rho == 0");
     }
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
-    const int64_t nn = int64_t(n);
-    const unsigned hgrid = home_grid(n);
-    auto go = [&](auto u) {
-        constexpr int U = decltype(u)::value;
-        if (reach == 1) k_force_c<1, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-        else if (reach == 2) k_force_c<2, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-        else if (reach == 3) k_force_c<3, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-        else k_force_c<4, U><<<hgrid, 256, 0, st>>>(pos, vel, pf, cell_start, perm, G, nn, words, a, du);
-    };
-    if (env_int_d("SFB_FORCE_UNROLL", 2) == 2) go(std::integral_constant<int, 2>{});
-    else go(std::integral_constant<int, 1>{});
+    ForceBlockSet B{};
+    B.b[0] = ForceBlock{pos, vel, pf, cell_start, words, 0, nx, lo[0]};
+    B.nb = 1;
+    B.NX = nx;
+    launch_force(B, perm, G, int64_t(n), reach, a, du, st);
     check_cuda(cudaGetLastError(), "force_cells launch");
     count_launches(2);
     check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
     check_cuda(cudaFreeAsync(pf, st), "cudaFreeAsync");
+}
+
+void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
+                const int32_t* perm, void* vel, float* pf, cudaStream_t st) {
+    require_device();
+    if (n >= (1ull << 31)) throw std::invalid_argument("force_pack: n must be < 2^31 per device");
+    const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
+    if (sp < 0) throw std::invalid_argument("force_pack precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
+    if (n == 0) return;
+    if (reinterpret_cast<uintptr_t>(vel) & 15) throw std::invalid_argument("vel must be 16-byte aligned");
+    unsigned* zero = nullptr;
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&zero), sizeof(unsigned), st), "cudaMallocAsync");
+    check_cuda(cudaMemsetAsync(zero, 0, sizeof(unsigned), st), "memset");
+    float4* v4 = static_cast<float4*>(vel);
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+    if (sp == SP_F32) k_pack_vel<SP_F32><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
+    else if (sp == SP_F16) k_pack_vel<SP_F16><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
+    else k_pack_vel<SP_BF16><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
+    count_launches(1);
+    unsigned flag = 0;
+    check_cuda(cudaMemcpyAsync(&flag, zero, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaFreeAsync(zero, st), "cudaFreeAsync");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    if (flag) throw std::domain_error("force: degenerate state, rho == 0");
+}
+
+void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
+                        const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* a, float* du,
+                        cudaStream_t st) {
+    require_device();
+    if (nb < 1 || nb > 3 || NX <= 0 || ny <= 0 || nz <= 0 || n_home > n || reach < 1 || reach > 4 || !(cell > 0))
+        throw std::invalid_argument("bad cell grid");
+    if (n >= (1ull << 31)) throw std::invalid_argument("force_cells: n must be < 2^31 per device");
+    ForceBlockSet B{};
+    B.nb = nb;
+    B.NX = NX;
+    for (int g = 0; g < nb; ++g) {
+        const ForceBlockDesc& d = blocks[g];
+        if (!d.pos || !d.vel || !d.pf || !d.cell_start || !d.hmax) throw std::invalid_argument("null block pointer");
+        if (d.nx <= 0 || d.x0 < 0 || d.x0 + d.nx > NX || int64_t(d.nx) * ny * nz >= (1ll << 31))
+            throw std::invalid_argument("block layers outside the grid");
+        B.b[g] = ForceBlock{static_cast<const float4*>(d.pos), static_cast<const float4*>(d.vel), d.pf, d.cell_start,
+                            d.hmax, d.x0, d.nx, d.x_origin};
+    }
+    if (n == 0) return;
+    CellGrid G{blocks[0].x_origin, lo_yz[0], lo_yz[1], 1.0f / cell, NX, ny, nz, reach, int64_t(n_home)};
+    launch_force(B, perm, G, int64_t(n), reach, a, du, st);
+    check_cuda(cudaGetLastError(), "force_cells_blocks launch");
+    count_launches(1);
 }
 
 // ------------------------------------------------------------------ binning

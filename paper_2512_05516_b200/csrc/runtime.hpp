@@ -58,6 +58,21 @@ void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t 
 void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                           const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* rho,
                           cudaStream_t st);
+struct ForceBlockDesc {
+    const void* pos;
+    const void* vel;
+    const float* pf;
+    const int32_t* cell_start;
+    const unsigned* hmax;
+    int32_t x0, nx;
+    float x_origin;
+    int32_t reserved;
+};
+void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
+                const int32_t* perm, void* vel, float* pf, cudaStream_t st);
+void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
+                        const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* a, float* du,
+                        cudaStream_t st);
 void force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho, const void* pr,
                  int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
                  int nx, int ny, int nz, int reach, uint64_t n_home, float* a, float* du, cudaStream_t st);

@@ -14,8 +14,11 @@ Rank r owns layers [x0, x1).  One step:
                           grid (own layers + one ghost layer each side), then
                           the cell-linked density over the own layers only
 
-`full_step` runs the reference's timestep order instead: density, a second
-halo of (x, v, m, h, rho, P), the cell-linked force, kick, drift, migrate.
+`full_step` runs the reference's timestep order instead: density, the
+cell-linked force (its halo: the neighbours' (x, h, v, m, P/rho^2)), kick,
+drift, migrate.  With halo="peer" (default) neither halo is copied: each
+rank's packed cell block is read in place by its neighbours through CUDA IPC
+peer pointers (PeerBlocks); halo="nccl" sends ghost rows instead.
 
 NVSwitch makes every peer equidistant, so slab r simply maps to rank r.  The
 exchange uses only neighbour point-to-point traffic; there is no collective
@@ -274,14 +277,17 @@ class PeerBlocks:
         self.x0, self.nx = slab.x0 * refine, (slab.x1 - slab.x0) * refine
         self.x_origin = self.x0 * self.cell
         self.ncell = self.nx * self.ny * self.nz
-        self.cap, self.buf, self.peers, self.perm = 0, None, {}, None
+        self.cap, self.buf, self.peers, self.perm, self.last = 0, None, {}, None, None
 
     @staticmethod
     def layout(ncell: int, cap: int):
+        """Byte offsets of pos, mass, hmax, vel, pf and the total size."""
         pos = _align(4 * (ncell + 1))
         mass = pos + 16 * cap
         hmax = _align(mass + 4 * cap)
-        return pos, mass, hmax, hmax + 256
+        vel = hmax + 256
+        pf = vel + 16 * cap
+        return pos, mass, hmax, vel, pf, _align(pf + 4 * cap)
 
     def _barrier(self):
         if self.slab.world > 1:
@@ -296,7 +302,7 @@ class PeerBlocks:
             if self.buf is not None:
                 self.buf.free()
             self.cap = max(int(n * 1.2) + 1024, 1024)
-            self.buf = self.api.DeviceBuffer(self.layout(self.ncell, self.cap)[3])
+            self.buf = self.api.DeviceBuffer(self.layout(self.ncell, self.cap)[-1])
         if self.slab.world == 1:
             return
         dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
@@ -315,10 +321,12 @@ class PeerBlocks:
                 hd, cap, x0, nx, ncell, xo = every[r]
                 self.peers[r] = (self.api.DeviceBuffer(handle=hd), cap, x0, nx, ncell, xo)
 
-    def _peer_block(self, r):
+    def _peer_block(self, r, force=False):
         mapped, cap, x0, nx, ncell, xo = self.peers[r]
-        pos, mass, hmax, _ = self.layout(ncell, cap)
+        pos, mass, hmax, vel, pf, _ = self.layout(ncell, cap)
         base = mapped.ptr
+        if force:
+            return self.api.force_block(base + pos, base + vel, base + pf, base, base + hmax, x0, nx, xo)
         return self.api.cell_block(base + pos, base + mass, base, base + hmax, x0, nx, xo)
 
     def __call__(self, x, m, h) -> torch.Tensor:
@@ -327,7 +335,7 @@ class PeerBlocks:
         n = m.shape[0]
         self._barrier()  # the neighbours are done reading the previous block
         self._ensure(n)
-        posb, massb, hmaxb, _ = self.layout(self.ncell, self.cap)
+        posb, massb, hmaxb, _, _, _ = self.layout(self.ncell, self.cap)
         cs = self.buf.tensor(0, (self.ncell + 1,), torch.int32)
         pos = self.buf.tensor(posb, (self.cap, 4), torch.float32)[:n]
         mass = self.buf.tensor(massb, (self.cap,), torch.float32)[:n]
@@ -347,6 +355,30 @@ class PeerBlocks:
         self.last = {"cs": cs, "perm": self.perm[:max(n, 1)], "n": n}  # valid until the next call
         _mark("store")
         return rho[:n]
+
+    def force(self, v, m, rho, P):
+        """(a, du) of this rank's particles, after __call__ in the same step
+        (same positions: the block's cell list and pos are reused); the
+        neighbours' (pos, vel, P/rho^2) are read in place."""
+        api = self.api
+        n = m.shape[0]
+        if self.last is None or self.last["n"] != n:
+            raise RuntimeError("PeerBlocks.force needs the density of the same particles first")
+        self._barrier()  # the neighbours are done reading the previous vel / pf
+        posb, _, hmaxb, velb, pfb, _ = self.layout(self.ncell, self.cap)
+        cs = self.buf.tensor(0, (self.ncell + 1,), torch.int32)
+        pos = self.buf.tensor(posb, (self.cap, 4), torch.float32)
+        hmax = self.buf.tensor(hmaxb, (4,), torch.int32)
+        vel = self.buf.tensor(velb, (self.cap, 4), torch.float32)[:max(n, 1)]
+        pf = self.buf.tensor(pfb, (self.cap,), torch.float32)[:max(n, 1)]
+        api.force_pack(v.contiguous(), m.contiguous(), rho.contiguous(), P.contiguous(), self.perm, vel, pf,
+                       self.prec)
+        self._barrier()  # every (vel, pf) of this step is complete
+        blocks = [api.force_block(pos, vel, pf, cs, hmax, self.x0, self.nx, self.x_origin)]
+        blocks += [self._peer_block(r, force=True) for r in sorted(self.peers)]
+        a, du = api.force_cells_blocks(blocks, n, self.perm, (0.0, 0.0), self.cell, self.NX, self.ny, self.nz,
+                                       reach=self.refine)
+        return a[:n], du[:n]
 
     def close(self):
         for old in self.peers.values():
@@ -466,6 +498,13 @@ class ShardedState:
         ghosts (second halo, after every rank has its rho)."""
         names = ["x", "v", "m", "h", "rho", "P"]
         own = [self.stream(k) for k in names]
+        if self._peer is not None:  # fused halo: the neighbours' (pos, vel, P/rho^2) read in place
+            _mark("halo2")
+            a, du = self._peer.force(own[1], own[2], own[4], own[5])
+            self.stream("a").copy_(a.to(self.stream("a").dtype))
+            self.stream("du").copy_(du.to(self.stream("du").dtype))
+            _mark("end2")
+            return
         _mark("halo2")
         ghosts = exchange_ghost_fields(own, own[0][:, 0], self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]

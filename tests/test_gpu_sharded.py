@@ -12,10 +12,11 @@ from paper_2512_05516_b200.sharded import ShardedState, Slab, density_with_ghost
 pytestmark = pytest.mark.gpu
 
 
-def test_single_rank_step_matches_oracle():
+@pytest.mark.parametrize("halo", ["peer", "nccl"])
+def test_single_rank_step_matches_oracle(halo):
     n = 1 << 15
     h, nc, cell = grid_for(n)
-    st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h)
+    st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h, halo=halo)
     st.sort_by_cell()
     before = {k: st.stream(k).double().cpu().numpy().copy() for k in ["x", "v", "u", "a", "du", "m", "h"]}
     st.step(1e-3)
@@ -87,12 +88,13 @@ def test_rank_force_with_ghost_layers(world):
     assert seen.all()
 
 
-def test_single_rank_full_step_runs_reference_order():
+@pytest.mark.parametrize("halo", ["peer", "nccl"])
+def test_single_rank_full_step_runs_reference_order(halo):
     """density -> force -> kick -> drift on one rank: a/du come from the force
     on the fresh rho, then kick/drift use them (checked against the oracle)."""
     n = 1 << 15
     h, nc, cell = grid_for(n)
-    st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h)
+    st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h, halo=halo)
     st.sort_by_cell()
     st.stream("P").copy_(torch.rand(st.n, device="cuda") + 0.2)
     before = {k: st.stream(k).double().cpu().numpy().copy() for k in ["x", "v", "u", "m", "h", "P"]}
@@ -157,6 +159,32 @@ def test_density_blocks_read_neighbours_in_place(world, refine):
         seen |= S[r]["own"]
     assert seen.all()
 
+    # the force over the same blocks: every slab packs (v, m), P/rho^2 in its cell order
+    v = rng.uniform(-1, 1, (n, 3))
+    rho = rng.uniform(0.5, 1.5, n)
+    P = rng.uniform(0.2, 1.2, n)
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(hh), dec(rho), dec(P),
+                                    0.0, 1.0, cell)
+    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+    fb = []
+    for r in range(world):
+        own, k = S[r]["own"], S[r]["n"]
+        vel = torch.empty(k, 4, device="cuda")
+        pf = torch.empty(k, device="cuda")
+        api.force_pack(t(v[own]), t(m[own]), t(rho[own]), t(P[own]), S[r]["perm"], vel, pf)
+        xt, mt, ht, cs, pos, mass, hmax = S[r]["keep"]
+        fine = cell / refine
+        S[r]["fkeep"] = (vel, pf)
+        fb.append(api.force_block(pos, vel, pf, cs, hmax, S[r]["block"].x0, S[r]["block"].nx, S[r]["block"].x_origin))
+    for r in range(world):
+        blocks = [fb[r]] + [fb[q] for q in (r - 1, r + 1) if 0 <= q < world]
+        a, du = api.force_cells_blocks(blocks, S[r]["n"], S[r]["perm"], (0.0, 0.0), cell / refine, nc * refine,
+                                       nc * refine, nc * refine, reach=refine)
+        own = S[r]["own"]
+        err = np.linalg.norm(a[: S[r]["n"]].double().cpu().numpy() - wa[own], axis=1)
+        assert np.all(err <= 2e-5 * sa[own])
+        assert np.all(np.abs(du[: S[r]["n"]].double().cpu().numpy() - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
+
 
 def _peer_worker(rank, world, port, outdir, n):
     import os
@@ -181,8 +209,10 @@ def _peer_worker(rank, world, port, outdir, n):
     pb = PeerBlocks(slab, 2)
     rho = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))
     rho2 = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))  # second step: buffers reused, no new handles
+    v = np.random.default_rng(32).uniform(-1, 1, (n, 3))
+    a, du = pb.force(t(v[own]), t(m[own]), rho2, rho2 * 0.7)
     np.savez(os.path.join(outdir, f"p{rank}.npz"), own=own, rho=rho.cpu().numpy(), rho2=rho2.cpu().numpy(),
-             npeers=len(pb.peers))
+             npeers=len(pb.peers), a=a.cpu().numpy(), du=du.cpu().numpy())
     torch.cuda.synchronize()
     dist.barrier()
     pb.close()
@@ -209,10 +239,22 @@ def test_peer_blocks_across_processes_cuda_ipc(tmp_path, world):
     dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
     want = O.density_cells(dec(x).reshape(-1), dec(m), dec(np.full(n, h)), 0.0, 1.0, cell)
     seen = np.zeros(n, bool)
+    rho_all = np.zeros(n)
     for r in range(world):
         d = np.load(tmp_path / f"p{r}.npz")
         np.testing.assert_allclose(d["rho"], want[d["own"]], rtol=1e-5)
         assert np.array_equal(d["rho"], d["rho2"])
         assert int(d["npeers"]) == (1 if r in (0, world - 1) else 2)
         seen |= d["own"]
+        rho_all[d["own"]] = d["rho"]
     assert seen.all()
+    # the force read the neighbours' (pos, vel, P/rho^2) blocks in place
+    v = np.random.default_rng(32).uniform(-1, 1, (n, 3))
+    P = (torch.tensor(rho_all, dtype=torch.float32) * 0.7).double().numpy()
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(np.full(n, h)), rho_all, P,
+                                    0.0, 1.0, cell)
+    for r in range(world):
+        d = np.load(tmp_path / f"p{r}.npz")
+        own = d["own"]
+        assert np.all(np.linalg.norm(d["a"] - wa[own], axis=1) <= 2e-5 * sa[own])
+        assert np.all(np.abs(d["du"] - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
