@@ -285,6 +285,30 @@ def b200_arm(args):
                             "(DRAM fetch granularity >= 64 B, profiles/r01_sector_probe.md), so frac <= 0.48 "
                             "by format; dram_frac is the measured-bytes fraction of the copy peak")
 
+    # SURVEY §8d C2 scatter-back row: the drifted SoA x' (binary16) widened exactly into the f64 x lanes of the
+    # AoS records, every other byte untouched (widen_merge of the drift write set; 30 B/particle algorithmic)
+    scatter = None
+    if world == 1:
+        tgt = api.PackedBuffer.empty(aos_v)  # a copy: the source AoS stays as generated for the e2e check
+        tgt.data.copy_(src.data)
+        for _ in range(3):
+            api.widen_merge(out, tgt, "drift")
+        torch.cuda.synchronize()
+        sa, sb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(args.steps // 2, 10)
+        sa.record(stream)
+        for _ in range(reps):
+            api.widen_merge(out, tgt, "drift")
+        sb.record(stream)
+        sb.synchronize()
+        s_ms = sa.elapsed_time(sb) / reps
+        scatter = {"ms": s_ms, "value": n / (s_ms * 1e-3), "algorithmic_bytes_per_particle": 30,
+                   "achieved_GBps": 30 * n / (s_ms * 1e-3) / 1e9, "frac": 30 * n / (s_ms * 1e-3) / 1e9 / peak,
+                   "kernel": "k_convert (SoA binary16 x -> AoS f64 x lanes, write set only)",
+                   "note": "the 24-B x lanes of an 88-B record straddle 32-B sectors, so HBM also reads the "
+                           "sectors' other bytes (partial-sector writes)"}
+        del tgt
+
     # end to end through the C ABI: pinned host AoS in, host SoA out
     e2e = None
     if not args.no_e2e:
@@ -337,7 +361,7 @@ def b200_arm(args):
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform random records, device RNG)",
                 "config": config(n, world, prec_name), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks, "impl": "b200"}
+                "gpu_launches": launches, "clocks": clocks, "impl": "b200", "scatter_back": scatter}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -287,6 +287,89 @@ __device__ __forceinline__ uint64_t axpy_ieee(uint64_t xq, uint64_t yq, double d
     return Ieee<DB>::from(r);
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+void count_launches(uint64_t n);  // runtime.cpp
+
+// ----------------------------------------------------------------- k_convert_ieee
+// One COPY stream between plain IEEE lanes at byte-aligned, naturally aligned
+// addresses (e.g. the scatter-back of the drifted binary16 x into the f64 x
+// lanes of the AoS records): typed loads, one hardware cvt + the NaN payload
+// select, typed stores.  Each thread owns U records and issues all their
+// loads before any store, so several DRAM round trips are in flight per
+// thread (the generic k_convert, one bit-level lane at a time, is latency
+// bound on this pattern).
+template <int SB, int DB, int AR, int U>
+__global__ void __launch_bounds__(256) k_convert_ieee(const uint8_t* __restrict__ src, uint64_t s_base, uint64_t s_stride,
+                                                      uint8_t* __restrict__ dst, uint64_t d_base, uint64_t d_stride,
+                                                      uint64_t n) {
+    using TS = typename std::conditional<Ieee<SB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<SB>::w == 32, uint32_t, uint16_t>::type>::type;
+    using TD = typename std::conditional<Ieee<DB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<DB>::w == 32, uint32_t, uint16_t>::type>::type;
+    const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t r0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r0 < n; r0 += step * U) {
+        TS v[U][AR];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t r = r0 + u * step;
+            if (r < n) {
+                const TS* p = reinterpret_cast<const TS*>(src + s_base + r * s_stride);
+#pragma unroll
+                for (int l = 0; l < AR; ++l) v[u][l] = p[l];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t r = r0 + u * step;
+            if (r < n) {
+                TD* q = reinterpret_cast<TD*>(dst + d_base + r * d_stride);
+#pragma unroll
+                for (int l = 0; l < AR; ++l) q[l] = TD(cvt_ieee<SB, DB>(v[u][l]));
+            }
+        }
+    }
+}
+
+static int ieee_code(LaneFmt f) {
+    if (!fmt_is_ieee(f)) return -1;
+    return f.base == B_F16 ? B_F16 : f.base == B_BF16 ? B_BF16 : f.base == B_F32 ? B_F32 : f.base == B_F64 ? B_F64 : -1;
+}
+
+// a COPY stream the typed kernel can take: IEEE formats, byte-aligned,
+// naturally aligned lane addresses, arity 1 or 3
+static bool convert_ieee_ok(const CStream& c, const void* src, const void* dst) {
+    if (c.op != OP_COPY || ieee_code(c.src.fmt) < 0 || ieee_code(c.dst.fmt) < 0) return false;
+    if (c.src.arity != c.dst.arity || (c.src.arity != 1 && c.src.arity != 3)) return false;
+    const uint64_t ws = c.src.fmt.width, wd = c.dst.fmt.width;
+    if ((c.src.base | c.src.stride) % ws || (c.dst.base | c.dst.stride) % wd) return false;
+    return (reinterpret_cast<uintptr_t>(src) % (ws / 8)) == 0 && (reinterpret_cast<uintptr_t>(dst) % (wd / 8)) == 0;
+}
+
+template <int SB, int DB>
+static void launch_convert_ieee_t(const CStream& c, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t st,
+                                  int blocks) {
+    if (c.src.arity == 3)
+        k_convert_ieee<SB, DB, 3, 4><<<blocks, 256, 0, st>>>(src, c.src.base / 8, c.src.stride / 8, dst, c.dst.base / 8,
+                                                             c.dst.stride / 8, n);
+    else
+        k_convert_ieee<SB, DB, 1, 4><<<blocks, 256, 0, st>>>(src, c.src.base / 8, c.src.stride / 8, dst, c.dst.base / 8,
+                                                             c.dst.stride / 8, n);
+}
+
+template <int SB>
+static void launch_convert_ieee_s(const CStream& c, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t st,
+                                  int blocks) {
+    switch (ieee_code(c.dst.fmt)) {
+        case B_F16: launch_convert_ieee_t<SB, B_F16>(c, n, src, dst, st, blocks); break;
+        case B_BF16: launch_convert_ieee_t<SB, B_BF16>(c, n, src, dst, st, blocks); break;
+        case B_F32: launch_convert_ieee_t<SB, B_F32>(c, n, src, dst, st, blocks); break;
+        default: launch_convert_ieee_t<SB, B_F64>(c, n, src, dst, st, blocks); break;
+    }
+}
+
 // ----------------------------------------------------------------- k_gather_warp
 // Warp-autonomous AoS -> SoA pipeline.  Each warp owns a ring of kWStages
 // shared-memory stages fed by 1-D TMA bulk copies (cp.async.bulk, UBLKCP)
@@ -889,6 +972,25 @@ int num_sms();  // runtime.cpp
 
 cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st) {
     if (p.count == 0 || p.n == 0) return cudaSuccess;
+    bool typed = env_int("SFB_CONVERT_TYPED", 1) != 0;
+    for (uint32_t i = 0; i < p.n && typed; ++i) typed = convert_ieee_ok(p.s[i], src, dst);
+    if (typed && src != dst) {  // per stream; in place (src == dst) keeps the one-pass generic kernel
+        const uint64_t want = (p.count + 4 * 256 - 1) / (4 * 256);
+        const int blocks = int(std::min<uint64_t>(want, uint64_t(num_sms()) * 16));
+        for (uint32_t i = 0; i < p.n; ++i) {
+            const CStream& c = p.s[i];
+            const uint8_t* s8 = static_cast<const uint8_t*>(src);
+            uint8_t* d8 = static_cast<uint8_t*>(dst);
+            switch (ieee_code(c.src.fmt)) {
+                case B_F16: launch_convert_ieee_s<B_F16>(c, p.count, s8, d8, st, blocks); break;
+                case B_BF16: launch_convert_ieee_s<B_BF16>(c, p.count, s8, d8, st, blocks); break;
+                case B_F32: launch_convert_ieee_s<B_F32>(c, p.count, s8, d8, st, blocks); break;
+                default: launch_convert_ieee_s<B_F64>(c, p.count, s8, d8, st, blocks); break;
+            }
+        }
+        count_launches(p.n - 1);  // the caller counts one
+        return cudaGetLastError();
+    }
     const uint64_t want = (p.count + 255) / 256;
     const int blocks = int(std::min<uint64_t>(want, uint64_t(num_sms()) * 16));
     k_convert<<<blocks, 256, 0, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst));
@@ -899,10 +1001,6 @@ static size_t gather_warp_bytes(const GatherPlan& p) {
     return size_t(p.stages) * ((p.tile_bytes + 16 + 15) & ~15u) + p.out_bytes;
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
                           int /*ctas_per_sm*/) {
