@@ -292,6 +292,7 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 void count_launches(uint64_t n);  // runtime.cpp
+int num_sms();                    // runtime.cpp
 
 // ----------------------------------------------------------------- k_convert_ieee
 // One COPY stream between plain IEEE lanes at byte-aligned, naturally aligned
@@ -333,6 +334,57 @@ __global__ void __launch_bounds__(256) k_convert_ieee(const uint8_t* __restrict_
     }
 }
 
+// 8-byte destination lanes scattered into wide records (the drift
+// scatter-back: binary16 x -> the f64 x lanes of 88-B AoS records).  Writing
+// 24 B inside 32-B sectors makes L2 fetch every partially written sector from
+// HBM before it can merge, so here each thread reads the 1-2 whole aligned
+// sectors around its lanes itself, patches the lanes in registers and writes
+// the sectors back whole (two 16-B stores each): the same DRAM bytes, but
+// full-sector writes and loads issued by the SMs.  The host takes this path
+// only when the record stride keeps neighbouring records' sectors disjoint.
+template <int SB, int AR>
+__global__ void __launch_bounds__(256) k_scatter_sectors(const uint8_t* __restrict__ src, uint64_t s_base,
+                                                         uint64_t s_stride, uint8_t* __restrict__ dst, uint64_t d_base,
+                                                         uint64_t d_stride, uint64_t n) {
+    using TS = typename std::conditional<Ieee<SB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<SB>::w == 32, uint32_t, uint16_t>::type>::type;
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
+        const TS* p = reinterpret_cast<const TS*>(src + s_base + r * s_stride);
+        uint64_t v[AR];
+#pragma unroll
+        for (int l = 0; l < AR; ++l) v[l] = p[l];
+        const uint64_t o = d_base + r * d_stride;
+        const uint64_t a = o & ~uint64_t(31);
+        const int w0 = int(o - a) >> 3;            // first lane's word in the window
+        const bool two = (o - a) + 8 * AR > 32;    // lanes spill into the next sector
+        // one 256-bit access per sector (LDG/STG.E.ENL2.256): L2 sees whole-sector writes
+        uint64_t wd[8];
+        const uint64_t* g = reinterpret_cast<const uint64_t*>(dst + a);
+        asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(wd[0]), "=l"(wd[1]), "=l"(wd[2]), "=l"(wd[3]) : "l"(g));
+        if (two)
+            asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(wd[4]), "=l"(wd[5]), "=l"(wd[6]), "=l"(wd[7]) : "l"(g + 4));
+        // static register indices for each of the four lane offsets
+#define SFB_PATCH(W0)                                                                    \
+    _Pragma("unroll") for (int l = 0; l < AR; ++l) wd[(W0) + l] = cvt_ieee<SB, B_F64>(v[l]);
+        switch (w0) {
+            case 0: SFB_PATCH(0) break;
+            case 1: SFB_PATCH(1) break;
+            case 2: SFB_PATCH(2) break;
+            default: SFB_PATCH(3) break;
+        }
+#undef SFB_PATCH
+        uint64_t* q = reinterpret_cast<uint64_t*>(dst + a);
+        asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(q), "l"(wd[0]), "l"(wd[1]), "l"(wd[2]), "l"(wd[3])
+                     : "memory");
+        if (two)
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(q + 4), "l"(wd[4]), "l"(wd[5]), "l"(wd[6]),
+                         "l"(wd[7])
+                         : "memory");
+    }
+}
+
 static int ieee_code(LaneFmt f) {
     if (!fmt_is_ieee(f)) return -1;
     return f.base == B_F16 ? B_F16 : f.base == B_BF16 ? B_BF16 : f.base == B_F32 ? B_F32 : f.base == B_F64 ? B_F64 : -1;
@@ -362,6 +414,19 @@ static void launch_convert_ieee_t(const CStream& c, uint64_t n, const uint8_t* s
 template <int SB>
 static void launch_convert_ieee_s(const CStream& c, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t st,
                                   int blocks) {
+    // sector read-patch-write for 8-B lanes in wide records (neighbouring records' sectors disjoint)
+    const uint64_t span = uint64_t(c.dst.arity) * 8;
+    if (ieee_code(c.dst.fmt) == B_F64 && c.dst.arity <= 3 && c.dst.stride / 8 >= span + 64 &&
+        (reinterpret_cast<uintptr_t>(dst) & 31) == 0 && env_int("SFB_SCATTER_SECTORS", 1)) {
+        const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+        if (c.dst.arity == 3)
+            k_scatter_sectors<SB, 3><<<g, 256, 0, st>>>(src, c.src.base / 8, c.src.stride / 8, dst, c.dst.base / 8,
+                                                        c.dst.stride / 8, n);
+        else
+            k_scatter_sectors<SB, 1><<<g, 256, 0, st>>>(src, c.src.base / 8, c.src.stride / 8, dst, c.dst.base / 8,
+                                                        c.dst.stride / 8, n);
+        return;
+    }
     switch (ieee_code(c.dst.fmt)) {
         case B_F16: launch_convert_ieee_t<SB, B_F16>(c, n, src, dst, st, blocks); break;
         case B_BF16: launch_convert_ieee_t<SB, B_BF16>(c, n, src, dst, st, blocks); break;
@@ -968,7 +1033,6 @@ __global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf
 }
 
 // ----------------------------------------------------------------- launchers
-int num_sms();  // runtime.cpp
 
 cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st) {
     if (p.count == 0 || p.n == 0) return cudaSuccess;
