@@ -511,3 +511,50 @@ def test_nan_inf_drift_matches_live_reference(prec):
     api.run_kernel(soa, "drift", 1e-3, 64)
     np.testing.assert_array_equal(host(soa), want)
     R.free(h, st, u, nw, so)
+
+
+def test_cells_non_cubic_grid():
+    """A box of 1 x 0.5 x 0.25 on a non-cubic cell grid (nx != ny != nz);
+    the oracle's cubic cell list only enumerates candidates, so any grid with
+    cells >= 2 h_max must give the same sums."""
+    n = 1 << 14
+    rng = np.random.default_rng(13)
+    x = rng.random((n, 3)) * np.array([1.0, 0.5, 0.25])
+    h = np.full(n, 0.5 * (3 * 64 * 0.125 / (4 * np.pi * n)) ** (1 / 3))
+    m = np.full(n, 1.0 / n)
+    nc = int(np.floor(1.0 / (2 * h[0])))
+    cell = 1.0 / nc
+    dims = (nc, int(np.ceil(0.5 / cell)), int(np.ceil(0.25 / cell)))
+    xt, mt, ht = (torch.tensor(a, device="cuda", dtype=torch.float32) for a in (x, m, h))
+    xd, md, hd = (t.double().cpu().numpy() for t in (xt, mt, ht))
+    want = O.density_cells(xd.reshape(-1), md, hd, 0.0, 1.0, cell)
+    for refine in (1, 2):
+        d = tuple(k * refine for k in dims)
+        cs, perm = api.bin_particles(xt, (0, 0, 0), cell / refine, d)
+        rho = api.density_cells(xt, mt, ht, cs, perm, (0, 0, 0), cell / refine, d, reach=refine)
+        np.testing.assert_allclose(rho.double().cpu().numpy(), want, rtol=1e-5)
+
+
+def test_cells_coincident_particles():
+    """Distinct particles at identical positions (r = 0): density counts
+    m_j W(0) for each, the force's grad W(0) = 0 (sph.cpp:35-40) — no NaN."""
+    n = 1 << 13
+    rng = np.random.default_rng(17)
+    x = rng.random((n, 3))
+    x[1::7] = x[0::7][: len(x[1::7])]   # every 7th pair coincides exactly
+    h = np.full(n, 0.5 * (3 * 64 / (4 * np.pi * n)) ** (1 / 3))
+    m = rng.uniform(0.5, 1.5, n) / n
+    v = rng.uniform(-1, 1, (n, 3))
+    nc = int(np.floor(1.0 / (2 * h[0])))
+    ts = [torch.tensor(a, device="cuda", dtype=torch.float32) for a in (x, v, m, h)]
+    xd, vd, md, hd = (t.double().cpu().numpy() for t in ts)
+    cs, perm = api.bin_particles(ts[0], (0, 0, 0), 1.0 / nc, (nc, nc, nc))
+    rho = api.density_cells(ts[0], ts[2], ts[3], cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc))
+    want = O.density_cells(xd.reshape(-1), md, hd, 0.0, 1.0, 1.0 / nc)
+    np.testing.assert_allclose(rho.double().cpu().numpy(), want, rtol=1e-5)
+    P = rho * 0.6
+    a, du = api.force_cells(ts[0], ts[1], ts[2], ts[3], rho, P, cs, perm, (0, 0, 0), 1.0 / nc, (nc, nc, nc))
+    assert torch.isfinite(a).all() and torch.isfinite(du).all()
+    wa, wdu, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rho.double().cpu().numpy(),
+                                    P.double().cpu().numpy(), 0.0, 1.0, 1.0 / nc)
+    assert np.all(np.linalg.norm(a.double().cpu().numpy() - wa, axis=1) <= FORCE_TOL * sa)
