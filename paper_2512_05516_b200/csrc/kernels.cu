@@ -435,6 +435,107 @@ static void launch_convert_ieee_s(const CStream& c, uint64_t n, const uint8_t* s
     }
 }
 
+// ----------------------------------------------------------------- k_gather_multi
+// Many-stream AoS -> SoA COPY plans (e.g. the full record set to binary16):
+// one thread per record reads every stream's lanes straight from the record
+// (typed loads; the record's sectors stay in L1 between streams, so HBM reads
+// each record once) and writes each SoA stream with lane-consecutive stores.
+// The TMA-tiled k_gather_warp pays a switch, a warp store and two warp
+// barriers per stream per 32-record tile, which dominates when a plan has a
+// dozen thin streams.  mkind: 1 + 4*src + dst over {F16, BF16, F32, F64}
+// (src == dst: bit copy), 17/18/19: raw 16/32/64-bit copy (any format).
+// the hardware conversion alone (finite and infinite values; NaN payloads
+// need cvt_ieee's select)
+template <int SB, int DB>
+__device__ __forceinline__ uint64_t cvt_plain(uint64_t s) {
+    if constexpr (SB == DB) {
+        return s;
+    } else if constexpr (SB == B_F32 && DB == B_F16) {
+        const __half h = __float2half_rn(bits_to_f32(uint32_t(s)));
+        return *reinterpret_cast<const uint16_t*>(&h);
+    } else if constexpr (SB == B_F32 && DB == B_BF16) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(bits_to_f32(uint32_t(s)));
+        return *reinterpret_cast<const uint16_t*>(&h);
+    } else {
+        return Ieee<DB>::from(Ieee<SB>::f64(s));
+    }
+}
+
+// Converts `ar` lanes; a NaN source lane redoes the stream through cvt_ieee
+// (the reference's payload rule) — rare, so off the hot path.
+template <int SB, int DB>
+__device__ __forceinline__ void multi_lanes(const uint8_t* __restrict__ s, uint8_t* __restrict__ d, int ar) {
+    using TS = typename std::conditional<Ieee<SB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<SB>::w == 32, uint32_t, uint16_t>::type>::type;
+    using TD = typename std::conditional<Ieee<DB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<DB>::w == 32, uint32_t, uint16_t>::type>::type;
+    const TS* ps = reinterpret_cast<const TS*>(s);
+    TD* pd = reinterpret_cast<TD*>(d);
+    bool bad = false;
+    if (ar == 3) {
+        const TS a = ps[0], b = ps[1], c = ps[2];
+        bad = Ieee<SB>::nan(a) | Ieee<SB>::nan(b) | Ieee<SB>::nan(c);
+        pd[0] = TD(cvt_plain<SB, DB>(a));
+        pd[1] = TD(cvt_plain<SB, DB>(b));
+        pd[2] = TD(cvt_plain<SB, DB>(c));
+    } else {
+        for (int l = 0; l < ar; ++l) {
+            bad |= Ieee<SB>::nan(ps[l]);
+            pd[l] = TD(cvt_plain<SB, DB>(ps[l]));
+        }
+    }
+    if (bad)
+        for (int l = 0; l < ar; ++l) pd[l] = TD(cvt_ieee<SB, DB>(ps[l]));
+}
+
+template <typename T>
+__device__ __forceinline__ void multi_raw(const uint8_t* __restrict__ s, uint8_t* __restrict__ d, int ar) {
+    for (int l = 0; l < ar; ++l) reinterpret_cast<T*>(d)[l] = reinterpret_cast<const T*>(s)[l];
+}
+
+__global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ GatherPlan P, const uint8_t* __restrict__ src,
+                                                      uint8_t* __restrict__ dst) {
+    const uint64_t n = P.count, rbytes = P.record_bits >> 3;
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
+        const uint8_t* rec = src + r * rbytes;
+        for (uint32_t q = 0; q < P.n; ++q) {
+            const GStream& g = P.s[q];
+            const uint8_t* s = rec + (g.src_off >> 3);
+            const int ar = g.arity;
+            uint8_t* d = dst + g.dst_base + r * uint64_t(ar) * (g.dst.width >> 3);
+            switch (g.mkind) {
+#define SFB_M(SI, SB, DI, DB) \
+    case 1 + 4 * SI + DI: multi_lanes<SB, DB>(s, d, ar); break;
+#define SFB_MS(SI, SB) SFB_M(SI, SB, 0, B_F16) SFB_M(SI, SB, 1, B_BF16) SFB_M(SI, SB, 2, B_F32) SFB_M(SI, SB, 3, B_F64)
+                SFB_MS(0, B_F16)
+                SFB_MS(1, B_BF16)
+                SFB_MS(2, B_F32)
+                SFB_MS(3, B_F64)
+#undef SFB_MS
+#undef SFB_M
+                case 17: multi_raw<uint16_t>(s, d, ar); break;
+                case 18: multi_raw<uint32_t>(s, d, ar); break;
+                default: multi_raw<uint64_t>(s, d, ar); break;
+            }
+        }
+    }
+}
+
+// the k_gather_multi kind of a stream, 0 when it cannot take it
+static uint8_t multi_kind(const GStream& g, uint32_t record_bits) {
+    if (g.op != OP_COPY || g.arity < 1) return 0;
+    const uint32_t ws = g.src.width, wd = g.dst.width;
+    if (g.src_off % ws || record_bits % ws || (wd != 16 && wd != 32 && wd != 64) || g.dst_base % (wd / 8)) return 0;
+    if (ws == wd && (fmt_eq(g.src, g.dst) || g.src.base == B_INT || g.dst.base == B_INT)) {
+        if (!fmt_eq(g.src, g.dst)) return 0;  // an int <-> float change is not a bit copy
+        return ws == 16 ? 17 : ws == 32 ? 18 : 19;
+    }
+    const int si = ieee_code(g.src), di = ieee_code(g.dst);
+    if (si < 0 || di < 0) return 0;
+    auto idx = [](int b) { return b == B_F16 ? 0 : b == B_BF16 ? 1 : b == B_F32 ? 2 : 3; };
+    return uint8_t(1 + 4 * idx(si) + idx(di));
+}
+
 // ----------------------------------------------------------------- k_gather_warp
 // Warp-autonomous AoS -> SoA pipeline.  Each warp owns a ring of kWStages
 // shared-memory stages fed by 1-D TMA bulk copies (cp.async.bulk, UBLKCP)
@@ -1089,6 +1190,19 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
                                                src_bytes);
         return cudaGetLastError();
     };
+    // many thin COPY streams: direct typed loads, one thread per record
+    if (p.proc != PROC_XV_F16 && p.proc != PROC_XV_BF16 && p.proc != PROC_XV_F32 && p.n >= 3 &&
+        env_int("SFB_GATHER_MULTI", 1) && (reinterpret_cast<uintptr_t>(src) & 7) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+        bool ok = true;
+        for (uint32_t i = 0; i < p.n && ok; ++i) ok = (p.s[i].mkind = multi_kind(p.s[i], p.record_bits)) != 0;
+        if (ok) {
+            // one thread per record, uncapped grid: CTAs in flight cover one compact record range
+            const int mb = int((p.count + 255) / 256);
+            k_gather_multi<<<mb, 256, 0, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst));
+            return cudaGetLastError();
+        }
+    }
     switch (p.proc) {
         case PROC_XV_F16: return go(k_gather_warp<ProcXV<B_F16>>);
         case PROC_XV_BF16: return go(k_gather_warp<ProcXV<B_BF16>>);

@@ -59,6 +59,8 @@ struct GStream {
     // compile-time-specialised IEEE path (kernels.cu gather_fast_kind);
     // 0 = generic bit-level path
     uint8_t fast = 0;
+    // typed direct-load COPY kind of k_gather_multi (set at launch); 0 = none
+    uint8_t mkind = 0;
 };
 
 struct GatherPlan {
