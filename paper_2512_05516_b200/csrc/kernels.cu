@@ -493,6 +493,31 @@ __device__ __forceinline__ void multi_raw(const uint8_t* __restrict__ s, uint8_t
     for (int l = 0; l < ar; ++l) reinterpret_cast<T*>(d)[l] = reinterpret_cast<const T*>(s)[l];
 }
 
+// x + y*dt (kick v, u / drift x) fused into the copy: quantize both operands
+// to the destination format, then the same arithmetic and NaN rules as
+// stream_hot / stream_fast.
+template <int SB, int DB, int AB>
+__device__ __forceinline__ void multi_axpy(const uint8_t* __restrict__ s, const uint8_t* __restrict__ y,
+                                           uint8_t* __restrict__ d, int ar, uint8_t op, double dt, uint8_t math) {
+    using TD = typename std::conditional<Ieee<DB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<DB>::w == 32, uint32_t, uint16_t>::type>::type;
+    constexpr int sb = Ieee<SB>::w / 8, ab = Ieee<AB>::w / 8;
+    TD* pd = reinterpret_cast<TD*>(d);
+    for (int l = 0; l < ar; ++l) {
+        const uint64_t xs = lds<SB>(s + l * sb), ys = lds<AB>(y + l * ab);
+        bool bad = Ieee<SB>::nan(xs) | Ieee<AB>::nan(ys);
+        const uint64_t xq = cvt_plain<SB, DB>(xs), yq = cvt_plain<AB, DB>(ys);
+        double res;
+        if (math == MATH_FP64_EXACT) res = __dadd_rn(Ieee<DB>::f64(xq), __dmul_rn(Ieee<DB>::f64(yq), dt));
+        else res = double(__fadd_rn(float(Ieee<DB>::f64(xq)), __fmul_rn(float(Ieee<DB>::f64(yq)), float(dt))));
+        bad |= isnan(res);
+        if (op == OP_AXPY_CLAMP0 && res < 0.0) res = 0.0;
+        uint64_t out = Ieee<DB>::from(res);
+        if (bad) out = axpy_ieee<DB>(cvt_ieee<SB, DB>(xs), cvt_ieee<AB, DB>(ys), dt, op, math);
+        pd[l] = TD(out);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ GatherPlan P, const uint8_t* __restrict__ src,
                                                       uint8_t* __restrict__ dst) {
     const uint64_t n = P.count, rbytes = P.record_bits >> 3;
@@ -515,7 +540,22 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
 #undef SFB_M
                 case 17: multi_raw<uint16_t>(s, d, ar); break;
                 case 18: multi_raw<uint32_t>(s, d, ar); break;
-                default: multi_raw<uint64_t>(s, d, ar); break;
+                case 19: multi_raw<uint64_t>(s, d, ar); break;
+                default: {  // 64 + 8 src + 2 dst + aux over src, aux in {F64, F32}
+                    const uint8_t* y = rec + (g.aux_off >> 3);
+                    switch (g.mkind) {
+#define SFB_A(SI, SB, DI, DB, AI, AB) \
+    case 64 + 8 * SI + 2 * DI + AI: multi_axpy<SB, DB, AB>(s, y, d, ar, g.op, P.dt, P.math); break;
+#define SFB_AD(SI, SB, DI, DB) SFB_A(SI, SB, DI, DB, 0, B_F64) SFB_A(SI, SB, DI, DB, 1, B_F32)
+#define SFB_AS(SI, SB) SFB_AD(SI, SB, 0, B_F16) SFB_AD(SI, SB, 1, B_BF16) SFB_AD(SI, SB, 2, B_F32) SFB_AD(SI, SB, 3, B_F64)
+                        SFB_AS(0, B_F64)
+                        SFB_AS(1, B_F32)
+#undef SFB_AS
+#undef SFB_AD
+#undef SFB_A
+                        default: break;
+                    }
+                }
             }
         }
     }
@@ -523,8 +563,18 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
 
 // the k_gather_multi kind of a stream, 0 when it cannot take it
 static uint8_t multi_kind(const GStream& g, uint32_t record_bits) {
-    if (g.op != OP_COPY || g.arity < 1) return 0;
+    if (g.arity < 1) return 0;
     const uint32_t ws = g.src.width, wd = g.dst.width;
+    if (g.op != OP_COPY) {  // fused x + y*dt: IEEE f64/f32 operands, y quantized to the destination format
+        const int si = ieee_code(g.src), di = ieee_code(g.dst), ai = ieee_code(g.aux_src);
+        if ((si != B_F64 && si != B_F32) || (ai != B_F64 && ai != B_F32) || di < 0 || !fmt_eq(g.aux_dst, g.dst))
+            return 0;
+        if (g.src_off % ws || g.aux_off % g.aux_src.width || record_bits % ws || record_bits % g.aux_src.width ||
+            g.dst_base % (wd / 8))
+            return 0;
+        auto didx = [](int b) { return b == B_F16 ? 0 : b == B_BF16 ? 1 : b == B_F32 ? 2 : 3; };
+        return uint8_t(64 + 8 * (si == B_F64 ? 0 : 1) + 2 * didx(di) + (ai == B_F64 ? 0 : 1));
+    }
     if (g.src_off % ws || record_bits % ws || (wd != 16 && wd != 32 && wd != 64) || g.dst_base % (wd / 8)) return 0;
     if (ws == wd && (fmt_eq(g.src, g.dst) || g.src.base == B_INT || g.dst.base == B_INT)) {
         if (!fmt_eq(g.src, g.dst)) return 0;  // an int <-> float change is not a bit copy

@@ -558,3 +558,34 @@ def test_cells_coincident_particles():
     wa, wdu, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rho.double().cpu().numpy(),
                                     P.double().cpu().numpy(), 0.0, 1.0, 1.0 / nc)
     assert np.all(np.linalg.norm(a.double().cpu().numpy() - wa, axis=1) <= FORCE_TOL * sa)
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("prec", [16, 32])
+def test_nan_inf_kick_matches_live_reference(prec):
+    """NaN / inf / overflow in v, u, a, du through store_state(T) -> kick (the
+    fused gather's x + y*dt and max(0, .) lanes): bit for bit vs the reference."""
+    n = 4096
+    ob, P, src = default_aos(n=n)
+    rec = ob.data.reshape(n, 88)
+    f32 = np.float32([np.nan, -np.nan, np.inf, -np.inf, 3e38, -3e38, 1e-45, 0.0, -0.0])
+    for k in range(0, n, 5):
+        lane = k % 3
+        rec[k, 32 + 4 * lane: 36 + 4 * lane] = f32[k % f32.size: k % f32.size + 1].view(np.uint8)      # v
+        rec[k, 68 + 4 * lane: 72 + 4 * lane] = f32[(k + 3) % f32.size:(k + 3) % f32.size + 1].view(np.uint8)  # a
+        if k % 2 == 0:
+            rec[k, 44:48] = f32[(k + 1) % f32.size:(k + 1) % f32.size + 1].view(np.uint8)   # u
+            rec[k, 80:84] = f32[(k + 5) % f32.size:(k + 5) % f32.size + 1].view(np.uint8)   # du
+    src = dev(ob, api.View(P, n, "aos"))
+    R = O.RefLib()
+    h = R.L.ref_buf_from_bytes(None, 0, b"", n, O._p(ob.data), ob.data.size)
+    assert h
+    st = R.restore(h, prec)
+    u = R.op(st, "unpack")
+    nw = R.op(u, "narrow", "kick")
+    so = R.op(nw, "aos_to_soa")
+    R.run_kernel(so, "kick", 64, 1e-3)
+    want = R.bytes(so)
+    got = api.gather_kernel(src, api.View(P, n, "soa", "kick", prec), "kick", 1e-3)
+    np.testing.assert_array_equal(host(got), want)
+    R.free(h, st, u, nw, so)
