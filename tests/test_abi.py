@@ -218,3 +218,28 @@ def test_cell_entry_points_fail_loudly_without_device():
     st = L.lib().sf_b200_force_cells(None, p(f), p(f), p(f), p(f), p(f), 1, n, p(i32), p(i32), p(lo), 0.5, 2, 2, 2,
                                      1, n, p(f), p(f), None)
     assert st == L.SF_INVALID_ARG
+
+
+def test_block_and_ipc_entry_points_fail_loudly_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    n = 64
+    f = (C.c_float * (4 * n))()
+    i32 = (C.c_int32 * (n + 8))()
+    p = lambda a: C.cast(a, C.c_void_p)  # noqa: E731
+    lib = L.lib()
+    assert lib.sf_b200_cells_pack(p(f), p(f), p(f), 1, n, p(i32), p(f), p(f), p(i32), None) == L.SF_ERROR
+    assert "no CUDA device" in lib.sf_last_error().decode()
+    blk = L.SfCellBlock(C.cast(f, C.c_void_p).value, C.cast(f, C.c_void_p).value, C.cast(i32, C.c_void_p).value,
+                        C.cast(i32, C.c_void_p).value, 0, 2, 0.0, 0)
+    lo = (C.c_float * 2)(0, 0)
+    arr = (L.SfCellBlock * 1)(blk)
+    assert lib.sf_b200_density_cells_blocks(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 1, p(f), None) == L.SF_ERROR
+    assert lib.sf_b200_force_pack(p(f), p(f), p(f), p(f), 1, n, p(i32), p(f), p(f), None) == L.SF_ERROR
+    out = C.c_void_p()
+    assert lib.sf_b200_dev_alloc(1024, C.byref(out)) == L.SF_ERROR
+    assert "no CUDA device" in lib.sf_last_error().decode()
+    h = (C.c_uint8 * L.SF_IPC_HANDLE_BYTES)()
+    assert lib.sf_b200_ipc_open(p(h), C.byref(out)) == L.SF_ERROR
+    assert lib.sf_b200_ipc_handle(None, p(h)) == L.SF_INVALID_ARG
