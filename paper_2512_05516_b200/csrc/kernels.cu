@@ -5,11 +5,19 @@
 //                    shared memory by per-warp 1-D TMA bulk copies (cp.async.bulk,
 //                    UBLKCP) through an mbarrier ring; lanes extracted with
 //                    funnel shifts (any bit offset/width); 16-B SoA stores.
+//   k_gather_multi   AoS -> SoA plans of many thin 16/32/64-bit streams (full
+//                    record, kick / density sets, gather fused with kick):
+//                    thread per record, direct typed loads.
+//   k_convert_ieee   one COPY stream between IEEE lanes, typed; and
+//   k_scatter_sectors  8-B lanes into wide records by whole-sector
+//                    read-patch-write (256-bit accesses): the scatter-back.
 //   k_convert        generic lane-by-lane conversion between any two views
-//                    (scatter-back / N^T merge, store_state narrowing,
-//                    in-place kick/drift on any view).  Byte-aligned
-//                    destinations use plain stores, bit-packed ones use
-//                    32-bit atomics so neighbouring lanes never race.
+//                    (truncated / bit-packed lanes, in-place kick/drift on
+//                    any view).  Byte-aligned destinations use plain stores,
+//                    bit-packed ones use 32-bit atomics so neighbouring lanes
+//                    never race.
+//   k_update_soa / k_update_rec(_multi)  in-place kick/drift on SoA streams /
+//                    AoS records with typed vector loads.
 //   k_density_buffer the reference density (sph.cpp:176-199): one CTA per
 //                    64-particle neighbour buffer, binary64 with separately
 //                    rounded operations, ascending j, self term included.
