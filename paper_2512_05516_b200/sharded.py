@@ -298,12 +298,14 @@ class PeerBlocks:
     def _ensure(self, n: int):
         import torch.distributed as dist
         grow = n > self.cap
+        retired = None
         if grow:
-            if self.buf is not None:
-                self.buf.free()
+            retired = self.buf  # freed only after every neighbour has unmapped it
             self.cap = max(int(n * 1.2) + 1024, 1024)
             self.buf = self.api.DeviceBuffer(self.layout(self.ncell, self.cap)[-1])
         if self.slab.world == 1:
+            if retired is not None:
+                retired.free()
             return
         dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
         flag = torch.tensor([int(grow)], device=dev)
@@ -314,12 +316,15 @@ class PeerBlocks:
         every = [None] * self.slab.world
         dist.all_gather_object(every, info, group=self.group)
         for r, old in list(self.peers.items()):
-            old[0].free()
+            old[0].free()  # unmap the neighbour's previous block
         self.peers = {}
         for r in (self.slab.rank - 1, self.slab.rank + 1):
             if 0 <= r < self.slab.world:
                 hd, cap, x0, nx, ncell, xo = every[r]
                 self.peers[r] = (self.api.DeviceBuffer(handle=hd), cap, x0, nx, ncell, xo)
+        dist.barrier(group=self.group)  # every mapping of the retired blocks is closed
+        if retired is not None:
+            retired.free()
 
     def _peer_block(self, r, force=False):
         mapped, cap, x0, nx, ncell, xo = self.peers[r]

@@ -209,6 +209,10 @@ def _peer_worker(rank, world, port, outdir, n):
     pb = PeerBlocks(slab, 2)
     rho = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))
     rho2 = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))  # second step: buffers reused, no new handles
+    if rank == 0:
+        pb.cap = 0  # rank 0 reallocates its block: every rank re-exchanges handles and re-maps
+    rho3 = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))
+    assert torch.equal(rho3, rho2)
     v = np.random.default_rng(32).uniform(-1, 1, (n, 3))
     a, du = pb.force(t(v[own]), t(m[own]), rho2, rho2 * 0.7)
     np.savez(os.path.join(outdir, f"p{rank}.npz"), own=own, rho=rho.cpu().numpy(), rho2=rho2.cpu().numpy(),
