@@ -480,7 +480,11 @@ __device__ __forceinline__ void multi_lanes(const uint8_t* __restrict__ s, uint8
     const TS* ps = reinterpret_cast<const TS*>(s);
     TD* pd = reinterpret_cast<TD*>(d);
     bool bad = false;
-    if (ar == 3) {
+    if (ar == 1) {
+        const TS a = ps[0];
+        bad = Ieee<SB>::nan(a);
+        pd[0] = TD(cvt_plain<SB, DB>(a));
+    } else if (ar == 3) {
         const TS a = ps[0], b = ps[1], c = ps[2];
         bad = Ieee<SB>::nan(a) | Ieee<SB>::nan(b) | Ieee<SB>::nan(c);
         pd[0] = TD(cvt_plain<SB, DB>(a));
@@ -498,6 +502,10 @@ __device__ __forceinline__ void multi_lanes(const uint8_t* __restrict__ s, uint8
 
 template <typename T>
 __device__ __forceinline__ void multi_raw(const uint8_t* __restrict__ s, uint8_t* __restrict__ d, int ar) {
+    if (ar == 1) {
+        reinterpret_cast<T*>(d)[0] = reinterpret_cast<const T*>(s)[0];
+        return;
+    }
     for (int l = 0; l < ar; ++l) reinterpret_cast<T*>(d)[l] = reinterpret_cast<const T*>(s)[l];
 }
 
@@ -531,14 +539,22 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
     const uint64_t n = P.count, rbytes = P.record_bits >> 3;
     for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
         const uint8_t* rec = src + r * rbytes;
-        for (uint32_t q = 0; q < P.n; ++q) {
-            const GStream& g = P.s[q];
-            const uint8_t* s = rec + (g.src_off >> 3);
-            const int ar = g.arity;
-            uint8_t* d = dst + g.dst_base + r * uint64_t(ar) * (g.dst.width >> 3);
-            switch (g.mkind) {
+        // the host orders the streams by kind: one dispatch per run of equal kinds
+        for (uint32_t q0 = 0; q0 < P.n;) {
+            const uint8_t kind = P.s[q0].mkind;
+            uint32_t q1 = q0 + 1;
+            while (q1 < P.n && P.s[q1].mkind == kind) ++q1;
+#define SFB_EACH(CALL)                                                              \
+    for (uint32_t q = q0; q < q1; ++q) {                                           \
+        const GStream& g = P.s[q];                                                  \
+        const uint8_t* s = rec + (g.src_off >> 3);                                  \
+        const int ar = g.arity;                                                     \
+        uint8_t* d = dst + g.dst_base + r * uint64_t(ar) * (g.dst.width >> 3);       \
+        CALL;                                                                       \
+    }
+            switch (kind) {
 #define SFB_M(SI, SB, DI, DB) \
-    case 1 + 4 * SI + DI: multi_lanes<SB, DB>(s, d, ar); break;
+    case 1 + 4 * SI + DI: SFB_EACH((multi_lanes<SB, DB>(s, d, ar))) break;
 #define SFB_MS(SI, SB) SFB_M(SI, SB, 0, B_F16) SFB_M(SI, SB, 1, B_BF16) SFB_M(SI, SB, 2, B_F32) SFB_M(SI, SB, 3, B_F64)
                 SFB_MS(0, B_F16)
                 SFB_MS(1, B_BF16)
@@ -546,14 +562,14 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
                 SFB_MS(3, B_F64)
 #undef SFB_MS
 #undef SFB_M
-                case 17: multi_raw<uint16_t>(s, d, ar); break;
-                case 18: multi_raw<uint32_t>(s, d, ar); break;
-                case 19: multi_raw<uint64_t>(s, d, ar); break;
+                case 17: SFB_EACH((multi_raw<uint16_t>(s, d, ar))) break;
+                case 18: SFB_EACH((multi_raw<uint32_t>(s, d, ar))) break;
+                case 19: SFB_EACH((multi_raw<uint64_t>(s, d, ar))) break;
                 default: {  // 64 + 8 src + 2 dst + aux over src, aux in {F64, F32}
-                    const uint8_t* y = rec + (g.aux_off >> 3);
-                    switch (g.mkind) {
+                    switch (kind) {
 #define SFB_A(SI, SB, DI, DB, AI, AB) \
-    case 64 + 8 * SI + 2 * DI + AI: multi_axpy<SB, DB, AB>(s, y, d, ar, g.op, P.dt, P.math); break;
+    case 64 + 8 * SI + 2 * DI + AI:   \
+        SFB_EACH((multi_axpy<SB, DB, AB>(s, rec + (g.aux_off >> 3), d, ar, g.op, P.dt, P.math))) break;
 #define SFB_AD(SI, SB, DI, DB) SFB_A(SI, SB, DI, DB, 0, B_F64) SFB_A(SI, SB, DI, DB, 1, B_F32)
 #define SFB_AS(SI, SB) SFB_AD(SI, SB, 0, B_F16) SFB_AD(SI, SB, 1, B_BF16) SFB_AD(SI, SB, 2, B_F32) SFB_AD(SI, SB, 3, B_F64)
                         SFB_AS(0, B_F64)
@@ -565,6 +581,8 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
                     }
                 }
             }
+#undef SFB_EACH
+            q0 = q1;
         }
     }
 }
@@ -1254,6 +1272,8 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
         (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
         bool ok = true;
         for (uint32_t i = 0; i < p.n && ok; ++i) ok = (p.s[i].mkind = multi_kind(p.s[i], p.record_bits)) != 0;
+        if (ok)  // group equal kinds (every stream writes its own SoA range, so the order is free)
+            std::stable_sort(p.s, p.s + p.n, [](const GStream& a, const GStream& b) { return a.mkind < b.mkind; });
         if (ok) {
             // one thread per record, uncapped grid: CTAs in flight cover one compact record range
             const int mb = int((p.count + 255) / 256);
