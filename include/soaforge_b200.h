@@ -225,12 +225,14 @@ SF_API uint64_t sf_b200_bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
  *                    in-place conversion on the migrated pages;
  *   mode 2 INPLACE:  pinned host memory, whole records each way (the
  *                    reference's in-place round trip).
+ *   mode 3 MANAGED_MAPPED: managed memory kept on the host and never
+ *                    migrated; the kernels read/write its pages over PCIe.
  * All modes pipeline H2D k+1 ∥ compute k ∥ D2H k-1 over 3 streams.
  * host_soa (optional): when non-NULL the SoA result (dst view, all
  * records) is copied to this host buffer instead of scattering back into
  * the AoS — the end-to-end form of the fused gather+kernel path.
  * metrics[0..4] = {seconds, h2d_bytes, d2h_bytes, chunks, kernel_launches}. */
-enum { SF_MODE_STREAMED = 0, SF_MODE_MANAGED = 1, SF_MODE_INPLACE = 2 };
+enum { SF_MODE_STREAMED = 0, SF_MODE_MANAGED = 1, SF_MODE_INPLACE = 2, SF_MODE_MANAGED_MAPPED = 3 };
 SF_API sf_status sf_b200_run_host(const sf_view* src, void* host_aos, const sf_view* dst,
                                   const char* kernels, double dt, int math, int mode,
                                   uint64_t chunk_records, void* host_soa, double* metrics);

@@ -14,7 +14,7 @@ SF_OK, SF_ERROR, SF_INVALID_ARG, SF_PARSE_ERROR, SF_CHECK_FAILED = range(5)
 SF_LAYOUT_AOS, SF_LAYOUT_SOA = 0, 1
 SF_PREC_STORED, SF_PREC_NATIVE, SF_PREC_BF16, SF_PREC_PACKED = 0, 1, 100, 1000
 SF_MATH_FP64_EXACT, SF_MATH_FP32 = 0, 1
-SF_MODE_STREAMED, SF_MODE_MANAGED, SF_MODE_INPLACE = 0, 1, 2
+SF_MODE_STREAMED, SF_MODE_MANAGED, SF_MODE_INPLACE, SF_MODE_MANAGED_MAPPED = 0, 1, 2, 3
 
 
 class SfCellBlock(C.Structure):

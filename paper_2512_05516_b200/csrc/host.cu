@@ -14,6 +14,10 @@
 //                migrated pages, prefetch back.
 //   INPLACE  (2) pinned host AoS, whole records each way (the reference's
 //                run_dev_inplace round trip, inplace_bytes_one_way).
+//   MANAGED_MAPPED (3) cudaMallocManaged AoS kept on the host (preferred
+//                location CPU, accessed-by GPU) and never migrated: the
+//                gather's TMA tiles and the scatter-back read and write the
+//                host pages over PCIe in place.
 //
 // Per chunk on the device: fused gather + first kernel (k_gather_warp) ->
 // further kernels on the SoA -> either the SoA slice to a host SoA buffer
@@ -70,7 +74,8 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
     if (src.layout != Layout::AoS || src.subset.size() != src.schema->fields.size())
         throw std::invalid_argument("run_host expects an AoS view over the full field set");
     if (dst.layout != Layout::SoA) throw std::invalid_argument("run_host computes on an SoA view");
-    if (mode < 0 || mode > 2) throw std::invalid_argument("unknown host orchestration mode");
+    if (mode < 0 || mode > 3) throw std::invalid_argument("unknown host orchestration mode");
+    const bool managed = mode == 1 || mode == 3;
     const std::vector<std::string> ks = split_names(kernels);
     if (ks.empty()) throw std::invalid_argument("no kernels given");
     for (const auto& k : ks)
@@ -97,9 +102,9 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
 
     cudaPointerAttributes attr{};
     check_cuda(cudaPointerGetAttributes(&attr, host), "pointer attributes");
-    if (mode != 1 && attr.type != cudaMemoryTypeHost)
+    if (!managed && attr.type != cudaMemoryTypeHost)
         throw std::invalid_argument("streamed/inplace modes need pinned host memory (sf_b200_host_alloc mode 0)");
-    if (mode == 1 && attr.type != cudaMemoryTypeManaged)
+    if (managed && attr.type != cudaMemoryTypeManaged)
         throw std::invalid_argument("managed mode needs cudaMallocManaged memory (sf_b200_host_alloc mode 1)");
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "device");
@@ -124,7 +129,7 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
             pool->streams.push_back(st);
         }
     }
-    if (mode == 1) {
+    if (managed) {
         const size_t total = size_t((n * rb + 7) / 8);
         check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId), "advise");
         check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetAccessedBy, dev), "advise");
@@ -149,7 +154,7 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
         const size_t off = size_t(r0 * rb / 8);
         const size_t bytes = size_t((cnt * rb + 7) / 8);
         uint8_t* hchunk = static_cast<uint8_t*>(host) + off;
-        void* aos = mode == 1 ? static_cast<void*>(hchunk) : pool->aos[s];
+        void* aos = managed ? static_cast<void*>(hchunk) : pool->aos[s];
         if (mode == 0) {
             check_cuda(cudaMemcpy2DAsync(aos, sbytes, hchunk + soff, rbytes, sbytes, cnt, cudaMemcpyHostToDevice, st),
                        "H2D 2D");
@@ -157,9 +162,11 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
         } else if (mode == 2) {
             check_cuda(cudaMemcpyAsync(aos, hchunk, bytes, cudaMemcpyHostToDevice, st), "H2D");
             h2d += bytes;
-        } else {
+        } else if (mode == 1) {
             check_cuda(cudaMemPrefetchAsync(hchunk, bytes, dev, st), "prefetch");
             h2d += bytes;
+        } else {
+            h2d += bytes;  // MANAGED_MAPPED: no migration, the kernels read the host pages over PCIe
         }
         const View sv = with_count(dev_view, cnt), dv = with_count(dst, cnt);
         gather(sv, aos, dv, pool->soa[s], ks[0].c_str(), dt, math, st);
@@ -185,9 +192,11 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
             } else if (mode == 2) {
                 check_cuda(cudaMemcpyAsync(hchunk, aos, bytes, cudaMemcpyDeviceToHost, st), "D2H");
                 d2h += bytes;
-            } else {
+            } else if (mode == 1) {
                 check_cuda(cudaMemPrefetchAsync(hchunk, bytes, cudaCpuDeviceId, st), "prefetch");
                 d2h += bytes;
+            } else {
+                d2h += bytes;  // written in place through the mapping
             }
         }
     }

@@ -432,13 +432,13 @@ def test_density_buffer_fp64_matches_oracle_random():
 
 
 # ----------------------------------------------------------- host orchestration
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("subset", ["all", "kick"])
 def test_run_host_streamed_managed_inplace(mode, subset):
     n = 100000
     ob, P, _ = default_aos(n=n)
     aos_v = api.View(P, n, "aos")
-    hb = api.HostBuffer(aos_v.nbytes, 1 if mode == 1 else 0)
+    hb = api.HostBuffer(aos_v.nbytes, 1 if mode in (1, 3) else 0)
     hb.numpy()[:] = ob.data
     kernels = "kick,drift" if subset == "all" else "kick"
     dst = api.View(P, n, "soa", None if subset == "all" else "kick", 16)
