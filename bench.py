@@ -167,6 +167,12 @@ def dist_init():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        # SFB_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 over gloo, to exercise the
+        # multi-rank logic on a one-GPU box; production runs are one NCCL rank per GPU
+        if os.environ.get("SFB_BENCH_ONE_DEVICE") == "1":
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            return world, rank, 0
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():

@@ -82,6 +82,11 @@ def neighbour_exchange(send_left: torch.Tensor, send_right: torch.Tensor, rank: 
     (ncclGroupStart; ncclSend/ncclRecv x 4; ncclGroupEnd under NCCL)."""
     import torch.distributed as dist
     dev = send_left.device
+    if dev.type == "cuda" and dist.get_backend(group) == "gloo":
+        # gloo has no point-to-point for CUDA tensors: stage through the host (tests / CPU fallback
+        # of the plumbing only; the NCCL path sends device buffers directly)
+        rl, rr = neighbour_exchange(send_left.cpu(), send_right.cpu(), rank, world, group)
+        return rl.to(dev), rr.to(dev)
     row = tuple(send_left.shape[1:])
     cnt_out = {d: torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
                for d, t in ((-1, send_left), (1, send_right))}
@@ -431,15 +436,29 @@ class ShardedState:
     def view(self, n):
         return self.api.View(self.schema, n, "soa", None, self.prec)
 
+    NAMES = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
+
     def set_fields(self, fields):
         self._binning = None
         n = fields["id"].shape[0]
         self.n = n
         self.buf = self.api.PackedBuffer.empty(self.view(n), self.device)
         for name, t in fields.items():
-            self.stream(name).copy_(t.reshape(self.stream(name).shape).to(self.stream(name).dtype))
+            _, _, w, _ = self.buf.view.lane(name)
+            dt = torch.int64 if name == "id" else FIELD_DTYPES[w]
+            self.stream_bytes(name).copy_(t.to(dt).contiguous().view(torch.uint8).reshape(n, -1))
+
+    def stream_bytes(self, name) -> torch.Tensor:
+        """The field's stream as (n, bytes per particle) uint8 — valid at any
+        offset (the reference SoA packs streams back to back, so e.g. the
+        int64 id stream of an odd particle count is not 8-byte aligned)."""
+        base, stride, w, ar = self.buf.view.lane(name)
+        nbytes = self.n * ar * w // 8
+        return self.buf.data[base // 8: base // 8 + nbytes].view(self.n, ar * w // 8)
 
     def stream(self, name) -> torch.Tensor:
+        """Typed view of a float field's stream (their offsets stay aligned:
+        every stream before them is a multiple of the float width)."""
         base, stride, w, ar = self.buf.view.lane(name)
         dt = torch.int64 if name == "id" else FIELD_DTYPES[w]
         nbytes = self.n * ar * w // 8
@@ -448,21 +467,16 @@ class ShardedState:
 
     def rows(self) -> torch.Tensor:
         """All fields of every particle as one byte row (for migration)."""
-        names = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
-        return torch.cat([self.stream(k).reshape(self.n, -1).view(torch.uint8) for k in names], dim=1)
+        return torch.cat([self.stream_bytes(k) for k in self.NAMES], dim=1)
 
     def from_rows(self, rows: torch.Tensor):
-        names = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
-        widths = {}
-        for k in names:
-            _, _, w, ar = self.buf.view.lane(k)
-            widths[k] = (w // 8) * ar
         n = rows.shape[0]
         fields, c = {}, 0
-        for k in names:
-            b = rows[:, c: c + widths[k]].contiguous()
-            c += widths[k]
+        for k in self.NAMES:
             _, _, w, ar = self.buf.view.lane(k)
+            wb = (w // 8) * ar
+            b = rows[:, c: c + wb].contiguous()
+            c += wb
             dt = torch.int64 if k == "id" else FIELD_DTYPES[w]
             fields[k] = b.view(dt).reshape(n, ar) if ar == 3 else b.view(dt).reshape(n)
         self.set_fields(fields)
@@ -474,10 +488,33 @@ class ShardedState:
         self.api.run_kernel(self.buf, "drift", dt, buffer_size=1)
 
     def migrate(self, group=None):
+        """Particles whose layer left the slab move to the neighbour.  Only the
+        leaving particles are packed into rows and sent; the new SoA buffer is
+        written in one pass per field (kept particles gathered in order, then
+        the received rows) — no full row materialisation of the rank."""
         if self.slab.world == 1:
             return
-        xcol = self.stream("x")[:, 0]
-        self.from_rows(migrate_rows(self.rows(), xcol, self.slab, group))
+        ix = self.slab.layer(self.stream("x")[:, 0])
+        go_l, go_r = ix < self.slab.x0, ix >= self.slab.x1
+        keep = (~(go_l | go_r)).nonzero().squeeze(1)
+        old = {k: self.stream_bytes(k) for k in self.NAMES}
+        pack = lambda idx: torch.cat([old[k][idx] for k in self.NAMES], dim=1)  # noqa: E731
+        rl, rr = neighbour_exchange(pack(go_l.nonzero().squeeze(1)), pack(go_r.nonzero().squeeze(1)),
+                                    self.slab.rank, self.slab.world, group)
+        recv = torch.cat([rl, rr], dim=0)
+        keep_buf = self.buf  # alive until every field is copied out
+        nk = keep.numel()
+        self.n = nk + recv.shape[0]
+        self.buf = self.api.PackedBuffer.empty(self.view(self.n), self.device)
+        self._binning = None
+        c = 0
+        for k in self.NAMES:
+            dst = self.stream_bytes(k)
+            wb = dst.shape[1]
+            torch.index_select(old[k], 0, keep, out=dst[:nk])
+            dst[nk:] = recv[:, c:c + wb]
+            c += wb
+        del keep_buf
 
     def density(self, group=None):
         x, m, h = self.stream("x"), self.stream("m"), self.stream("h")

@@ -262,3 +262,61 @@ def test_peer_blocks_across_processes_cuda_ipc(tmp_path, world):
         own = d["own"]
         assert np.all(np.linalg.norm(d["a"] - wa[own], axis=1) <= 2e-5 * sa[own])
         assert np.all(np.abs(d["du"] - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
+
+
+def _state_worker(rank, world, port, outdir, n, full):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    h, nc, cell = grid_for(n)
+    st = ShardedState(n, Slab(nc, cell, rank, world), prec=32, h=h)
+    for _ in range(3):  # large dt: particles cross slab planes every step
+        if full:
+            st.stream("P").copy_(st.stream("rho") * 0.7)
+            st.full_step(0.02)
+        else:
+            st.step(0.02)
+    if full:  # full_step ends with kick/drift + migration: refresh rho for the final positions
+        st.density()
+    torch.cuda.synchronize()
+    lay = st.slab.layer(st.stream("x")[:, 0])
+    np.savez(os.path.join(outdir, f"s{rank}.npz"), id=st.stream_bytes("id").cpu().numpy().view(np.int64).ravel(),
+             x=st.stream("x").double().cpu().numpy(), rho=st.stream("rho").double().cpu().numpy(),
+             m=st.stream("m").double().cpu().numpy(), h=st.stream("h").double().cpu().numpy(),
+             inside=bool(((lay >= st.slab.x0) & (lay < st.slab.x1)).all()), n=st.n)
+    dist.barrier()
+    st._peer.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_sharded_state_steps_across_processes(tmp_path, full):
+    """ShardedState on 2 ranks sharing one GPU (gloo control, CUDA IPC peer
+    blocks): after steps with migration every particle is owned by exactly one
+    rank, lies in its slab, and the densities equal the global oracle's."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    n, world = 1 << 16, 2
+    mp.spawn(_state_worker, args=(world, port, str(tmp_path), n, full), nprocs=world, join=True)
+    d = [np.load(tmp_path / f"s{r}.npz") for r in range(world)]
+    ids = np.concatenate([q["id"] for q in d])
+    assert sorted(ids.tolist()) == list(range(n))          # conserved, no duplicates
+    assert all(bool(q["inside"]) for q in d)
+    assert sum(int(q["n"]) for q in d) == n and all(0 < int(q["n"]) < n for q in d)
+    x = np.concatenate([q["x"] for q in d])
+    m = np.concatenate([q["m"] for q in d])
+    hh = np.concatenate([q["h"] for q in d])
+    rho = np.concatenate([q["rho"] for q in d])
+    h, nc, cell = grid_for(n)
+    want = O.density_cells(x.reshape(-1), m, hh, 0.0, 1.0, cell)
+    np.testing.assert_allclose(rho, want.astype(np.float32), rtol=2e-5)
