@@ -589,3 +589,64 @@ def test_nan_inf_kick_matches_live_reference(prec):
     got = api.gather_kernel(src, api.View(P, n, "soa", "kick", prec), "kick", 1e-3)
     np.testing.assert_array_equal(host(got), want)
     R.free(h, st, u, nw, so)
+
+
+def _random_schema(rng):
+    """A random record (test_layout_ops.cpp:31-52 / acceptance.cpp:77-100 in
+    spirit): 1-12 fields of f32/f64/i64, arity 1 or 3, some @truncate(7..w)."""
+    fields = []
+    for i in range(int(rng.integers(1, 13))):
+        base = str(rng.choice(["f32", "f64", "i64"]))
+        ar = 3 if rng.random() < 0.3 else 1
+        trunc = 0
+        if base != "i64" and rng.random() < 0.4:
+            trunc = int(rng.integers(7, 33 if base == "f32" else 65))
+        fields.append(O.Field(f"f{i}", base, ar, trunc))
+    names = [f.name for f in fields]
+    k = max(1, len(names) // 2)
+    reads = sorted(rng.choice(names, size=k, replace=False).tolist())
+    writes = [w for w in reads if rng.random() < 0.5 and fields[names.index(w)].base != "i64"] or []
+    return O.Schema("rnd", fields, {"k": (reads, writes)})
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_schemas_match_oracle(seed):
+    """Random schemas x random bit patterns x every precision code, through
+    whichever kernel each plan selects (TMA tiles, many-stream direct loads,
+    typed / sector / generic conversions): bit-exact vs the oracle moves."""
+    rng = np.random.default_rng(9000 + seed)
+    S = _random_schema(rng)
+    n = int(rng.integers(1, 3000))
+    ob = O._alloc(S, n, "aos", list(range(len(S.fields))), [f.fmt(False) for f in S.fields])
+    ob.data[:] = rng.integers(0, 256, ob.data.size, dtype=np.uint8)
+    tail = ob.length_bits % 8
+    if tail:
+        ob.data[-1] &= (1 << tail) - 1
+    P = api.Schema(S.text())
+    assert P.record_bits == S.record_bits
+    src = dev(ob, api.View(P, n, "aos"))
+    codes = [(api.SF_PREC_STORED, lambda f: f.fmt(False)), (api.SF_PREC_NATIVE, lambda f: f.fmt(True)),
+             (16, lambda f: O.NATIVE(16) if f.is_float else O.OR_I64),
+             (api.SF_PREC_BF16, lambda f: O.OR_BF16 if f.is_float else O.OR_I64),
+             (api.SF_PREC_PACKED + 12, lambda f: 12 if f.is_float else O.OR_I64)]
+    for access in (None, "k"):
+        sub = S.subset(access)
+        for code, fmt in codes:
+            fm = [fmt(S.fields[i]) for i in sub]
+            want = O.transform(ob, "soa", subset=sub, fmts=fm)
+            got = api.gather(src, api.View(P, n, "soa", access, code))
+            np.testing.assert_array_equal(host(got), want.data, err_msg=f"{S.text()} access={access} code={code}")
+            if code == api.SF_PREC_STORED and access is None:  # lossless: back to the AoS bit for bit
+                back = api.convert(got, api.View(P, n, "aos"))
+                np.testing.assert_array_equal(host(back), ob.data)
+    # N^T: the access set's write set from a binary16 SoA merged into the stored AoS
+    w = S.kernels["k"][1]
+    if w:
+        sub = S.subset("k")
+        narrowed = O.transform(ob, "soa", subset=sub, fmts=[O.NATIVE(16) if S.fields[i].is_float else O.OR_I64
+                                                              for i in sub])
+        soa = api.gather(src, api.View(P, n, "soa", "k", 16))
+        api.widen_merge(soa, src, "k")
+        merged = copy.deepcopy(ob)
+        O.merge_into(narrowed, merged, w)
+        np.testing.assert_array_equal(host(src), merged.data)
