@@ -119,8 +119,11 @@ SF_API sf_status sf_b200_convert(const sf_view* src, const void* src_dev, const 
 SF_API sf_status sf_b200_scatter_merge(const sf_view* src, const void* src_dev, const sf_view* dst,
                                        void* dst_dev, const char* kernel, void* stream);
 /* run_kernel_chunked (sph.cpp:286-308) on a device buffer in place:
- * kick | drift | density.  density uses contiguous `buffer_size` neighbour
- * buffers with reference semantics; per_access selects Writeback::PerAccess. */
+ * kick | drift | density | force.  density uses contiguous `buffer_size` neighbour
+ * buffers with reference semantics; per_access selects Writeback::PerAccess.
+ * A comma-separated list ("kick,drift") runs the kernels in order, with the
+ * same result as one call per kernel; on a byte-aligned AoS of plain IEEE
+ * lanes the whole list is one pass over the records (k_update_rec_seq). */
 SF_API sf_status sf_b200_run_kernel(const sf_view* view, void* dev, const char* kernel, double dt,
                                     uint64_t buffer_size, int per_access, int math, void* stream);
 

@@ -16,8 +16,12 @@
 //                    any view).  Byte-aligned destinations use plain stores,
 //                    bit-packed ones use 32-bit atomics so neighbouring lanes
 //                    never race.
-//   k_update_soa / k_update_rec(_multi)  in-place kick/drift on SoA streams /
-//                    AoS records with typed vector loads.
+//   k_update_soa     in-place kick/drift on SoA streams, typed vector accesses.
+//   k_update_rec_tile  in-place kick / drift / "kick,drift" on AoS records:
+//                    one TMA bulk copy of the CTA's records into shared
+//                    memory, the ops in order there, 256-bit write-back of
+//                    the chunks holding written bytes (k_update_rec(_multi):
+//                    the per-lane kernels for buffers that do not qualify).
 //   k_density_buffer the reference density (sph.cpp:176-199): one CTA per
 //                    64-particle neighbour buffer, binary64 with separately
 //                    rounded operations, ascending j, self term included.
@@ -1289,6 +1293,107 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
     }
 }
 
+__device__ __forceinline__ LaneFmt ieee_fmt(int b) { return b == B_BF16 ? fmt_bf16() : fmt_native(base_width(b)); }
+
+// NaN / invalid lanes of the sequence kernel: the exact reference rule, out of line.
+__device__ __noinline__ uint64_t axpy_lane_slow(uint64_t xv, int xb, uint64_t yv, int yb, double dt, uint8_t op,
+                                                uint8_t math) {
+    return axpy_lane(xv, ieee_fmt(xb), yv, ieee_fmt(yb), dt, op, math);
+}
+
+// One op of the sequence on one record in shared memory, formats known at
+// compile time: x[l] = Q(Q(x[l]) + Q(y[l]) dt) [max 0]; NaN operands and
+// inf - inf take the exact rule (axpy_lane) out of line.
+template <int XB, int YB, int AR>
+__device__ __forceinline__ void rec_op(uint8_t* xp, const uint8_t* yp, double dt, uint8_t op, uint8_t math) {
+    using TX = typename std::conditional<Ieee<XB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<XB>::w == 32, uint32_t, uint16_t>::type>::type;
+    using TY = typename std::conditional<Ieee<YB>::w == 64, uint64_t,
+                                         typename std::conditional<Ieee<YB>::w == 32, uint32_t, uint16_t>::type>::type;
+    TX* x = reinterpret_cast<TX*>(xp);
+    const TY* y = reinterpret_cast<const TY*>(yp);
+    TX xv[AR], out[AR];
+    TY yv[AR];
+    bool bad = false;
+#pragma unroll
+    for (int l = 0; l < AR; ++l) {
+        xv[l] = x[l], yv[l] = y[l];
+        double v;
+        if (math == MATH_FP64_EXACT) v = __dadd_rn(Ieee<XB>::f64(xv[l]), __dmul_rn(Ieee<YB>::f64(yv[l]), dt));
+        else v = double(__fadd_rn(float(Ieee<XB>::f64(xv[l])), __fmul_rn(float(Ieee<YB>::f64(yv[l])), float(dt))));
+        bad |= Ieee<XB>::nan(xv[l]) | Ieee<YB>::nan(yv[l]) | isnan(v);
+        out[l] = TX(Ieee<XB>::from(op == OP_AXPY_CLAMP0 && v < 0.0 ? 0.0 : v));
+    }
+    if (bad)
+#pragma unroll
+        for (int l = 0; l < AR; ++l) out[l] = TX(axpy_lane_slow(xv[l], XB, yv[l], YB, dt, op, math));
+#pragma unroll
+    for (int l = 0; l < AR; ++l) x[l] = out[l];
+}
+
+// A kernel sequence ("kick,drift": v += a dt, u = max(0, u + du dt), x += v dt;
+// or one kernel) in place on AoS records, one pass: each CTA pulls its R
+// whole records (R * stride bytes) into shared memory with one TMA bulk
+// copy, every thread runs the ops on its record in order there (a later op
+// reads the stored bits an earlier one wrote, exactly like one launch per
+// kernel), and each thread writes back the 32-B chunks that hold its record's
+// written bytes [wlo, whi) with 256-bit stores.  DRAM sees each record once
+// however many kernels run, and no lane is fetched by a scalar global load.
+template <int R>
+__global__ void __launch_bounds__(R) k_update_rec_tile(uint8_t* __restrict__ buf, uint64_t n, uint32_t stride,
+                                                         const __grid_constant__ RecSeq S, double dt, uint8_t math,
+                                                         uint32_t wlo, uint32_t whi) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* tile = smem + 128;
+    const uint64_t r0 = uint64_t(blockIdx.x) * R;
+    const uint32_t nrec = uint32_t(min(uint64_t(R), n - r0));
+    const uint32_t bytes = nrec * stride, bulk = bytes & ~15u;
+    uint8_t* g = buf + r0 * stride;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, bulk);
+        if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
+    }
+    for (uint32_t b = bulk + threadIdx.x; b < bytes; b += R) tile[b] = g[b];  // the <16-B tail
+    __syncthreads();
+    mbar_wait(bar, 0);
+    if (threadIdx.x < nrec) {
+        uint8_t* rec = tile + threadIdx.x * stride;
+#pragma unroll 1
+        for (int o = 0; o < S.n; ++o) {
+            uint8_t* xp = rec + S.xoff[o];
+            const uint8_t* yp = rec + S.yoff[o];
+            switch (S.kind[o]) {  // uniform across the grid: one indirect branch per op
+#define SFB_K(XB, YB)                                                                              \
+    case (XB * 4 + YB) * 2: rec_op<XB, YB, 1>(xp, yp, dt, S.op[o], math); break;                  \
+    case (XB * 4 + YB) * 2 + 1: rec_op<XB, YB, 3>(xp, yp, dt, S.op[o], math); break;
+#define SFB_KY(XB) SFB_K(XB, B_F16) SFB_K(XB, B_BF16) SFB_K(XB, B_F32) SFB_K(XB, B_F64)
+                SFB_KY(B_F16) SFB_KY(B_BF16) SFB_KY(B_F32) SFB_KY(B_F64)
+#undef SFB_KY
+#undef SFB_K
+                default: break;
+            }
+        }
+    }
+    __syncthreads();  // a chunk may hold bytes of the neighbouring records
+    if (threadIdx.x < nrec) {
+        const uint32_t lo = threadIdx.x * stride + wlo, hi = threadIdx.x * stride + whi;
+        for (uint32_t b = lo & ~31u; b < hi; b += 32) {
+            if (b + 32 <= bytes) {
+                const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(tile + b);
+                const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(tile + b + 16);
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(g + b), "l"(p.x), "l"(p.y), "l"(q.x),
+                             "l"(q.y)
+                             : "memory");
+            } else {
+                for (uint32_t e = max(b, lo); e < hi; ++e) g[e] = tile[e];  // the buffer's last chunk
+            }
+        }
+    }
+}
+
 cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate) {
     if (p.count == 0) {
         *degenerate = false;
@@ -1336,6 +1441,28 @@ cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint3
     SFB_M(B_F64, B_F64) SFB_M(B_F32, B_F32) SFB_M(B_F16, B_F16) SFB_M(B_BF16, B_BF16) SFB_M(B_F64, B_F32)
 #undef SFB_M
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_update_rec_tile(void* buf, uint64_t n, uint32_t stride, const RecSeq& seq, double dt,
+                                   uint8_t math, uint32_t wlo, uint32_t whi, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    static const int R = env_int("SFB_REC_TILE_RECS", 128) == 256 ? 256 : 128;  // records (threads) per CTA
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_update_rec_tile<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(128 + 128 * kRecTileMaxStride));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_update_rec_tile<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(128 + 256 * kRecTileMaxStride));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const size_t smem = 128 + size_t(R) * stride;
+    const unsigned blocks = unsigned((n + R - 1) / R);
+    uint8_t* b = static_cast<uint8_t*>(buf);
+    if (R == 128) k_update_rec_tile<128><<<blocks, 128, smem, st>>>(b, n, stride, seq, dt, math, wlo, whi);
+    else k_update_rec_tile<256><<<blocks, 256, smem, st>>>(b, n, stride, seq, dt, math, wlo, whi);
+    return cudaGetLastError();
 }
 
 // x/y bases: BaseKind of plain IEEE lanes; pointers 16-B aligned (caller checks).

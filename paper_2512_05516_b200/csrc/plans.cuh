@@ -84,6 +84,17 @@ struct RecOps {
     int n;
 };
 
+// ---- kernels (kick | drift | kick,drift ...) in place on AoS records ---------
+// Ops run in order per record on the CTA's shared-memory copy of its records.
+constexpr int kMaxSeq = 4;
+constexpr uint32_t kRecTileMaxStride = 384;  // at most 256 records of at most 384 B per CTA (96 KB)
+struct RecSeq {
+    uint32_t xoff[kMaxSeq], yoff[kMaxSeq];
+    uint8_t kind[kMaxSeq];  // (x base * 4 + y base) * 2 + (arity == 3)
+    uint8_t op[kMaxSeq];
+    int n;
+};
+
 // ---- SPH density over 64-particle neighbour buffers (sph.cpp:176-199) -------
 struct DensityPlan {
     Lanes x, m, h, rho;

@@ -1,6 +1,8 @@
 #include "runtime.hpp"
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <stdexcept>
 
 namespace sfb {
@@ -116,10 +118,69 @@ void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, c
     count_launches(1);
 }
 
+namespace {
+// plain IEEE x/y lanes of one op, naturally aligned inside every record
+bool rec_op_ok(const View& v, const CStream& c, const void* p) {
+    const uint64_t rb = v.record_bits();
+    const auto al = [&](const Lanes& L) { return L.base % L.fmt.width == 0 && rb % L.fmt.width == 0; };
+    return fmt_is_ieee(c.dst.fmt) && fmt_is_ieee(c.aux.fmt) && c.dst.arity == c.aux.arity && al(c.dst) &&
+           al(c.aux) && (reinterpret_cast<uintptr_t>(p) & 7) == 0;
+}
+
+// The ops of one or more kick/drift kernels in one shared-memory pass over the
+// AoS records (k_update_rec_tile); false when the layout does not qualify.
+bool rec_tile(const View& v, void* p, const std::vector<CStream>& ops, double dt, uint8_t math, cudaStream_t st) {
+    static const bool on = [] {
+        const char* e = std::getenv("SFB_REC_TILE");
+        return !e || std::atoi(e) != 0;
+    }();
+    const uint64_t stride = v.record_bits() / 8;
+    if (!on || v.layout != Layout::AoS || !v.byte_aligned() || ops.empty() || ops.size() > size_t(kMaxSeq) ||
+        stride == 0 || stride > kRecTileMaxStride || (reinterpret_cast<uintptr_t>(p) & 31) != 0)
+        return false;
+    for (const auto& c : ops)
+        if (!rec_op_ok(v, c, p)) return false;
+    RecSeq q{};
+    q.n = int(ops.size());
+    uint32_t wlo = uint32_t(stride), whi = 0;  // hull of the written bytes inside a record
+    for (int o = 0; o < q.n; ++o) {
+        const CStream& c = ops[o];
+        q.xoff[o] = uint32_t(c.dst.base / 8);
+        q.yoff[o] = uint32_t(c.aux.base / 8);
+        if (c.dst.arity != 1 && c.dst.arity != 3) return false;
+        q.kind[o] = uint8_t((c.dst.fmt.base * 4 + c.aux.fmt.base) * 2 + (c.dst.arity == 3));
+        q.op[o] = c.op;
+        wlo = std::min(wlo, q.xoff[o]);
+        whi = std::max(whi, q.xoff[o] + uint32_t(c.dst.arity * c.dst.fmt.width / 8));
+    }
+    check_cuda(launch_update_rec_tile(p, v.count, uint32_t(stride), q, dt, math, wlo, whi, st), "aos update launch");
+    count_launches(1);
+    return true;
+}
+}  // namespace
+
 void run_kernel(const View& v, void* p, const std::string& kernel, double dt, uint64_t bs, int per_access, int math,
                 cudaStream_t st) {
     require_device();
     check_ptr(p, "buffer");
+    if (kernel.find(',') != std::string::npos) {  // "kick,drift": the kernels in order, one pass where possible
+        const std::vector<std::string> ks = split_names(kernel);
+        if (ks.empty()) throw std::invalid_argument("no kernels given");
+        bool linear = v.layout == Layout::AoS && bs != 0 && v.count % bs == 0;
+        for (const auto& k : ks) linear = linear && (k == "kick" || k == "drift");
+        if (linear) {
+            std::vector<CStream> ops;
+            uint8_t m = 0;
+            for (const auto& k : ks) {
+                const KernelPlan kp = plan_kernel(v, k, dt, math);
+                m = kp.math;
+                for (uint32_t i = 0; i < kp.n; ++i) ops.push_back(kp.s[i]);
+            }
+            if (rec_tile(v, p, ops, dt, m, st)) return;
+        }
+        for (const auto& k : ks) run_kernel(v, p, k, dt, bs, per_access, math, st);
+        return;
+    }
     if (kernel == "density") {
         if (math != MATH_FP64_EXACT) throw std::invalid_argument("buffer-mode density is binary64 (reference semantics)");
         const DensityPlan d = plan_density(v, bs, per_access);
@@ -146,16 +207,11 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
         return;
     }
     const KernelPlan kp = plan_kernel(v, kernel, dt, math);
+    if (v.layout == Layout::AoS && rec_tile(v, p, std::vector<CStream>(kp.s, kp.s + kp.n), dt, kp.math, st)) return;
     if (v.layout == Layout::AoS && v.byte_aligned()) {  // typed per-record lanes when every op is plain IEEE
         bool ok = true;
         const uint64_t rb = v.record_bits();
-        for (uint32_t i = 0; i < kp.n && ok; ++i) {
-            const CStream& c = kp.s[i];
-            const auto al = [&](const Lanes& L) { return L.base % L.fmt.width == 0 && rb % L.fmt.width == 0; };
-            ok = fmt_is_ieee(c.dst.fmt) && fmt_is_ieee(c.aux.fmt) && c.dst.fmt.base != B_INT &&
-                 c.aux.fmt.base != B_INT && c.dst.arity == c.aux.arity && al(c.dst) && al(c.aux) &&
-                 (reinterpret_cast<uintptr_t>(p) & 7) == 0;
-        }
+        for (uint32_t i = 0; i < kp.n && ok; ++i) ok = rec_op_ok(v, kp.s[i], p);
         bool same = ok && kp.n <= 2;
         for (uint32_t i = 1; i < kp.n && same; ++i)
             same = fmt_eq(kp.s[i].dst.fmt, kp.s[0].dst.fmt) && fmt_eq(kp.s[i].aux.fmt, kp.s[0].aux.fmt);

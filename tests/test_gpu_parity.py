@@ -650,3 +650,94 @@ def test_random_schemas_match_oracle(seed):
         merged = copy.deepcopy(ob)
         O.merge_into(narrowed, merged, w)
         np.testing.assert_array_equal(host(src), merged.data)
+
+
+def _salted_default(n, seed):
+    """The default 88-B AoS with NaN / inf / overflow salted into v, u, a, du
+    (and x), so the sequence kernel's exact-rule lanes are exercised."""
+    ob, P, _ = default_aos(n=n, seed=seed)
+    rec = ob.data.reshape(n, 88)
+    f32 = np.float32([np.nan, -np.nan, np.inf, -np.inf, 3e38, -3e38, 1e-45, 0.0, -0.0])
+    f64 = np.float64([np.nan, np.inf, -np.inf, 1.7e308, -0.0])
+    for k in range(0, n, 7):
+        lane = k % 3
+        rec[k, 32 + 4 * lane: 36 + 4 * lane] = f32[k % 9: k % 9 + 1].view(np.uint8)              # v
+        rec[k, 68 + 4 * lane: 72 + 4 * lane] = f32[(k + 3) % 9:(k + 3) % 9 + 1].view(np.uint8)  # a
+        rec[k, 44:48] = f32[(k + 1) % 9:(k + 1) % 9 + 1].view(np.uint8)                          # u
+        rec[k, 80:84] = f32[(k + 5) % 9:(k + 5) % 9 + 1].view(np.uint8)                          # du
+        if k % 3 == 0:
+            rec[k, 8 * lane: 8 * lane + 8] = f64[k % 5: k % 5 + 1].view(np.uint8)                # x
+    return ob, P
+
+
+@pytest.mark.parametrize("prec", [api.SF_PREC_NATIVE, 16, api.SF_PREC_BF16, 32, 12])
+@pytest.mark.parametrize("math", [api.SF_MATH_FP64_EXACT, api.SF_MATH_FP32])
+@pytest.mark.parametrize("seq", ["kick", "drift", "kick,drift", "drift,kick", "kick,kick", "drift,drift,kick",
+                                 "kick,drift,kick"])
+def test_kernel_sequence_on_aos_equals_soa_kernels(prec, math, seq):
+    """run_kernel(seq) in place on an AoS (one shared-memory pass,
+    k_update_rec_tile, for IEEE lanes; the per-kernel loop for bit-packed
+    T=12 or more than kMaxSeq ops) = the same kernels one launch each on the
+    SoA (k_update_soa / k_convert), bit for bit, NaN / inf salted; n is not a
+    multiple of the 256-record tile."""
+    n = 50001
+    ob, P = _salted_default(n, 11)
+    src = dev(ob, api.View(P, n, "aos"))
+    aos = api.convert(src, api.View(P, n, "aos", None, prec))
+    soa = api.gather(src, api.View(P, n, "soa", None, prec))
+    for k in seq.split(","):
+        api.run_kernel(soa, k, 1e-3, buffer_size=1, math=math)
+    api.run_kernel(aos, seq, 1e-3, buffer_size=1, math=math)
+    np.testing.assert_array_equal(host(aos), host(api.convert(soa, aos.view)))
+
+
+@pytest.mark.parametrize("n", [1, 31, 255, 256, 257, 4097])
+def test_kernel_sequence_ragged_tails_and_odd_strides(n):
+    """Tile tails (n % 256), a 52-B record (32-B chunks straddle records, the
+    stride is not a multiple of 8) and a 16-B-aligned buffer (not 32: the
+    per-lane kernels)."""
+    S = O.Schema("s36", [O.Field("x", "f32", 3), O.Field("v", "f32", 3), O.Field("id", "i64"),
+                          O.Field("u", "f32"), O.Field("a", "f32", 3), O.Field("du", "f32")],
+                 {"kick": (["v", "a", "u", "du"], ["v", "u"]), "drift": (["x", "v"], ["x"])})
+    assert S.record_bits == 8 * 52
+    rng = np.random.default_rng(n)
+    ob = O._alloc(S, n, "aos", list(range(len(S.fields))), [f.fmt(False) for f in S.fields])
+    ob.data[:] = rng.integers(0, 256, ob.data.size, dtype=np.uint8)
+    P = api.Schema(S.text())
+    aos = dev(ob, api.View(P, n, "aos"))
+    soa = api.gather(aos, api.View(P, n, "soa"))
+    for k in ("kick", "drift"):
+        api.run_kernel(soa, k, 1e-3, buffer_size=1)
+    want = host(api.convert(soa, aos.view))
+    api.run_kernel(aos, "kick,drift", 1e-3, buffer_size=1)
+    np.testing.assert_array_equal(host(aos), want)
+    # the same records 16 B into a larger allocation: not 32-B aligned
+    raw = torch.zeros(ob.data.size + 64, dtype=torch.uint8, device="cuda")
+    raw[16:16 + ob.data.size] = torch.from_numpy(ob.data).cuda()
+    off = api.PackedBuffer(aos.view, raw[16:16 + ob.data.size])
+    api.run_kernel(off, "kick,drift", 1e-3, buffer_size=1)
+    np.testing.assert_array_equal(host(off), want)
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("prec", [16, 32])
+def test_kernel_sequence_matches_live_reference(prec):
+    """store_state(T) -> unpack -> run_kernel(kick) -> run_kernel(drift) in the
+    reference vs one run_kernel("kick,drift") here, NaN / inf salted."""
+    n = 4096
+    ob, P = _salted_default(n, 5)
+    src = dev(ob, api.View(P, n, "aos"))
+    R = O.RefLib()
+    h = R.L.ref_buf_from_bytes(None, 0, b"", n, O._p(ob.data), ob.data.size)
+    assert h
+    st = R.restore(h, prec)
+    u = R.op(st, "unpack")
+    R.run_kernel(u, "kick", 64, 1e-3)
+    R.run_kernel(u, "drift", 64, 1e-3)
+    want = R.bytes(u)
+    got = api.convert(src, api.View(P, n, "aos", None, prec))
+    api.run_kernel(got, "kick,drift", 1e-3)
+    np.testing.assert_array_equal(host(got), want)
+    R.free(h, st, u)
+    with pytest.raises(Exception):
+        api.run_kernel(got, "kick,drift", 1e-3, buffer_size=3)  # 3 does not divide 4096: rejected like one call
