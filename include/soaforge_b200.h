@@ -151,7 +151,8 @@ typedef struct sf_cell_block {
     const void* pos;            /* float4 (x, y, z, h) per particle, cell-sorted */
     const float* mass;          /* cell-sorted masses */
     const int32_t* cell_start;  /* nx*ny*nz + 1 entries */
-    const uint32_t* hmax;       /* the block's largest h (float bits) */
+    const uint32_t* hmax;       /* h range, 2 words: [0] largest h (float bits), [1] ~bits of the
+                                   smallest h (0 = unknown); equal ends select the uniform-h loop */
     int32_t x0, nx;             /* global x-layers held by the block */
     float x_origin;             /* the lo[0] its binning used (layer x0 starts there) */
     int32_t reserved;           /* 0 */
@@ -159,7 +160,7 @@ typedef struct sf_cell_block {
 #define SF_IPC_HANDLE_BYTES 64
 /* Packs x (3n), m, h (n) in `prec` through perm (sorted position -> particle)
  * into caller-owned pos_out (16*n bytes, 16-B aligned), mass_out (4*n) and
- * hmax_out (one word). */
+ * hmax_out (two words: the h range of sf_cell_block.hmax). */
 SF_API sf_status sf_b200_cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n,
                                     const int32_t* perm, void* pos_out, float* mass_out,
                                     uint32_t* hmax_out, void* stream);
@@ -177,7 +178,7 @@ typedef struct sf_force_block {
     const void* vel;            /* float4 (vx, vy, vz, m) */
     const float* pf;            /* P / rho^2 */
     const int32_t* cell_start;
-    const uint32_t* hmax;
+    const uint32_t* hmax;       /* the density block's h range (2 words) */
     int32_t x0, nx;
     float x_origin;
     int32_t reserved;

@@ -289,7 +289,8 @@ def force_cells(x, v, m, h, rho, P, cell_start, perm, lo, cell: float, dims, n_h
 
 def cells_pack(x, m, h, perm, pos, mass, hmax, prec: int = SF_PREC_NATIVE):
     """Pack x (n,3), m, h (n,) through perm (sorted position -> particle) into
-    caller-owned float4 pos (n,4), mass (n,) and hmax (1 int32 word)."""
+    caller-owned float4 pos (n,4), mass (n,) and hmax (>= 2 int32 words: the h
+    range, [0] bits of the largest h, [1] ~bits of the smallest)."""
     n = m.shape[0]
     check(lib().sf_b200_cells_pack(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
                                    _ptr(pos), _ptr(mass), _ptr(hmax), _stream()))

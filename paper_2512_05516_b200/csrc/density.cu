@@ -43,24 +43,38 @@ __device__ __forceinline__ float ldf(const void* p, uint64_t i) {
     else return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
 }
 
+// The packed block's smoothing-length range: word [0] = bits of the largest h,
+// word [1] = ~bits of the smallest (positive floats order like their bits, so
+// both are atomicMax over words zeroed before the pack).  A word [1] of 0
+// reads as "range unknown" (no uniform-h fast path).
+__device__ __forceinline__ void h_range(float hmax, float hmin, unsigned* __restrict__ words) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, d));
+        hmin = fminf(hmin, __shfl_xor_sync(0xffffffffu, hmin, d));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (hmax > 0.0f) atomicMax(words, __float_as_uint(hmax));
+        if (hmin < __int_as_float(0x7f800000)) atomicMax(words + 1, ~__float_as_uint(fmaxf(hmin, 0.0f)));
+    }
+}
+
 // Stored values are exactly representable in binary32, so the packed
 // float4 record is lossless for every stream precision.
 template <int P>
 __global__ void k_pack(const void* __restrict__ x, const void* __restrict__ m, const void* __restrict__ h,
                        const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ pos,
                        float* __restrict__ mass, unsigned* __restrict__ hmax_bits) {
-    float hmax = 0.0f;
+    float hmax = 0.0f, hmin = __int_as_float(0x7f800000);
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = perm ? uint64_t(perm[k]) : k;
         const float hi = ldf<P>(h, i);
         pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), hi);
         mass[k] = ldf<P>(m, i);
         hmax = fmaxf(hmax, hi);
+        hmin = fminf(hmin, hi);
     }
-    // largest smoothing length (non-negative floats order like their bits)
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, d));
-    if ((threadIdx.x & 31) == 0 && hmax > 0.0f) atomicMax(hmax_bits, __float_as_uint(hmax));
+    h_range(hmax, hmin, hmax_bits);
 }
 
 // M4 cubic spline (sph.cpp:17-24) in binary32; caller guarantees q < 2.
@@ -207,6 +221,36 @@ __device__ __forceinline__ float pair_term(const float4 pi, float hh_i, const fl
     return (mj * (inv_h * inv_h * inv_h)) * w;
 }
 
+// pair_term when every candidate has the home's h (uniform smoothing length,
+// detected per launch from the blocks' h range): h_ij = h, so 1/h_ij and its
+// cube are per-home constants.  The same float operations in the same order
+// as pair_term with h_j = h_i, so the result is bit-identical.
+__device__ __forceinline__ float pair_term_u(const float4 pi, float inv_h, float ih3, const float4 pj, float mj) {
+    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float q = sqrt_approx(r2) * inv_h;
+    const float t = fmaxf(2.0f - q, 0.0f);
+    const float u = fmaxf(1.0f - q, 0.0f);
+    const float w = fmaf(t * t, t, (u * u) * (-4.0f * u));
+    return (mj * ih3) * w;
+}
+
+// The smoothing-length range of the candidate blocks: hmax word [0] = bits of
+// the largest h, word [1] = ~bits of the smallest (0 = unknown: not uniform).
+template <class BS>
+__device__ __forceinline__ bool uniform_h(const BS& B, float* hmax) {
+    float hi = 0.0f, lo = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+        if (g >= B.nb) break;
+        hi = fmaxf(hi, __uint_as_float(B.b[g].hmax[0]));
+        const unsigned w1 = B.b[g].hmax[1];
+        lo = w1 ? fminf(lo, __uint_as_float(~w1)) : 0.0f;
+    }
+    *hmax = hi;
+    return lo == hi && hi > 0.0f;
+}
+
 // Per-particle culled candidate runs.  As k_pairs_r (one thread per home
 // particle, the (2R+1)^2 neighbour columns swept in lockstep so neighbouring
 // lanes share candidate lines in L1), but every column's z-window is cut to
@@ -235,74 +279,86 @@ struct BlockSet {
     int nb, NX;  // blocks in use; global x-layers (faces at 0 and NX)
 };
 
-template <int R>
-__global__ void __launch_bounds__(256) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
-                                                 int64_t n, float* __restrict__ rho) {
+template <int R, bool UNI>
+__device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __restrict__ perm, const CellGrid& G,
+                                           int64_t k, float hmax, float* __restrict__ rho) {
     constexpr int W = 2 * R + 1;
-    float hmax = 0.0f;
-    for (int g = 0; g < B.nb; ++g) hmax = fmaxf(hmax, __uint_as_float(*B.b[g].hmax));
     const float4* __restrict__ hpos = B.b[0].pos;
     const int hx0 = B.b[0].x0, hnx = B.b[0].nx;
     const float hlox = B.b[0].lox;
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i_home = perm ? perm[k] : k;
-        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
-        const float4 pi = hpos[k];
-        // the binning formula of the own block (same origin, same rounding), then global layers
-        const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
-                    fz = (pi.z - G.loz) * G.inv_cell;
-        const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
-        const float fx = fxl + float(hx0);
-        const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
-        const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
-        const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
-        const float rc2 = rc * rc;
-        const float hh_i = 0.5f * pi.w;
-        const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
-        const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
-        float acc = 0.0f;
+    const int64_t i_home = perm ? perm[k] : k;
+    if (i_home >= G.n_home) return;  // ghosts: neighbours only
+    const float4 pi = hpos[k];
+    // the binning formula of the own block (same origin, same rounding), then global layers
+    const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell, fz = (pi.z - G.loz) * G.inv_cell;
+    const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
+    const float fx = fxl + float(hx0);
+    const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
+    const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
+    const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
+    const float rc2 = rc * rc;
+    const float hh_i = 0.5f * pi.w;
+    const float inv_hu = rcp_approx(fmaf(0.5f, pi.w, hh_i));  // UNI: 1/h_ij for every candidate
+    const float ih3 = inv_hu * inv_hu * inv_hu;
+    const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
+    const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
+    float acc = 0.0f;
+    auto term = [&](const float4 pj, float mj) {
+        if constexpr (UNI) return pair_term_u(pi, inv_hu, ih3, pj, mj);
+        else return pair_term(pi, hh_i, pj, mj);
+    };
 #pragma unroll 1
-        for (int dxi = -R; dxi <= R; ++dxi) {
-            const int jx = ix + dxi;
-            if (jx < 0 || jx >= B.NX) continue;
-            int g = 0;
-            while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
-            if (g == B.nb) continue;  // layer held by no block
-            const float4* __restrict__ pos = B.b[g].pos;
-            const float* __restrict__ mass = B.b[g].mass;
-            const int32_t* __restrict__ cell_start = B.b[g].cs;
-            // faces of the global grid extend to infinity (binning clamps)
-            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
-                                    0.0f);
-            int b[W], e[W];
-            const int cx = (jx - B.b[g].x0) * G.ny;  // cell ids fit in int32 (checked on the host)
+    for (int dxi = -R; dxi <= R; ++dxi) {
+        const int jx = ix + dxi;
+        if (jx < 0 || jx >= B.NX) continue;
+        int g = 0;
+        while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
+        if (g == B.nb) continue;  // layer held by no block
+        const float4* __restrict__ pos = B.b[g].pos;
+        const float* __restrict__ mass = B.b[g].mass;
+        const int32_t* __restrict__ cell_start = B.b[g].cs;
+        // faces of the global grid extend to infinity (binning clamps)
+        const float ddx =
+            fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f), 0.0f);
+        int b[W], e[W];
+        const int cx = (jx - B.b[g].x0) * G.ny;  // cell ids fit in int32 (checked on the host)
 #pragma unroll
-            for (int t = 0; t < W; ++t) {
-                const int jy = iy - R + t;
-                const float ddy = fmaxf(
-                    fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
-                const float d2 = fmaf(ddx, ddx, ddy * ddy);
-                const float dz = sqrt_approx(fmaxf(rc2 - d2, 0.0f));  // rel err ~1e-7, inside the margin
-                const int zlo = min(max(int(floorf(fzc - dz)), zmin), G.nz - 1);
-                const int zhi = max(min(int(floorf(fzc + dz)), zmax), 0);
-                const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
-                const int c0 = (cx + (ok ? jy : 0)) * G.nz;
-                b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
-                e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
-            }
-#pragma unroll
-            for (int t = 0; t < W; ++t) {
-                int j = b[t];
-                for (; j + 1 < e[t]; j += 2) {
-                    const float4 p0 = (pos[j]), p1 = (pos[j + 1]);
-                    const float m0 = __ldg(mass + j), m1 = __ldg(mass + j + 1);
-                    acc += pair_term(pi, hh_i, p0, m0);
-                    acc += pair_term(pi, hh_i, p1, m1);
-                }
-                if (j < e[t]) acc += pair_term(pi, hh_i, (pos[j]), __ldg(mass + j));
-            }
+        for (int t = 0; t < W; ++t) {
+            const int jy = iy - R + t;
+            const float ddy =
+                fmaxf(fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
+            const float d2 = fmaf(ddx, ddx, ddy * ddy);
+            const float dz = sqrt_approx(fmaxf(rc2 - d2, 0.0f));  // rel err ~1e-7, inside the margin
+            const int zlo = min(max(int(floorf(fzc - dz)), zmin), G.nz - 1);
+            const int zhi = max(min(int(floorf(fzc + dz)), zmax), 0);
+            const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
+            const int c0 = (cx + (ok ? jy : 0)) * G.nz;
+            b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
+            e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
         }
-        rho[i_home] = acc * 0.079577471545947668f;  // 1 / (4 pi)
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+            int j = b[t];
+            for (; j + 1 < e[t]; j += 2) {
+                const float4 p0 = (pos[j]), p1 = (pos[j + 1]);
+                const float m0 = __ldg(mass + j), m1 = __ldg(mass + j + 1);
+                acc += term(p0, m0);
+                acc += term(p1, m1);
+            }
+            if (j < e[t]) acc += term((pos[j]), __ldg(mass + j));
+        }
+    }
+    rho[i_home] = acc * 0.079577471545947668f;  // 1 / (4 pi)
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+                                                 int64_t n, float* __restrict__ rho) {
+    float hmax;
+    const bool uni = uniform_h(B, &hmax);
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        if (uni) pairs_home<R, true>(B, perm, G, k, hmax, rho);
+        else pairs_home<R, false>(B, perm, G, k, hmax, rho);
     }
 }
 
@@ -336,7 +392,7 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pos), 16 * n, st), "cudaMallocAsync");
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&mass), 4 * n + 16, st), "cudaMallocAsync");
     unsigned* hmax = reinterpret_cast<unsigned*>(mass + n);
-    check_cuda(cudaMemsetAsync(hmax, 0, sizeof(unsigned), st), "memset");
+    check_cuda(cudaMemsetAsync(hmax, 0, 2 * sizeof(unsigned), st), "memset");
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
     const int64_t nn = int64_t(n);
@@ -372,7 +428,7 @@ void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t 
     if (n >= (1ull << 31)) throw std::invalid_argument("cells_pack: n must be < 2^31 per device");
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
     if (sp < 0) throw std::invalid_argument("cells_pack precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
-    check_cuda(cudaMemsetAsync(hmax, 0, sizeof(unsigned), st), "memset");
+    check_cuda(cudaMemsetAsync(hmax, 0, 2 * sizeof(unsigned), st), "memset");
     if (n == 0) return;
     if (reinterpret_cast<uintptr_t>(pos) & 15) throw std::invalid_argument("pos must be 16-byte aligned");
     float4* p4 = static_cast<float4*>(pos);
@@ -428,7 +484,7 @@ __global__ void k_pack_force(const void* __restrict__ x, const void* __restrict_
                              const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ pos,
                              float4* __restrict__ vel, float* __restrict__ pf, unsigned* __restrict__ hmax_bits,
                              unsigned* __restrict__ degenerate) {
-    float hmax = 0.0f;
+    float hmax = 0.0f, hmin = __int_as_float(0x7f800000);
     bool zero = false;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = perm ? uint64_t(perm[k]) : k;
@@ -437,11 +493,10 @@ __global__ void k_pack_force(const void* __restrict__ x, const void* __restrict_
         vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(m, i));
         pf[k] = ldf<P>(pr, i) / (ri * ri);
         hmax = fmaxf(hmax, hi);
+        hmin = fminf(hmin, hi);
         zero |= ri == 0.0f;
     }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, d));
-    if ((threadIdx.x & 31) == 0 && hmax > 0.0f) atomicMax(hmax_bits, __float_as_uint(hmax));
+    h_range(hmax, hmin, hmax_bits);
     if (__any_sync(0xffffffffu, zero) && (threadIdx.x & 31) == 0) atomicOr(degenerate, 1u);
 }
 
@@ -467,97 +522,113 @@ struct ForceBlockSet {
     int nb, NX;
 };
 
+template <int R, int U, bool UNI>
+__device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t* __restrict__ perm, const CellGrid& G,
+                                           int64_t k, float hmax, float* __restrict__ a_out,
+                                           float* __restrict__ du_out) {
+    constexpr int W = 2 * R + 1;
+    const int hx0 = B.b[0].x0, hnx = B.b[0].nx;
+    const float hlox = B.b[0].lox;
+    const int64_t i_home = perm ? perm[k] : k;
+    if (i_home >= G.n_home) return;  // ghosts: neighbours only
+    const float4 pi = B.b[0].pos[k];
+    const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
+                fz = (pi.z - G.loz) * G.inv_cell;
+    const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
+    const float fx = fxl + float(hx0);
+    const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
+    const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
+    const float4 vi = B.b[0].vel[k];
+    const float pfi = B.b[0].pf[k];
+    const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;
+    const float rc2 = rc * rc;
+    const float hh_i = 0.5f * pi.w;
+    const float inv_hu = rcp_approx(fmaf(0.5f, pi.w, hh_i));  // UNI: 1/h_ij for every candidate
+    const float ih4u = (inv_hu * inv_hu) * (inv_hu * inv_hu);
+    const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
+    const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
+    float ax = 0.0f, ay = 0.0f, az = 0.0f, cp = 0.0f;
+#pragma unroll 1
+    for (int dxi = -R; dxi <= R; ++dxi) {
+        const int jx = ix + dxi;
+        if (jx < 0 || jx >= B.NX) continue;
+        int g = 0;
+        while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
+        if (g == B.nb) continue;  // layer held by no block
+        const float4* __restrict__ pos = B.b[g].pos;
+        const float4* __restrict__ vel = B.b[g].vel;
+        const float* __restrict__ pf = B.b[g].pf;
+        const int32_t* __restrict__ cell_start = B.b[g].cs;
+        auto pair = [&](int j) {
+            const float4 pj = pos[j];
+            const float4 vj = vel[j];
+            const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
+            float inv_h, ih4;
+            if constexpr (UNI) {
+                inv_h = inv_hu, ih4 = ih4u;
+            } else {
+                inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
+                const float ih2 = inv_h * inv_h;
+                ih4 = ih2 * ih2;
+            }
+            const float q = (r2 * inv_r) * inv_h;
+            const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
+            const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
+            const float sc = dw * ih4 * inv_r;                    // pi dW/dr / r
+            const float f = vj.w * (pfi + __ldg(pf + j)) * sc;
+            ax = fmaf(f, dx, ax);
+            ay = fmaf(f, dy, ay);
+            az = fmaf(f, dz, az);
+            const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
+            cp = fmaf(vj.w * sc, dvx, cp);
+        };
+        const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
+                                0.0f);
+        int b[W], e[W];
+        const int cx = (jx - B.b[g].x0) * G.ny;
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+            const int jy = iy - R + t;
+            const float ddy = fmaxf(
+                fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
+            const float d2 = fmaf(ddx, ddx, ddy * ddy);
+            const float dzr = sqrt_approx(fmaxf(rc2 - d2, 0.0f));
+            const int zlo = min(max(int(floorf(fzc - dzr)), zmin), G.nz - 1);
+            const int zhi = max(min(int(floorf(fzc + dzr)), zmax), 0);
+            const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
+            const int c0 = (cx + (ok ? jy : 0)) * G.nz;
+            b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
+            e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
+        }
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+            int j = b[t];
+            if constexpr (U == 2) {
+                for (; j + 1 < e[t]; j += 2) {
+                    pair(j);
+                    pair(j + 1);
+                }
+            }
+            for (; j < e[t]; ++j) pair(j);
+        }
+    }
+    constexpr float kInvPi = 0.31830988618379067f;
+    a_out[3 * i_home] = -kInvPi * ax;
+    a_out[3 * i_home + 1] = -kInvPi * ay;
+    a_out[3 * i_home + 2] = -kInvPi * az;
+    du_out[i_home] = pfi * (kInvPi * cp);
+}
+
 template <int R, int U>
 __global__ void __launch_bounds__(256) k_force_c(const ForceBlockSet B, const int32_t* __restrict__ perm, CellGrid G,
                                                  int64_t n, float* __restrict__ a_out, float* __restrict__ du_out) {
-    constexpr int W = 2 * R + 1;
-    float hmax = 0.0f;
-    for (int g = 0; g < B.nb; ++g) hmax = fmaxf(hmax, __uint_as_float(*B.b[g].hmax));
-    const int hx0 = B.b[0].x0, hnx = B.b[0].nx;
-    const float hlox = B.b[0].lox;
+    float hmax;
+    const bool uni = uniform_h(B, &hmax);
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i_home = perm ? perm[k] : k;
-        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
-        const float4 pi = B.b[0].pos[k];
-        const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
-                    fz = (pi.z - G.loz) * G.inv_cell;
-        const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
-        const float fx = fxl + float(hx0);
-        const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
-        const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
-        const float4 vi = B.b[0].vel[k];
-        const float pfi = B.b[0].pf[k];
-        const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;
-        const float rc2 = rc * rc;
-        const float hh_i = 0.5f * pi.w;
-        const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
-        const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
-        float ax = 0.0f, ay = 0.0f, az = 0.0f, cp = 0.0f;
-#pragma unroll 1
-        for (int dxi = -R; dxi <= R; ++dxi) {
-            const int jx = ix + dxi;
-            if (jx < 0 || jx >= B.NX) continue;
-            int g = 0;
-            while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
-            if (g == B.nb) continue;  // layer held by no block
-            const float4* __restrict__ pos = B.b[g].pos;
-            const float4* __restrict__ vel = B.b[g].vel;
-            const float* __restrict__ pf = B.b[g].pf;
-            const int32_t* __restrict__ cell_start = B.b[g].cs;
-            auto pair = [&](int j) {
-                const float4 pj = pos[j];
-                const float4 vj = vel[j];
-                const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
-                const float inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
-                const float q = (r2 * inv_r) * inv_h;
-                const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
-                const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
-                const float ih2 = inv_h * inv_h;
-                const float sc = dw * (ih2 * ih2) * inv_r;           // pi dW/dr / r
-                const float f = vj.w * (pfi + __ldg(pf + j)) * sc;
-                ax = fmaf(f, dx, ax);
-                ay = fmaf(f, dy, ay);
-                az = fmaf(f, dz, az);
-                const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
-                cp = fmaf(vj.w * sc, dvx, cp);
-            };
-            const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
-                                    0.0f);
-            int b[W], e[W];
-            const int cx = (jx - B.b[g].x0) * G.ny;
-#pragma unroll
-            for (int t = 0; t < W; ++t) {
-                const int jy = iy - R + t;
-                const float ddy = fmaxf(
-                    fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
-                const float d2 = fmaf(ddx, ddx, ddy * ddy);
-                const float dzr = sqrt_approx(fmaxf(rc2 - d2, 0.0f));
-                const int zlo = min(max(int(floorf(fzc - dzr)), zmin), G.nz - 1);
-                const int zhi = max(min(int(floorf(fzc + dzr)), zmax), 0);
-                const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
-                const int c0 = (cx + (ok ? jy : 0)) * G.nz;
-                b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
-                e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
-            }
-#pragma unroll
-            for (int t = 0; t < W; ++t) {
-                int j = b[t];
-                if constexpr (U == 2) {
-                    for (; j + 1 < e[t]; j += 2) {
-                        pair(j);
-                        pair(j + 1);
-                    }
-                }
-                for (; j < e[t]; ++j) pair(j);
-            }
-        }
-        constexpr float kInvPi = 0.31830988618379067f;
-        a_out[3 * i_home] = -kInvPi * ax;
-        a_out[3 * i_home + 1] = -kInvPi * ay;
-        a_out[3 * i_home + 2] = -kInvPi * az;
-        du_out[i_home] = pfi * (kInvPi * cp);
+        if (uni) force_home<R, U, true>(B, perm, G, k, hmax, a_out, du_out);
+        else force_home<R, U, false>(B, perm, G, k, hmax, a_out, du_out);
     }
 }
 
@@ -607,14 +678,14 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pos), 32 * n, st), "cudaMallocAsync");
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pf), 4 * n + 16, st), "cudaMallocAsync");
     vel = pos + n;
-    unsigned* words = reinterpret_cast<unsigned*>(pf + n);  // [0] h_max bits, [1] rho == 0 flag
-    check_cuda(cudaMemsetAsync(words, 0, 2 * sizeof(unsigned), st), "memset");
+    unsigned* words = reinterpret_cast<unsigned*>(pf + n);  // [0], [1] h range (h_range), [2] rho == 0 flag
+    check_cuda(cudaMemsetAsync(words, 0, 3 * sizeof(unsigned), st), "memset");
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    if (sp == SP_F32) k_pack_force<SP_F32><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 1);
-    else if (sp == SP_F16) k_pack_force<SP_F16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 1);
-    else k_pack_force<SP_BF16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 1);
+    if (sp == SP_F32) k_pack_force<SP_F32><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 2);
+    else if (sp == SP_F16) k_pack_force<SP_F16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 2);
+    else k_pack_force<SP_BF16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 2);
     unsigned flag = 0;
-    check_cuda(cudaMemcpyAsync(&flag, words + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaMemcpyAsync(&flag, words + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
     check_cuda(cudaStreamSynchronize(st), "sync");
     if (flag) {
         cudaFreeAsync(pos, st);

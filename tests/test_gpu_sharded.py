@@ -320,3 +320,38 @@ def test_sharded_state_steps_across_processes(tmp_path, full):
     h, nc, cell = grid_for(n)
     want = O.density_cells(x.reshape(-1), m, hh, 0.0, 1.0, cell)
     np.testing.assert_allclose(rho, want.astype(np.float32), rtol=2e-5)
+
+
+@pytest.mark.parametrize("refine", [1, 2])
+def test_uniform_h_path_is_bit_identical(refine):
+    """With one smoothing length everywhere the pair loops take the uniform-h
+    path (1/h_ij hoisted per home); zeroing the block's h-range word [1]
+    ("range unknown") forces the general path: rho, a and du agree bit for
+    bit, and both match the oracle."""
+    n = 1 << 14
+    rng = np.random.default_rng(5)
+    x = rng.random((n, 3))
+    h, nc, cell = grid_for(n)
+    hh = np.full(n, h)
+    m = rng.uniform(0.5, 1.5, n) / n
+    S = _slab_blocks(x, m, hh, nc, cell, 1, refine)[0]
+    xt, mt, ht, cs, pos, mass, hmax = S["keep"]
+    assert hmax[0].item() == int(np.float32(h).view(np.int32))
+    assert (~hmax[1].item()) & 0xffffffff == int(np.float32(h).view(np.uint32))
+    args = (n, S["perm"], (0.0, 0.0), cell / refine, nc * refine, nc * refine, nc * refine)
+    fast = api.density_cells_blocks([S["block"]], *args, reach=refine).clone()
+    v = torch.tensor(rng.uniform(-1, 1, (n, 3)), dtype=torch.float32, device="cuda")
+    P = torch.tensor(rng.uniform(0.2, 1.2, n), dtype=torch.float32, device="cuda")
+    vel = torch.empty(n, 4, device="cuda")
+    pf = torch.empty(n, device="cuda")
+    api.force_pack(v, mt, fast[:n].contiguous(), P, S["perm"], vel, pf)
+    fb = api.force_block(pos, vel, pf, cs, hmax, 0, nc * refine, 0.0)
+    fa, fdu = (t.clone() for t in api.force_cells_blocks([fb], *args, reach=refine))
+    hmax[1] = 0  # range unknown: the general path
+    slow = api.density_cells_blocks([S["block"]], *args, reach=refine)
+    sa, sdu = api.force_cells_blocks([fb], *args, reach=refine)
+    assert torch.equal(fast, slow)
+    assert torch.equal(fa, sa) and torch.equal(fdu, sdu)
+    dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
+    want = O.density_cells(dec(x).reshape(-1), dec(m), dec(hh), 0.0, 1.0, cell)
+    np.testing.assert_allclose(fast[:n].double().cpu().numpy(), want, rtol=1e-5)
