@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstdint>
 #include <type_traits>
@@ -1447,15 +1448,19 @@ cudaError_t launch_update_rec_tile(void* buf, uint64_t n, uint32_t stride, const
                                    uint8_t math, uint32_t wlo, uint32_t whi, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     static const int R = env_int("SFB_REC_TILE_RECS", 128) == 256 ? 256 : 128;  // records (threads) per CTA
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_update_rec_tile<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(128 + 128 * kRecTileMaxStride));
+    static std::atomic<uint64_t> attr_done{0};  // per device: the >48 KB shared-memory opt-in
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(k_update_rec_tile<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(128 + 128 * kRecTileMaxStride));
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_update_rec_tile<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(128 + 256 * kRecTileMaxStride));
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr_done.fetch_or(bit, std::memory_order_release);
     }
     const size_t smem = 128 + size_t(R) * stride;
     const unsigned blocks = unsigned((n + R - 1) / R);

@@ -16,32 +16,31 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
+    static const int sms = [] {  // thread-safe one-time init
+        int dev = 0, n = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
     return sms;
 }
 
 void require_device() {
-    static int have = -1;
-    if (have < 0) {
+    static const bool have = [] {  // thread-safe one-time init
         int n = 0;
-        have = (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) ? 1 : 0;
+        const bool any = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
         // Stream-ordered scratch (density_cells) comes from the device's default
         // pool; keep freed blocks cached instead of unmapping them at every
         // synchronize (the default release threshold is 0).
-        for (int d = 0; d < n && have; ++d) {
+        for (int d = 0; d < n && any; ++d) {
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
                 uint64_t keep = ~0ull;
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
             }
         }
-    }
+        return any;
+    }();
     if (!have) throw std::runtime_error("no CUDA device: libsoaforge_b200 runs on the GPU only (no CPU path)");
 }
 
