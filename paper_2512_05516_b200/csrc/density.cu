@@ -2,11 +2,16 @@
 //
 // New algorithm relative to the reference (whose density is all-pairs inside
 // contiguous 64-particle buffers, sph.cpp:176-199).  Particles are counting-
-// sorted into cells (x-major ids, z fastest; bin_particles below).  The pass
+// sorted into cells (x-major ids, z fastest; bin_particles below: k_cell_rank
+// gives every particle its cell and slot with one returning atomic per (warp,
+// cell), a reduce-then-scan turns counts into cell starts, k_place writes the
+// permutation without atomics and k_sort_runs orders each cell by particle
+// index, so the result is deterministic).  The pass
 //
 //   k_pack        applies the sort permutation once and packs each particle
 //                 as a float4 (x, y, z, h) plus its mass (fp16/bf16 stream
-//                 values widen exactly), and finds the largest h;
+//                 values widen exactly), and finds the h range (largest and
+//                 smallest h: equal ends select the uniform-h pair loop);
 //   k_pairs_c     one thread per home particle of the own x-layers (a
 //                 contiguous range of the sorted order): for each of the
 //                 (2R+1)^2 (dx, dy) neighbour columns the cells of one
@@ -14,7 +19,8 @@
 //                 through L1/L2 (neighbouring lanes sweep the same runs in
 //                 lockstep); each window is culled to the support sphere
 //                 h_i + h_max; every candidate runs the same branch-free pair
-//                 term.  rho is stored back in particle (unsorted) order.
+//                 term (1/h_ij hoisted per home when h is uniform).  rho is
+//                 stored back in particle (unsorted) order.
 //
 // With cells of side >= 2h use reach 1 (27 cells); with cells of side >= h
 // reach 2 (125 smaller cells, ~84 after culling).  Pair formula: the
@@ -362,6 +368,11 @@ __global__ void __launch_bounds__(256) k_pairs_c(const BlockSet B, const int32_t
     }
 }
 
+static int env_int_d(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
 static void launch_pairs(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach, float* rho,
                          cudaStream_t st) {
     const unsigned grid = home_grid(uint64_t(n));
@@ -371,10 +382,6 @@ static void launch_pairs(const BlockSet& B, const int32_t* perm, const CellGrid&
     else k_pairs_c<4><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
 }
 
-static int env_int_d(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
                    const int32_t* cell_start, const float* lo, float cell, int nx, int ny, int nz, int reach,
@@ -754,8 +761,13 @@ void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const 
 }
 
 // ------------------------------------------------------------------ binning
-__global__ void k_cell_ids(const float* __restrict__ x, uint64_t n, float lox, float loy, float loz, float inv_cell,
-                           int nx, int ny, int nz, int32_t* __restrict__ cid, int32_t* __restrict__ counts) {
+// Pass 1: cell id of every particle and its slot among the particles of its
+// cell (the value its cell counter had when it arrived: one returning atomic
+// per (warp, cell), lanes of one cell take consecutive slots in lane order).
+__global__ void k_cell_rank(const float* __restrict__ x, uint64_t n, float lox, float loy, float loz, float inv_cell,
+                            int nx, int ny, int nz, int32_t* __restrict__ cid, int32_t* __restrict__ rank,
+                            int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         int cx = int(floorf((x[3 * i] - lox) * inv_cell));
         int cy = int(floorf((x[3 * i + 1] - loy) * inv_cell));
@@ -764,82 +776,109 @@ __global__ void k_cell_ids(const float* __restrict__ x, uint64_t n, float lox, f
         cy = min(max(cy, 0), ny - 1);
         cz = min(max(cz, 0), nz - 1);
         const int c = (cx * ny + cy) * nz + cz;
-        cid[i] = c;
-        // lanes of one cell (cell-sorted input: most of a warp) share one atomic
-        const unsigned peers = __match_any_sync(__activemask(), c);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[c], __popc(peers));
-    }
-}
-
-constexpr int kScanBlock = 1024;
-
-// in-place exclusive scan of each 2*kScanBlock segment; segment totals out
-__global__ void k_scan_segments(int32_t* __restrict__ a, int64_t n, int32_t* __restrict__ totals) {
-    __shared__ int32_t s[2 * kScanBlock];
-    const int64_t seg0 = int64_t(blockIdx.x) * 2 * kScanBlock;
-    const int t = threadIdx.x;
-    for (int k = t; k < 2 * kScanBlock; k += kScanBlock) s[k] = seg0 + k < n ? a[seg0 + k] : 0;
-    __syncthreads();
-    // Blelloch up-sweep / down-sweep
-    int off = 1;
-    for (int d = kScanBlock; d > 0; d >>= 1) {
-        __syncthreads();
-        if (t < d) {
-            const int ai = off * (2 * t + 1) - 1, bi = off * (2 * t + 2) - 1;
-            s[bi] += s[ai];
-        }
-        off <<= 1;
-    }
-    if (t == 0) {
-        totals[blockIdx.x] = s[2 * kScanBlock - 1];
-        s[2 * kScanBlock - 1] = 0;
-    }
-    for (int d = 1; d <= kScanBlock; d <<= 1) {
-        off >>= 1;
-        __syncthreads();
-        if (t < d) {
-            const int ai = off * (2 * t + 1) - 1, bi = off * (2 * t + 2) - 1;
-            const int32_t v = s[ai];
-            s[ai] = s[bi];
-            s[bi] += v;
-        }
-    }
-    __syncthreads();
-    for (int k = t; k < 2 * kScanBlock; k += kScanBlock)
-        if (seg0 + k < n) a[seg0 + k] = s[k];
-}
-
-__global__ void k_add_offsets(int32_t* __restrict__ a, int64_t n, const int32_t* __restrict__ offs) {
-    const int64_t seg = blockIdx.x;
-    const int32_t o = offs[seg];
-    for (int64_t k = seg * 2 * kScanBlock + threadIdx.x; k < min(n, (seg + 1) * 2 * kScanBlock); k += blockDim.x)
-        a[k] += o;
-}
-
-static void exclusive_scan(int32_t* a, int64_t n, int32_t* scratch, cudaStream_t st) {
-    const int64_t segs = (n + 2 * kScanBlock - 1) / (2 * kScanBlock);
-    k_scan_segments<<<unsigned(segs), kScanBlock, 0, st>>>(a, n, scratch);
-    count_launches(1);
-    if (segs > 1) {
-        exclusive_scan(scratch, segs, scratch + ((segs + 15) / 16) * 16, st);
-        k_add_offsets<<<unsigned(segs), 256, 0, st>>>(a, n, scratch);
-        count_launches(1);
-    }
-}
-
-__global__ void k_place(const int32_t* __restrict__ cid, uint64_t n, const int32_t* __restrict__ start,
-                        int32_t* __restrict__ fill, int32_t* __restrict__ perm) {
-    const int lane = threadIdx.x & 31;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        const int c = cid[i];
-        // one atomic per (warp, cell); lanes take consecutive slots in lane order
         const unsigned peers = __match_any_sync(__activemask(), c);
         const int leader = __ffs(peers) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(&fill[c], __popc(peers));
+        if (lane == leader) base = atomicAdd(&counts[c], __popc(peers));
         base = __shfl_sync(peers, base, leader);
-        perm[start[c] + base + __popc(peers & ((1u << lane) - 1))] = int32_t(i);
+        cid[i] = c;
+        rank[i] = base + __popc(peers & ((1u << lane) - 1));
     }
+}
+
+// Exclusive scan, reduce-then-scan over tiles of kScanTile ints: per-tile
+// sums, a scan of the sums (recursively), then each tile scanned in shared
+// memory (coalesced striped loads/stores, 16 consecutive values per thread,
+// warp-shuffle scan of the thread totals) with its tile offset added.
+constexpr int kScanT = 256, kScanV = 16, kScanTile = kScanT * kScanV;
+
+__device__ __forceinline__ int block_exclusive_sum(int v, int* warp_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < kScanT / 32 ? warp_tot[lane] : 0, wi = w;
+#pragma unroll
+        for (int d = 1; d < kScanT / 32; d <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wi, d);
+            if (lane >= d) wi += t;
+        }
+        if (lane < kScanT / 32) warp_tot[lane] = wi - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    return warp_tot[warp] + inc - v;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_reduce(const int32_t* __restrict__ a, int64_t n,
+                                                        int32_t* __restrict__ partial) {
+    __shared__ int warp_tot[kScanT / 32];
+    const int64_t base = int64_t(blockIdx.x) * kScanTile;
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) {
+        const int64_t i = base + k * kScanT + threadIdx.x;
+        if (i < n) sum += a[i];
+    }
+    const int excl = block_exclusive_sum(sum, warp_tot);
+    if (threadIdx.x == kScanT - 1) partial[blockIdx.x] = excl + sum;
+}
+
+__global__ void __launch_bounds__(kScanT) k_scan_apply(int32_t* __restrict__ a, int64_t n,
+                                                       const int32_t* __restrict__ offs) {
+    __shared__ int sm[kScanTile + kScanTile / 32];
+    __shared__ int warp_tot[kScanT / 32];
+    const int64_t base = int64_t(blockIdx.x) * kScanTile;
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) {
+        const int i = k * kScanT + t;
+        sm[i + (i >> 5)] = base + i < n ? a[base + i] : 0;
+    }
+    __syncthreads();
+    int v[kScanV], tot = 0;
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) {
+        const int i = t * kScanV + k;
+        v[k] = tot;
+        tot += sm[i + (i >> 5)];
+    }
+    const int excl = block_exclusive_sum(tot, warp_tot) + (offs ? offs[blockIdx.x] : 0);
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) {
+        const int i = t * kScanV + k;
+        sm[i + (i >> 5)] = v[k] + excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) {
+        const int i = k * kScanT + t;
+        if (base + i < n) a[base + i] = sm[i + (i >> 5)];
+    }
+}
+
+// scratch: >= ceil(n / kScanTile) ints, plus the same again for every level above
+static void exclusive_scan(int32_t* a, int64_t n, int32_t* scratch, cudaStream_t st) {
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles > 1) {
+        k_scan_reduce<<<unsigned(tiles), kScanT, 0, st>>>(a, n, scratch);
+        exclusive_scan(scratch, tiles, scratch + ((tiles + 63) / 64) * 64, st);
+        count_launches(1);
+    }
+    k_scan_apply<<<unsigned(tiles), kScanT, 0, st>>>(a, n, tiles > 1 ? scratch : nullptr);
+    count_launches(1);
+}
+
+// Pass 2: every particle to its slot, no atomics.
+__global__ void k_place(const int32_t* __restrict__ cid, const int32_t* __restrict__ rank, uint64_t n,
+                        const int32_t* __restrict__ start, int32_t* __restrict__ perm) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        perm[start[cid[i]] + rank[i]] = int32_t(i);
 }
 
 // Sort a run of <= N particle indices in registers: fully unrolled
@@ -881,8 +920,8 @@ __global__ void k_sort_runs(const int32_t* __restrict__ start, int64_t ncell, in
 
 uint64_t bin_scratch_bytes(uint64_t n, int nx, int ny, int nz) {
     const uint64_t ncell = uint64_t(nx) * ny * nz;
-    // cid[n] + fill[ncell] + scan scratch (< ncell/1024 * 2 levels, padded)
-    return 4 * (n + ncell + 2 * (ncell / 1024 + 64)) + 256;
+    // cid[n] + rank[n] + scan partials (ncell / 4096 per level, 64-int padded)
+    return 4 * (2 * n + 2 * (ncell / kScanTile + 64) + 64) + 256;
 }
 
 void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int nx, int ny, int nz,
@@ -893,20 +932,19 @@ void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int 
     if (ncell <= 0 || ncell >= (1ll << 31)) throw std::invalid_argument("bad cell grid");
     if (scratch_bytes < bin_scratch_bytes(n, nx, ny, nz)) throw std::invalid_argument("bin scratch too small");
     int32_t* cid = static_cast<int32_t*>(scratch);
-    int32_t* fill = cid + n;
-    int32_t* scan_tmp = fill + ncell;
+    int32_t* rank = cid + n;
+    int32_t* scan_tmp = rank + ((n + 63) / 64) * 64;
     check_cuda(cudaMemsetAsync(cell_start, 0, sizeof(int32_t) * (ncell + 1), st), "memset");
-    check_cuda(cudaMemsetAsync(fill, 0, sizeof(int32_t) * ncell, st), "memset");
     // uncapped grids: the CTAs in flight touch one compact range of particles
     // (and, for cell-sorted input, of cells)
     const unsigned blocks = unsigned((n + 255) / 256);
     if (n) {
-        k_cell_ids<<<blocks, 256, 0, st>>>(x, n, lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, cid, cell_start);
+        k_cell_rank<<<blocks, 256, 0, st>>>(x, n, lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, cid, rank, cell_start);
         count_launches(1);
     }
     exclusive_scan(cell_start, ncell + 1, scan_tmp, st);  // counts -> starts (last entry = n)
     if (n) {
-        k_place<<<blocks, 256, 0, st>>>(cid, n, cell_start, fill, perm);
+        k_place<<<blocks, 256, 0, st>>>(cid, rank, n, cell_start, perm);
         k_sort_runs<<<unsigned((ncell + 255) / 256), 256, 0, st>>>(cell_start, ncell, perm);
         count_launches(2);
     }

@@ -741,3 +741,26 @@ def test_kernel_sequence_matches_live_reference(prec):
     R.free(h, st, u)
     with pytest.raises(Exception):
         api.run_kernel(got, "kick,drift", 1e-3, buffer_size=3)  # 3 does not divide 4096: rejected like one call
+
+
+@pytest.mark.parametrize("n,dims", [(0, (3, 4, 5)), (1, (2, 2, 2)), (5000, (7, 9, 11)), (1 << 20, (100, 100, 100)),
+                                    (1 << 20, (260, 260, 260))])
+def test_bin_particles_is_a_stable_counting_sort(n, dims):
+    """cell_start / perm equal numpy's stable argsort of the x-major cell ids
+    (same binary32 formula, clamped at the faces), incl. particles outside the
+    grid; the 260^3 grid takes the scan's two-level recursion (> 4096 tiles)."""
+    rng = np.random.default_rng(n + dims[0])
+    lo = np.float32([-0.1, 0.05, 0.0])
+    cell = 1.1 / max(dims)
+    x = (rng.random((n, 3)) * 1.3 - 0.15).astype(np.float32)
+    if n > 100:
+        x[:n // 2] = np.sort(x[:n // 2], axis=0)  # half nearly cell-ordered, half random
+    inv = np.float32(1.0) / np.float32(cell)
+    c = [np.clip(np.floor((x[:, a] - lo[a]) * inv).astype(np.int64), 0, dims[a] - 1) for a in range(3)]
+    cid = (c[0] * dims[1] + c[1]) * dims[2] + c[2]
+    want_perm = np.argsort(cid, kind="stable")
+    want_start = np.searchsorted(cid[want_perm], np.arange(np.prod(dims) + 1), side="left")
+    xt = torch.tensor(x, device="cuda").reshape(max(n, 0), 3)
+    cs, perm = api.bin_particles(xt, tuple(float(v) for v in lo), cell, dims)
+    np.testing.assert_array_equal(cs.cpu().numpy(), want_start)
+    np.testing.assert_array_equal(perm[:n].cpu().numpy(), want_perm)
