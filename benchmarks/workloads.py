@@ -234,7 +234,7 @@ def c4(args, peak, peak_kind):
     best = out["drift:" + best_mode]
     return {"value": best["value"], "ms_per_step": best["ms"],
             "roofline": {"bound": "pcie", "achieved": best["pcie_GBps"], "peak": None, "unit": "GB/s",
-                         "frac": None, "kernel": "run_host %s (k_gather_warp + scatter-merge, 3-stream chunk ring)" % best_mode},
+                         "frac": None, "kernel": "run_host %s (k_gather_multi + scatter-merge, 3-stream chunk ring)" % best_mode},
             "config": {"workload": "C4 (BASELINE configs[3]): 64M host-resident particles, streamed vs managed "
                                    "vs in-place, one drift and one kick+drift step (gather, compute, scatter-back)",
                        "particles": n, "chunk": args.chunk, "soa_precision": "binary16",

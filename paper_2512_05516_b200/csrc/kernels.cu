@@ -1,13 +1,17 @@
 // sm_100a kernels for the AoS<->SoA + reduced-precision SPH hot path.
 //
-//   k_gather_warp    AoS -> SoA (U∘N∘C plus narrowing), optionally fused with
-//                    kick/drift.  Persistent warps; record tiles staged into
+//   k_gather_warp    AoS -> SoA (U∘N∘C plus narrowing) for bit-packed /
+//                    truncated lanes, optionally fused with kick/drift.
+//                    Persistent warps; record tiles staged into
 //                    shared memory by per-warp 1-D TMA bulk copies (cp.async.bulk,
 //                    UBLKCP) through an mbarrier ring; lanes extracted with
 //                    funnel shifts (any bit offset/width); 16-B SoA stores.
-//   k_gather_multi   AoS -> SoA plans of many thin 16/32/64-bit streams (full
-//                    record, kick / density sets, gather fused with kick):
-//                    thread per record, direct typed loads.
+//   k_gather_multi   AoS -> SoA for every plan of plain 16/32/64-bit lanes
+//                    (the C2 drift set fused with drift, full records, kick /
+//                    density sets): each CTA pulls its 256 records into shared
+//                    memory with one TMA bulk copy, then one thread per record
+//                    converts every stream from there (staged; the direct
+//                    typed-load variant remains for unaligned sources).
 //   k_convert_ieee   one COPY stream between IEEE lanes, typed; and
 //   k_scatter_sectors  8-B lanes into wide records by whole-sector
 //                    read-patch-write (256-bit accesses): the scatter-back.
@@ -539,11 +543,15 @@ __device__ __forceinline__ void multi_axpy(const uint8_t* __restrict__ s, const 
     }
 }
 
+// STAGED: each CTA first pulls its 256 whole records into shared memory with
+// one TMA bulk copy, and the lanes are read from there: one L1 wavefront per
+// lane load instead of one sector request per lane per record through the
+// LSU (which bounds the direct version at ~4.6 TB/s on the full record).
+template <bool STAGED>
 __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ GatherPlan P, const uint8_t* __restrict__ src,
                                                       uint8_t* __restrict__ dst) {
     const uint64_t n = P.count, rbytes = P.record_bits >> 3;
-    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x) {
-        const uint8_t* rec = src + r * rbytes;
+    auto body = [&](const uint64_t r, const uint8_t* __restrict__ rec) {
         // the host orders the streams by kind: one dispatch per run of equal kinds
         for (uint32_t q0 = 0; q0 < P.n;) {
             const uint8_t kind = P.s[q0].mkind;
@@ -589,6 +597,28 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
 #undef SFB_EACH
             q0 = q1;
         }
+    };
+    if constexpr (STAGED) {
+        extern __shared__ __align__(128) uint8_t smem[];
+        uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+        uint8_t* tile = smem + 128;
+        const uint64_t r0 = uint64_t(blockIdx.x) * 256;
+        const uint32_t nrec = uint32_t(min(uint64_t(256), n - r0));
+        const uint32_t bytes = uint32_t(nrec * rbytes), bulk = bytes & ~15u;
+        const uint8_t* g = src + r0 * rbytes;
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(bar, bulk);
+            if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
+        }
+        for (uint32_t b = bulk + threadIdx.x; b < bytes; b += 256) tile[b] = g[b];  // the <16-B tail
+        __syncthreads();
+        mbar_wait(bar, 0);
+        if (threadIdx.x < nrec) body(r0 + threadIdx.x, tile + threadIdx.x * rbytes);
+    } else {
+        for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x)
+            body(r, src + r * rbytes);
     }
 }
 
@@ -1272,7 +1302,9 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
         return cudaGetLastError();
     };
     // many thin COPY streams: direct typed loads, one thread per record
-    if (p.proc != PROC_XV_F16 && p.proc != PROC_XV_BF16 && p.proc != PROC_XV_F32 && p.n >= 3 &&
+    static const int min_streams = env_int("SFB_GATHER_MULTI_MIN", 1);  // tuning override (3: thin plans via TMA tiles)
+    const bool xv = p.proc == PROC_XV_F16 || p.proc == PROC_XV_BF16 || p.proc == PROC_XV_F32;
+    if ((min_streams <= 1 || (!xv && int(p.n) >= min_streams)) &&
         env_int("SFB_GATHER_MULTI", 1) && (reinterpret_cast<uintptr_t>(src) & 7) == 0 &&
         (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
         bool ok = true;
@@ -1282,7 +1314,17 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
         if (ok) {
             // one thread per record, uncapped grid: CTAs in flight cover one compact record range
             const int mb = int((p.count + 255) / 256);
-            k_gather_multi<<<mb, 256, 0, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst));
+            const size_t rbytes = p.record_bits / 8, smem = 128 + 256 * rbytes;
+            if (p.record_bits % 8 == 0 && rbytes <= kRecTileMaxStride && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                env_int("SFB_GATHER_MULTI_STAGED", 1)) {
+                cudaError_t e = cudaFuncSetAttribute(k_gather_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     int(smem));
+                if (e != cudaSuccess) return e;
+                k_gather_multi<true><<<mb, 256, smem, st>>>(p, static_cast<const uint8_t*>(src),
+                                                            static_cast<uint8_t*>(dst));
+            } else {
+                k_gather_multi<false><<<mb, 256, 0, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst));
+            }
             return cudaGetLastError();
         }
     }
