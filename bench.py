@@ -311,9 +311,10 @@ def b200_arm(args):
         s_ms = sa.elapsed_time(sb) / reps
         scatter = {"ms": s_ms, "value": n / (s_ms * 1e-3), "algorithmic_bytes_per_particle": 30,
                    "achieved_GBps": 30 * n / (s_ms * 1e-3) / 1e9, "frac": 30 * n / (s_ms * 1e-3) / 1e9 / peak,
-                   "kernel": "k_scatter_sectors (SoA binary16 x -> AoS f64 x lanes, whole-sector read-patch-write)",
-                   "note": "the 24-B x lanes of an 88-B record straddle 32-B sectors, so HBM also reads the "
-                           "sectors' other bytes (partial-sector writes)"}
+                   "kernel": "k_scatter_tile (records staged by one TMA bulk copy, binary16 x widened into the f64 "
+                             "x lanes in shared memory, 256-bit write-back of the chunks holding x)",
+                   "note": "the 24-B x lanes of an 88-B record straddle 32-B sectors and DRAM fetches >= 64 B, "
+                           "so the whole record is read and 1-2 whole chunks written per record"}
         del tgt
 
     # end to end through the C ABI: pinned host AoS in, host SoA out

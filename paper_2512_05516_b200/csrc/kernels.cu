@@ -12,9 +12,14 @@
 //                    memory with one TMA bulk copy, then one thread per record
 //                    converts every stream from there (staged; the direct
 //                    typed-load variant remains for unaligned sources).
+//   k_scatter_tile   SoA -> AoS merge of a write set (the scatter-back):
+//                    the CTA's records staged by one TMA bulk copy, every
+//                    stream converted into them in shared memory, 256-bit
+//                    write-back of the chunks holding written bytes.
 //   k_convert_ieee   one COPY stream between IEEE lanes, typed; and
 //   k_scatter_sectors  8-B lanes into wide records by whole-sector
-//                    read-patch-write (256-bit accesses): the scatter-back.
+//                    read-patch-write (256-bit accesses) when the staged
+//                    kernel does not apply (destination not 32-B aligned).
 //   k_convert        generic lane-by-lane conversion between any two views
 //                    (truncated / bit-packed lanes, in-place kick/drift on
 //                    any view).  Byte-aligned destinations use plain stores,
@@ -620,6 +625,130 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
         for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x)
             body(r, src + r * rbytes);
     }
+}
+
+// ----------------------------------------------------------------- k_scatter_tile
+// SoA -> AoS merge of a write set (widen_merge / scatter-back) into records
+// that already hold the other fields: each CTA pulls its R whole records into
+// shared memory with one TMA bulk copy, every thread converts each stream's
+// lanes of its record from the SoA (lane-consecutive loads) into the staged
+// record, and writes back the 32-B chunks holding the written bytes
+// [wlo, whi) with 256-bit stores.  One pass over the records for any number
+// of streams; no partially written sector reaches L2.
+struct ScatterKinds {
+    uint8_t k[kMaxStreams];  // 1 + 4*src + dst over {F16, BF16, F32, F64}; 17/18/19 raw 16/32/64-bit
+};
+
+template <int R>
+__global__ void __launch_bounds__(R) k_scatter_tile(const __grid_constant__ ConvertPlan P,
+                                                    const __grid_constant__ ScatterKinds K,
+                                                    const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                    uint32_t stride, uint32_t wlo, uint32_t whi, int full) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* tile = smem + 128;
+    const uint64_t n = P.count, r0 = uint64_t(blockIdx.x) * R;
+    const uint32_t nrec = uint32_t(min(uint64_t(R), n - r0));
+    const uint32_t bytes = full ? 0 : nrec * stride, bulk = bytes & ~15u;  // full: every byte is rewritten
+    uint8_t* g = dst + r0 * stride;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, bulk);
+        if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
+    }
+    for (uint32_t b = bulk + threadIdx.x; b < bytes; b += R) tile[b] = g[b];  // the <16-B tail
+    __syncthreads();
+    mbar_wait(bar, 0);
+    if (threadIdx.x < nrec) {
+        const uint64_t r = r0 + threadIdx.x;
+        uint8_t* rec = tile + threadIdx.x * stride;
+        for (uint32_t q = 0; q < P.n; ++q) {
+            const CStream& c = P.s[q];
+            const int ar = c.src.arity;
+            const uint8_t* sp = src + (c.src.base + r * c.src.stride) / 8;
+            uint8_t* dp = rec + c.dst.base / 8;
+            switch (K.k[q]) {
+#define SFB_M(SI, SB, DI, DB) \
+    case 1 + 4 * SI + DI: multi_lanes<SB, DB>(sp, dp, ar); break;
+#define SFB_MS(SI, SB) SFB_M(SI, SB, 0, B_F16) SFB_M(SI, SB, 1, B_BF16) SFB_M(SI, SB, 2, B_F32) SFB_M(SI, SB, 3, B_F64)
+                SFB_MS(0, B_F16)
+                SFB_MS(1, B_BF16)
+                SFB_MS(2, B_F32)
+                SFB_MS(3, B_F64)
+#undef SFB_MS
+#undef SFB_M
+                case 17: multi_raw<uint16_t>(sp, dp, ar); break;
+                case 18: multi_raw<uint32_t>(sp, dp, ar); break;
+                case 19: multi_raw<uint64_t>(sp, dp, ar); break;
+                default: break;
+            }
+        }
+    }
+    __syncthreads();  // a chunk may hold bytes of the neighbouring records
+    if (threadIdx.x < nrec) {
+        const uint32_t lo = threadIdx.x * stride + wlo, hi = threadIdx.x * stride + whi, end = nrec * stride;
+        for (uint32_t b = lo & ~31u; b < hi; b += 32) {
+            if (b + 32 <= end) {
+                const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(tile + b);
+                const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(tile + b + 16);
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(g + b), "l"(p.x), "l"(p.y), "l"(q.x),
+                             "l"(q.y)
+                             : "memory");
+            } else {
+                for (uint32_t e = max(b, lo); e < hi; ++e) g[e] = tile[e];  // the buffer's last chunk
+            }
+        }
+    }
+}
+
+// The k_scatter_tile kind of a COPY stream into an AoS record, 0 if it cannot take it.
+static uint8_t scatter_kind(const CStream& c) {
+    if (c.op != OP_COPY || c.src.arity != c.dst.arity || c.src.arity < 1) return 0;
+    const uint32_t ws = c.src.fmt.width, wd = c.dst.fmt.width;
+    if ((ws != 16 && ws != 32 && ws != 64) || (wd != 16 && wd != 32 && wd != 64)) return 0;
+    if ((c.src.base | c.src.stride) % ws || (c.dst.base | c.dst.stride) % wd) return 0;
+    if (ws == wd && (fmt_eq(c.src.fmt, c.dst.fmt) || c.src.fmt.base == B_INT || c.dst.fmt.base == B_INT)) {
+        if (!fmt_eq(c.src.fmt, c.dst.fmt)) return 0;
+        return ws == 16 ? 17 : ws == 32 ? 18 : 19;
+    }
+    const int si = ieee_code(c.src.fmt), di = ieee_code(c.dst.fmt);
+    if (si < 0 || di < 0) return 0;
+    auto idx = [](int b) { return b == B_F16 ? 0 : b == B_BF16 ? 1 : b == B_F32 ? 2 : 3; };
+    return uint8_t(1 + 4 * idx(si) + idx(di));
+}
+
+// k_scatter_tile for a plan whose destination is one AoS record layout (every
+// stream inside the same record stride); false when it does not qualify.
+static bool launch_scatter_tile(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st, cudaError_t* err) {
+    if (!env_int("SFB_SCATTER_TILE", 1) || src == dst || p.n == 0 || (reinterpret_cast<uintptr_t>(dst) & 31) ||
+        (reinterpret_cast<uintptr_t>(src) & 7))
+        return false;
+    const uint64_t S = p.s[0].dst.stride;
+    if (S % 8 || S / 8 == 0 || S / 8 > kRecTileMaxStride) return false;
+    ScatterKinds K{};
+    uint32_t wlo = uint32_t(S / 8), whi = 0;
+    uint64_t written = 0;
+    for (uint32_t i = 0; i < p.n; ++i) {
+        const CStream& c = p.s[i];
+        const uint64_t span = uint64_t(c.dst.arity) * c.dst.fmt.width;
+        if (c.dst.stride != S || c.dst.base + span > S || c.dst.base % 8) return false;  // not one AoS record
+        if (!(K.k[i] = scatter_kind(c))) return false;
+        wlo = std::min(wlo, uint32_t(c.dst.base / 8));
+        whi = std::max(whi, uint32_t((c.dst.base + span) / 8));
+        written += span;  // streams of one plan never overlap
+    }
+    const int full = written == S;  // every byte rewritten: no need to read the old records
+    constexpr int R = 128;
+    const size_t smem = 128 + size_t(R) * (S / 8);
+    cudaError_t e = cudaFuncSetAttribute(k_scatter_tile<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e == cudaSuccess) {
+        k_scatter_tile<R><<<unsigned((p.count + R - 1) / R), R, smem, st>>>(
+            p, K, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), uint32_t(S / 8), wlo, whi, full);
+        e = cudaGetLastError();
+    }
+    *err = e;
+    return true;
 }
 
 // the k_gather_multi kind of a stream, 0 when it cannot take it
@@ -1248,6 +1377,8 @@ __global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf
 
 cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st) {
     if (p.count == 0 || p.n == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    if (launch_scatter_tile(p, src, dst, st, &err)) return err;  // into AoS records: one staged pass
     bool typed = env_int("SFB_CONVERT_TYPED", 1) != 0;
     for (uint32_t i = 0; i < p.n && typed; ++i) typed = convert_ieee_ok(p.s[i], src, dst);
     if (typed && src != dst) {  // per stream; in place (src == dst) keeps the one-pass generic kernel

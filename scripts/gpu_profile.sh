@@ -7,7 +7,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --cs
 echo "launches $?"
 timeout 900 $NCU -k regex:k_gather_multi -s 5 -c 1 -o gpurun_out/prof_gather python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_gather.log 2>&1
 echo "gather $?"
-timeout 900 $NCU -k regex:k_scatter_sectors -s 3 -c 1 -o gpurun_out/prof_scatter python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_scatter.log 2>&1
+timeout 900 $NCU -k regex:k_scatter_tile -s 3 -c 1 -o gpurun_out/prof_scatter python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_scatter.log 2>&1
 echo "scatter $?"
 timeout 900 $NCU -k regex:k_gather_multi -s 3 -c 1 -o gpurun_out/prof_gather_multi python scripts/probe_gather_one.py all > gpurun_out/ncu_gmulti.log 2>&1
 echo "gather_multi $?"
