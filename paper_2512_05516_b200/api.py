@@ -309,7 +309,8 @@ def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: in
     candidates from every block (own slab + neighbouring slabs in place)."""
     import torch
     n_home = n if n_home is None else n_home
-    rho = rho if rho is not None else torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+    alloc = torch.empty if n_home == n else torch.zeros  # entries past n_home are not written
+    rho = rho if rho is not None else alloc(max(n, 1), dtype=torch.float32, device="cuda")
     arr = (L.SfCellBlock * len(blocks))(*blocks)
     lo_arr = (C.c_float * 2)(*[float(t) for t in lo_yz])
     check(lib().sf_b200_density_cells_blocks(C.cast(arr, C.c_void_p), len(blocks), n,
@@ -338,8 +339,9 @@ def force_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int,
     candidates from every block; returns (a (n,3), du (n,))."""
     import torch
     n_home = n if n_home is None else n_home
-    a = a if a is not None else torch.zeros((max(n, 1), 3), dtype=torch.float32, device="cuda")
-    du = du if du is not None else torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+    alloc = torch.empty if n_home == n else torch.zeros  # entries past n_home are not written
+    a = a if a is not None else alloc((max(n, 1), 3), dtype=torch.float32, device="cuda")
+    du = du if du is not None else alloc(max(n, 1), dtype=torch.float32, device="cuda")
     arr = (L.SfForceBlock * len(blocks))(*blocks)
     lo_arr = (C.c_float * 2)(*[float(t) for t in lo_yz])
     check(lib().sf_b200_force_cells_blocks(C.cast(arr, C.c_void_p), len(blocks), n,

@@ -339,8 +339,9 @@ class PeerBlocks:
             return self.api.force_block(base + pos, base + vel, base + pf, base, base + hmax, x0, nx, xo)
         return self.api.cell_block(base + pos, base + mass, base, base + hmax, x0, nx, xo)
 
-    def __call__(self, x, m, h) -> torch.Tensor:
-        """rho of this rank's particles (x, m, h in particle order)."""
+    def __call__(self, x, m, h, out=None) -> torch.Tensor:
+        """rho of this rank's particles (x, m, h in particle order), into `out`
+        (fp32, n) when given."""
         api = self.api
         n = m.shape[0]
         self._barrier()  # the neighbours are done reading the previous block
@@ -361,12 +362,12 @@ class PeerBlocks:
         blocks = [api.cell_block(pos, mass, cs, hmax, self.x0, self.nx, self.x_origin)]
         blocks += [self._peer_block(r) for r in sorted(self.peers)]
         rho = api.density_cells_blocks(blocks, n, self.perm, (0.0, 0.0), self.cell, self.NX, self.ny, self.nz,
-                                       reach=self.refine)
+                                       reach=self.refine, rho=out)
         self.last = {"cs": cs, "perm": self.perm[:max(n, 1)], "n": n}  # valid until the next call
         _mark("store")
         return rho[:n]
 
-    def force(self, v, m, rho, P):
+    def force(self, v, m, rho, P, a=None, du=None):
         """(a, du) of this rank's particles, after __call__ in the same step
         (same positions: the block's cell list and pos are reused); the
         neighbours' (pos, vel, P/rho^2) are read in place."""
@@ -387,7 +388,7 @@ class PeerBlocks:
         blocks = [api.force_block(pos, vel, pf, cs, hmax, self.x0, self.nx, self.x_origin)]
         blocks += [self._peer_block(r, force=True) for r in sorted(self.peers)]
         a, du = api.force_cells_blocks(blocks, n, self.perm, (0.0, 0.0), self.cell, self.NX, self.ny, self.nz,
-                                       reach=self.refine)
+                                       reach=self.refine, a=a, du=du)
         return a[:n], du[:n]
 
     def close(self):
@@ -521,10 +522,13 @@ class ShardedState:
         if self._peer is not None:  # fused halo: the neighbours' blocks are read in place
             _mark("halo")
             self._peer.group = group
-            rho = self._peer(x, m, h)
+            dst = self.stream("rho")
+            direct = dst.dtype == torch.float32 and dst.is_contiguous() and self.n > 0
+            rho = self._peer(x, m, h, out=dst if direct else None)  # fp32 state: written in place
             # at world 1 the own-block grid is the force's local grid: its binning is reusable
             self._binning = self._peer.last if self.slab.world == 1 else None
-            self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
+            if not direct:
+                dst.copy_(rho.to(dst.dtype))
             _mark("end")
             return
         _mark("halo")
@@ -542,9 +546,13 @@ class ShardedState:
         own = [self.stream(k) for k in names]
         if self._peer is not None:  # fused halo: the neighbours' (pos, vel, P/rho^2) read in place
             _mark("halo2")
-            a, du = self._peer.force(own[1], own[2], own[4], own[5])
-            self.stream("a").copy_(a.to(self.stream("a").dtype))
-            self.stream("du").copy_(du.to(self.stream("du").dtype))
+            sa, sd = self.stream("a"), self.stream("du")
+            direct = (sa.dtype == torch.float32 and sd.dtype == torch.float32 and sa.is_contiguous() and
+                      sd.is_contiguous() and self.n > 0)
+            a, du = self._peer.force(own[1], own[2], own[4], own[5], *((sa, sd) if direct else ()))
+            if not direct:
+                sa.copy_(a.to(sa.dtype))
+                sd.copy_(du.to(sd.dtype))
             _mark("end2")
             return
         _mark("halo2")
