@@ -764,3 +764,37 @@ def test_bin_particles_is_a_stable_counting_sort(n, dims):
     cs, perm = api.bin_particles(xt, tuple(float(v) for v in lo), cell, dims)
     np.testing.assert_array_equal(cs.cpu().numpy(), want_start)
     np.testing.assert_array_equal(perm[:n].cpu().numpy(), want_perm)
+
+
+def test_wide_records_take_the_unstaged_kernels():
+    """Records wider than the staged kernels' 384-B limit (424 B: the default
+    fields plus fourteen f64x3 padding fields) go through the direct /
+    per-lane kernels: gather, the scatter-back, and kick,drift in place stay
+    bit-exact vs the oracle and vs the same kernels on the SoA."""
+    base = O.default_schema()
+    fields = list(base.fields) + [O.Field("pad%d" % i, "f64", 3) for i in range(14)]
+    kernels = dict(base.kernels)
+    kernels["kd"] = (["x", "v", "a", "u", "du"], ["x", "v", "u"])
+    S = O.Schema("wide", fields, kernels)
+    assert S.record_bits // 8 > 384
+    n = 3001
+    rng = np.random.default_rng(77)
+    ob = O._alloc(S, n, "aos", list(range(len(S.fields))), [f.fmt(False) for f in S.fields])
+    ob.data[:] = rng.integers(0, 256, ob.data.size, dtype=np.uint8)
+    P = api.Schema(S.text())
+    src = dev(ob, api.View(P, n, "aos"))
+    sub = S.subset("drift")
+    want = O.transform(ob, "soa", subset=sub, fmts=[O.NATIVE(16) for _ in sub])
+    got = api.gather(src, api.View(P, n, "soa", "drift", 16))
+    np.testing.assert_array_equal(host(got), want.data)
+    merged = copy.deepcopy(ob)
+    O.merge_into(want, merged, S.kernels["drift"][1])
+    api.widen_merge(got, src, "drift")
+    np.testing.assert_array_equal(host(src), merged.data)
+    soa = api.gather(src, api.View(P, n, "soa", "kd"))
+    for k in ("kick", "drift"):
+        api.run_kernel(soa, k, 1e-3, buffer_size=1)
+    ref = api.PackedBuffer(src.view, src.data.clone())
+    api.widen_merge(soa, ref, "kd")
+    api.run_kernel(src, "kick,drift", 1e-3, buffer_size=1)
+    np.testing.assert_array_equal(host(src), host(ref))
