@@ -798,3 +798,33 @@ def test_wide_records_take_the_unstaged_kernels():
     api.widen_merge(soa, ref, "kd")
     api.run_kernel(src, "kick,drift", 1e-3, buffer_size=1)
     np.testing.assert_array_equal(host(src), host(ref))
+
+
+@pytest.mark.parametrize("shift", [8, 16, 48])
+def test_gather_and_scatter_from_shifted_buffers(shift):
+    """AoS buffers that start 16 / 48 bytes into an allocation (16-B but not
+    32-B aligned): the scatter and in-place kernels hand off to their per-lane
+    forms, the same bytes either way.  8 bytes breaks the ABI's 16-B buffer
+    alignment and is rejected (SF_INVALID_ARG), never silently misread."""
+    n = 20001
+    ob, P, src = default_aos(n=n)
+    raw = torch.zeros(ob.data.size + 128, dtype=torch.uint8, device="cuda")
+    raw[shift:shift + ob.data.size] = torch.from_numpy(ob.data).cuda()
+    sh = api.PackedBuffer(src.view, raw[shift:shift + ob.data.size])
+    if shift % 16:
+        with pytest.raises(ValueError):
+            api.gather(sh, api.View(P, n, "soa", "drift", 16))
+        return
+    for access, prec in ((None, 16), ("drift", api.SF_PREC_BF16), ("kick", 32)):
+        dst = api.View(P, n, "soa", access, prec)
+        np.testing.assert_array_equal(host(api.gather(sh, dst)), host(api.gather(src, dst)))
+    fused = api.gather_kernel(sh, api.View(P, n, "soa", "drift", 16), "drift", 1e-3)
+    np.testing.assert_array_equal(host(fused), host(api.gather_kernel(src, api.View(P, n, "soa", "drift", 16),
+                                                                      "drift", 1e-3)))
+    ref = api.PackedBuffer(src.view, src.data.clone())
+    api.widen_merge(fused, ref, "drift")
+    api.widen_merge(fused, sh, "drift")
+    np.testing.assert_array_equal(host(sh), host(ref))
+    api.run_kernel(ref, "kick,drift", 1e-3, buffer_size=1)
+    api.run_kernel(sh, "kick,drift", 1e-3, buffer_size=1)
+    np.testing.assert_array_equal(host(sh), host(ref))
