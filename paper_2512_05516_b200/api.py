@@ -224,7 +224,10 @@ scatter_merge = widen_merge
 
 def run_kernel(buf: PackedBuffer, kernel: str, dt: float = 1e-3, buffer_size: int = 64,
                per_access: bool = False, math: int = SF_MATH_FP64_EXACT) -> None:
-    """run_kernel_chunked (sph.cpp:286-308) in place on the device."""
+    """run_kernel_chunked (sph.cpp:286-308) in place on the device.  `kernel`:
+    kick | drift | density | force, or a comma-separated list ("kick,drift")
+    run in order with the same result as one call each (one pass over the
+    records on an AoS of plain IEEE lanes)."""
     check(lib().sf_b200_run_kernel(buf.view.handle, _ptr(buf.data), kernel.encode(), dt, buffer_size,
                                    int(per_access), math, _stream()))
 
