@@ -419,7 +419,7 @@ def other_arm(args):
     return 0
 
 
-def main():
+def build_parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -441,7 +441,11 @@ def main():
                     help="C5 with the full reference timestep (density, force, kick, drift)")
     ap.add_argument("--refine", type=int, default=2,
                     help="C3/C5 binning cells per density cell side (searched with reach = refine)")
-    args = ap.parse_args()
+    return ap
+
+
+def main():
+    args = build_parser().parse_args()
     if args.impl == "reference":
         return reference_arm(args)
     if args.workload != "c2":
