@@ -11,3 +11,6 @@ echo "racecheck $?"
 timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
   -k "sequence_ragged or random_schemas_match_oracle[2]" -p no:cacheprovider > gpurun_out/sync.log 2>&1
 echo "synccheck $?"
+timeout 2200 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sharded.py -q \
+  -k "(cells or density or force or uniform) and not across_processes and not peer" -p no:cacheprovider > gpurun_out/sanitize2.log 2>&1
+echo "memcheck cells $?"
