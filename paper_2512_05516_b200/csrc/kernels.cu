@@ -457,6 +457,51 @@ static void launch_convert_ieee_s(const CStream& c, uint64_t n, const uint8_t* s
     }
 }
 
+// ----------------------------------------------------------------- CTA record tiles
+// The staged kernels (k_gather_multi<true>, k_scatter_tile, k_update_rec_tile)
+// give each CTA a tile of whole records at smem + 128 (the mbarrier below it).
+// stage_tile: one TMA bulk copy of the 16-B-aligned part plus a byte loop for
+// the <16-B tail; returns when every thread can read the tile (bytes == 0:
+// nothing to load).  T = threads per CTA.
+template <int T>
+__device__ __forceinline__ void stage_tile(uint8_t* smem, const uint8_t* g, uint32_t bytes) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* tile = smem + 128;
+    const uint32_t bulk = bytes & ~15u;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, bulk);
+        if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
+    }
+    for (uint32_t b = bulk + threadIdx.x; b < bytes; b += T) tile[b] = g[b];
+    __syncthreads();
+    mbar_wait(bar, 0);
+}
+
+// After every thread updated its record in the tile: each thread stores the
+// 32-B chunks that hold bytes [wlo, whi) of its record (256-bit stores; g is
+// 32-B aligned), so no partially written sector reaches L2.  A chunk may hold
+// bytes of the neighbouring records (rewritten with the staged values, which
+// no other CTA touches); the buffer's last partial chunk goes byte by byte.
+__device__ __forceinline__ void write_back_chunks(const uint8_t* tile, uint8_t* g, uint32_t nrec, uint32_t stride,
+                                                  uint32_t wlo, uint32_t whi) {
+    __syncthreads();
+    if (threadIdx.x >= nrec) return;
+    const uint32_t lo = threadIdx.x * stride + wlo, hi = threadIdx.x * stride + whi, end = nrec * stride;
+    for (uint32_t b = lo & ~31u; b < hi; b += 32) {
+        if (b + 32 <= end) {
+            const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(tile + b);
+            const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(tile + b + 16);
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(g + b), "l"(p.x), "l"(p.y), "l"(q.x),
+                         "l"(q.y)
+                         : "memory");
+        } else {
+            for (uint32_t e = max(b, lo); e < hi; ++e) g[e] = tile[e];
+        }
+    }
+}
+
 // ----------------------------------------------------------------- k_gather_multi
 // Many-stream AoS -> SoA COPY plans (e.g. the full record set to binary16):
 // one thread per record reads every stream's lanes straight from the record
@@ -605,22 +650,10 @@ __global__ void __launch_bounds__(256) k_gather_multi(const __grid_constant__ Ga
     };
     if constexpr (STAGED) {
         extern __shared__ __align__(128) uint8_t smem[];
-        uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-        uint8_t* tile = smem + 128;
         const uint64_t r0 = uint64_t(blockIdx.x) * 256;
         const uint32_t nrec = uint32_t(min(uint64_t(256), n - r0));
-        const uint32_t bytes = uint32_t(nrec * rbytes), bulk = bytes & ~15u;
-        const uint8_t* g = src + r0 * rbytes;
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            mbar_expect_tx(bar, bulk);
-            if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
-        }
-        for (uint32_t b = bulk + threadIdx.x; b < bytes; b += 256) tile[b] = g[b];  // the <16-B tail
-        __syncthreads();
-        mbar_wait(bar, 0);
-        if (threadIdx.x < nrec) body(r0 + threadIdx.x, tile + threadIdx.x * rbytes);
+        stage_tile<256>(smem, src + r0 * rbytes, uint32_t(nrec * rbytes));
+        if (threadIdx.x < nrec) body(r0 + threadIdx.x, smem + 128 + threadIdx.x * rbytes);
     } else {
         for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n; r += uint64_t(gridDim.x) * blockDim.x)
             body(r, src + r * rbytes);
@@ -645,21 +678,11 @@ __global__ void __launch_bounds__(R) k_scatter_tile(const __grid_constant__ Conv
                                                     const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                                     uint32_t stride, uint32_t wlo, uint32_t whi, int full) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* tile = smem + 128;
     const uint64_t n = P.count, r0 = uint64_t(blockIdx.x) * R;
     const uint32_t nrec = uint32_t(min(uint64_t(R), n - r0));
-    const uint32_t bytes = full ? 0 : nrec * stride, bulk = bytes & ~15u;  // full: every byte is rewritten
     uint8_t* g = dst + r0 * stride;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(bar, bulk);
-        if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
-    }
-    for (uint32_t b = bulk + threadIdx.x; b < bytes; b += R) tile[b] = g[b];  // the <16-B tail
-    __syncthreads();
-    mbar_wait(bar, 0);
+    stage_tile<R>(smem, g, full ? 0u : nrec * stride);  // full: every byte is rewritten, nothing to load
     if (threadIdx.x < nrec) {
         const uint64_t r = r0 + threadIdx.x;
         uint8_t* rec = tile + threadIdx.x * stride;
@@ -685,21 +708,7 @@ __global__ void __launch_bounds__(R) k_scatter_tile(const __grid_constant__ Conv
             }
         }
     }
-    __syncthreads();  // a chunk may hold bytes of the neighbouring records
-    if (threadIdx.x < nrec) {
-        const uint32_t lo = threadIdx.x * stride + wlo, hi = threadIdx.x * stride + whi, end = nrec * stride;
-        for (uint32_t b = lo & ~31u; b < hi; b += 32) {
-            if (b + 32 <= end) {
-                const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(tile + b);
-                const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(tile + b + 16);
-                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(g + b), "l"(p.x), "l"(p.y), "l"(q.x),
-                             "l"(q.y)
-                             : "memory");
-            } else {
-                for (uint32_t e = max(b, lo); e < hi; ++e) g[e] = tile[e];  // the buffer's last chunk
-            }
-        }
-    }
+    write_back_chunks(tile, g, nrec, stride, wlo, whi);
 }
 
 // The k_scatter_tile kind of a COPY stream into an AoS record, 0 if it cannot take it.
@@ -1518,21 +1527,11 @@ __global__ void __launch_bounds__(R) k_update_rec_tile(uint8_t* __restrict__ buf
                                                          const __grid_constant__ RecSeq S, double dt, uint8_t math,
                                                          uint32_t wlo, uint32_t whi) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint8_t* tile = smem + 128;
     const uint64_t r0 = uint64_t(blockIdx.x) * R;
     const uint32_t nrec = uint32_t(min(uint64_t(R), n - r0));
-    const uint32_t bytes = nrec * stride, bulk = bytes & ~15u;
     uint8_t* g = buf + r0 * stride;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(bar, bulk);
-        if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
-    }
-    for (uint32_t b = bulk + threadIdx.x; b < bytes; b += R) tile[b] = g[b];  // the <16-B tail
-    __syncthreads();
-    mbar_wait(bar, 0);
+    stage_tile<R>(smem, g, nrec * stride);
     if (threadIdx.x < nrec) {
         uint8_t* rec = tile + threadIdx.x * stride;
 #pragma unroll 1
@@ -1551,21 +1550,7 @@ __global__ void __launch_bounds__(R) k_update_rec_tile(uint8_t* __restrict__ buf
             }
         }
     }
-    __syncthreads();  // a chunk may hold bytes of the neighbouring records
-    if (threadIdx.x < nrec) {
-        const uint32_t lo = threadIdx.x * stride + wlo, hi = threadIdx.x * stride + whi;
-        for (uint32_t b = lo & ~31u; b < hi; b += 32) {
-            if (b + 32 <= bytes) {
-                const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(tile + b);
-                const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(tile + b + 16);
-                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(g + b), "l"(p.x), "l"(p.y), "l"(q.x),
-                             "l"(q.y)
-                             : "memory");
-            } else {
-                for (uint32_t e = max(b, lo); e < hi; ++e) g[e] = tile[e];  // the buffer's last chunk
-            }
-        }
-    }
+    write_back_chunks(tile, g, nrec, stride, wlo, whi);
 }
 
 cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate) {
