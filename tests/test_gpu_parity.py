@@ -3,6 +3,7 @@ oracle and the reference's golden checksums.  Bit-exact for every layout /
 precision conversion and for fp64-exact kick/drift/density; stated
 tolerances for the fp32 math mode and the cell-linked density."""
 import copy
+import os
 
 import numpy as np
 import pytest
@@ -609,7 +610,7 @@ def _random_schema(rng):
     return O.Schema("rnd", fields, {"k": (reads, writes)})
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SFB_RANDOM_SCHEMAS", "24"))))
 def test_random_schemas_match_oracle(seed):
     """Random schemas x random bit patterns x every precision code, through
     whichever kernel each plan selects (TMA tiles, many-stream direct loads,
