@@ -829,3 +829,49 @@ def test_gather_and_scatter_from_shifted_buffers(shift):
     api.run_kernel(ref, "kick,drift", 1e-3, buffer_size=1)
     api.run_kernel(sh, "kick,drift", 1e-3, buffer_size=1)
     np.testing.assert_array_equal(host(sh), host(ref))
+
+
+def _random_kd_schema(rng):
+    """kick / drift fields in random order and formats among random extra
+    fields (f32/f64, optional @truncate), so the in-place sequence runs on
+    every format pair, aligned or bit-packed."""
+    def fld(name, ar):
+        base = str(rng.choice(["f32", "f64"]))
+        trunc = int(rng.integers(10, 33 if base == "f32" else 65)) if rng.random() < 0.25 else 0
+        return O.Field(name, base, ar, trunc)
+    fields = [fld("x", 3), fld("v", 3), fld("a", 3), fld("u", 1), fld("du", 1)]
+    for i in range(int(rng.integers(0, 5))):
+        fields.append(O.Field("e%d" % i, str(rng.choice(["f32", "f64", "i64"])), int(rng.choice([1, 3]))))
+    order = rng.permutation(len(fields))
+    fields = [fields[k] for k in order]
+    return O.Schema("kd", fields, {"kick": (["v", "a", "u", "du"], ["v", "u"]), "drift": (["x", "v"], ["x"])})
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SFB_RANDOM_KD", "16"))))
+def test_random_kick_drift_layouts_match_live_reference(seed):
+    """run_kernel("kick,drift") in place on a random stored AoS (byte-aligned
+    IEEE lanes: the one-pass tile kernel; truncated lanes: the generic path)
+    vs the unmodified reference running kick then drift on the same bytes."""
+    rng = np.random.default_rng(4000 + seed)
+    S = _random_kd_schema(rng)
+    n = int(rng.integers(1, 4000))
+    ob = O._alloc(S, n, "aos", list(range(len(S.fields))), [f.fmt(False) for f in S.fields])
+    vals = rng.standard_normal(ob.data.size // 4 + 1).astype(np.float32)  # finite lanes in every format
+    ob.data[:] = vals.view(np.uint8)[: ob.data.size]
+    for i, f in enumerate(S.fields):  # finite, representable values in every float lane
+        if f.is_float:
+            O._write_field_bits(ob, i, O.encode(rng.uniform(-2, 2, n * f.arity), f.fmt(False)))
+    tail = ob.length_bits % 8
+    if tail:
+        ob.data[-1] &= (1 << tail) - 1
+    R = O.RefLib()
+    h = R._chk(R.L.ref_buf_from_bytes(S.text().encode(), 0, b"", n, O._p(ob.data), ob.data.size))
+    R.run_kernel(h, "kick", 1, 1e-3)
+    R.run_kernel(h, "drift", 1, 1e-3)
+    want = R.bytes(h)
+    R.free(h)
+    P = api.Schema(S.text())
+    src = dev(ob, api.View(P, n, "aos"))
+    api.run_kernel(src, "kick,drift", 1e-3, buffer_size=1)
+    np.testing.assert_array_equal(host(src), want, err_msg=S.text())
