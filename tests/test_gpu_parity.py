@@ -875,3 +875,45 @@ def test_random_kick_drift_layouts_match_live_reference(seed):
     src = dev(ob, api.View(P, n, "aos"))
     api.run_kernel(src, "kick,drift", 1e-3, buffer_size=1)
     np.testing.assert_array_equal(host(src), want, err_msg=S.text())
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SFB_RANDOM_DF", "8"))))
+def test_random_density_force_layouts_match_live_reference(seed):
+    """Buffer-mode density then force (64-particle buffers, binary64, the
+    reference's association order) in place on random stored AoS layouts vs
+    the unmodified reference on the same bytes: bit for bit."""
+    rng = np.random.default_rng(5000 + seed)
+
+    def fld(name, ar):
+        base = str(rng.choice(["f32", "f64"]))
+        trunc = int(rng.integers(12, 33 if base == "f32" else 65)) if rng.random() < 0.2 else 0
+        return O.Field(name, base, ar, trunc)
+    fields = [fld("x", 3), fld("v", 3), fld("m", 1), fld("h", 1), fld("rho", 1), fld("P", 1), fld("a", 3),
+              fld("du", 1)]
+    for i in range(int(rng.integers(0, 3))):
+        fields.append(O.Field("e%d" % i, "i64", 1))
+    fields = [fields[k] for k in rng.permutation(len(fields))]
+    S = O.Schema("df", fields, {"density": (["x", "m", "h"], ["rho"]),
+                                 "force": (["x", "v", "m", "h", "rho", "P"], ["a", "du"])})
+    n = 64 * int(rng.integers(1, 40))
+    ob = O._alloc(S, n, "aos", list(range(len(S.fields))), [f.fmt(False) for f in S.fields])
+    ranges = {"x": (0, 1), "v": (-1, 1), "m": (0.5 / 64, 1.5 / 64), "h": (0.2, 0.6), "rho": (0.5, 1.5),
+              "P": (0.1, 1.0), "a": (-1, 1), "du": (-1, 1)}
+    for i, f in enumerate(S.fields):
+        if f.is_float:
+            lo, hi = ranges[f.name]
+            O._write_field_bits(ob, i, O.encode(rng.uniform(lo, hi, n * f.arity), f.fmt(False)))
+        else:
+            O._write_field_bits(ob, i, rng.integers(0, 1 << 62, n, dtype=np.int64).view(np.uint64))
+    R = O.RefLib()
+    h = R._chk(R.L.ref_buf_from_bytes(S.text().encode(), 0, b"", n, O._p(ob.data), ob.data.size))
+    R.run_kernel(h, "density", 64, 1e-3)
+    R.run_kernel(h, "force", 64, 1e-3)
+    want = R.bytes(h)
+    R.free(h)
+    P = api.Schema(S.text())
+    src = dev(ob, api.View(P, n, "aos"))
+    api.run_kernel(src, "density", 1e-3, buffer_size=64)
+    api.run_kernel(src, "force", 1e-3, buffer_size=64)
+    np.testing.assert_array_equal(host(src), want, err_msg=S.text())
