@@ -917,3 +917,33 @@ def test_random_density_force_layouts_match_live_reference(seed):
     api.run_kernel(src, "density", 1e-3, buffer_size=64)
     api.run_kernel(src, "force", 1e-3, buffer_size=64)
     np.testing.assert_array_equal(host(src), want, err_msg=S.text())
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SFB_RANDOM_FUSED", "12"))))
+def test_random_fused_gather_kernel_matches_live_reference(seed):
+    """The north-star composition on random layouts: store_state(T) -> unpack
+    -> narrow(k) -> aos_to_soa -> run_kernel(k) in the reference vs one fused
+    gather_kernel (T in {16, 24, 32}, k in {kick, drift}), bit for bit."""
+    rng = np.random.default_rng(6000 + seed)
+    S = _random_kd_schema(rng)
+    n = int(rng.integers(1, 3000))
+    ob = O._alloc(S, n, "aos", list(range(len(S.fields))), [f.fmt(False) for f in S.fields])
+    for i, f in enumerate(S.fields):
+        if f.is_float:
+            O._write_field_bits(ob, i, O.encode(rng.uniform(-2, 2, n * f.arity), f.fmt(False)))
+    T = int(rng.choice([16, 24, 32]))
+    k = str(rng.choice(["kick", "drift"]))
+    R = O.RefLib()
+    h = R._chk(R.L.ref_buf_from_bytes(S.text().encode(), 0, b"", n, O._p(ob.data), ob.data.size))
+    st = R.restore(h, T, "", S.text())
+    u = R.op(st, "unpack")
+    nw = R.op(u, "narrow", k)
+    so = R.op(nw, "aos_to_soa")
+    R.run_kernel(so, k, 1, 1e-3)
+    want = R.bytes(so)
+    R.free(h, st, u, nw, so)
+    P = api.Schema(S.text())
+    src = dev(ob, api.View(P, n, "aos"))
+    got = api.gather_kernel(src, api.View(P, n, "soa", k, T), k, 1e-3)
+    np.testing.assert_array_equal(host(got), want, err_msg="%s T=%d %s" % (S.text(), T, k))
