@@ -437,6 +437,8 @@ def build_parser():
                     help="BASELINE.json config (default c2 = configs[1], the headline)")
     ap.add_argument("--c4-n", type=int, default=1 << 26)
     ap.add_argument("--c5-n", type=int, default=1 << 27)
+    ap.add_argument("--c5-reorder", type=int, default=0,
+                    help="C5: permute the state into the density's cell order every k-th step (0: never)")
     ap.add_argument("--c5-full", action="store_true",
                     help="C5 with the full reference timestep (density, force, kick, drift)")
     ap.add_argument("--refine", type=int, default=2,

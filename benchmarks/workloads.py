@@ -257,12 +257,12 @@ def c5(args, peak, peak_kind, world, rank, group=None):
     n = args.c5_n
     h, nc, cell = grid_for(n)
     slab = Slab(nc, cell, rank, world)
-    st = ShardedState(n, slab, prec=32, h=h)
-    st.sort_by_cell()  # particles kept in cell order (re-sorted every few steps in a long run)
+    st = ShardedState(n, slab, prec=32, h=h, reorder_every=args.c5_reorder)
+    st.sort_by_cell()  # particles start in cell order; --c5-reorder k keeps them there every k-th step
     for _ in range(max(1, min(args.warmup, 2))):
         st.full_step(group=group) if args.c5_full else st.step(group=group)
     torch.cuda.synchronize()
-    phases = {"kick_drift": [], "migrate": [], "density": []}
+    phases = {"kick_drift": [], "migrate": [], "density": [], "reorder": []}
     if args.c5_full:
         phases["force"] = []
     times = []
@@ -270,23 +270,26 @@ def c5(args, peak, peak_kind, world, rank, group=None):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         ev[0].record()
         if args.c5_full:  # the reference's timestep order: density, force, kick+drift, migrate
             st.density(group)
             ev[1].record()
             st.force(group)
             ev[2].record()
-            st.kick_drift()
+            st.maybe_reorder()
             ev[3].record()
-            st.migrate(group)
+            st.kick_drift()
             ev[4].record()
-            ev[4].synchronize()
+            st.migrate(group)
+            ev[5].record()
+            ev[5].synchronize()
             phases["density"].append(ev[0].elapsed_time(ev[1]))
             phases["force"].append(ev[1].elapsed_time(ev[2]))
-            phases["kick_drift"].append(ev[2].elapsed_time(ev[3]))
-            phases["migrate"].append(ev[3].elapsed_time(ev[4]))
-            times.append(ev[0].elapsed_time(ev[4]))
+            phases["reorder"].append(ev[2].elapsed_time(ev[3]))
+            phases["kick_drift"].append(ev[3].elapsed_time(ev[4]))
+            phases["migrate"].append(ev[4].elapsed_time(ev[5]))
+            times.append(ev[0].elapsed_time(ev[5]))
             continue
         st.kick_drift()
         ev[1].record()
@@ -294,11 +297,14 @@ def c5(args, peak, peak_kind, world, rank, group=None):
         ev[2].record()
         st.density(group)
         ev[3].record()
-        ev[3].synchronize()
+        st.maybe_reorder()
+        ev[4].record()
+        ev[4].synchronize()
         phases["kick_drift"].append(ev[0].elapsed_time(ev[1]))
         phases["migrate"].append(ev[1].elapsed_time(ev[2]))
         phases["density"].append(ev[2].elapsed_time(ev[3]))
-        times.append(ev[0].elapsed_time(ev[3]))
+        phases["reorder"].append(ev[3].elapsed_time(ev[4]))
+        times.append(ev[0].elapsed_time(ev[4]))
     ms = sum(times) / len(times)
     # one more step with sub-phase events (not part of the timed mean)
     import paper_2512_05516_b200.sharded as SH

@@ -114,6 +114,12 @@ SF_API sf_status sf_b200_gather_kernel(const sf_view* src, const void* src_dev, 
  * (AoS<->SoA, any precisions). */
 SF_API sf_status sf_b200_convert(const sf_view* src, const void* src_dev, const sf_view* dst,
                                  void* dst_dev, void* stream);
+/* Reorder: dst record k = src record perm[k] for every lane of the view
+ * (AoS: whole records; SoA: every stream), e.g. a particle population into
+ * the cell order of sf_b200_bin_particles' perm.  Byte-aligned views; src
+ * and dst must not alias. */
+SF_API sf_status sf_b200_permute(const sf_view* view, const void* src_dev, void* dst_dev, const int32_t* perm,
+                                 void* stream);
 /* Fused C^T∘U^T∘N^T: write only `kernel`'s write set from src into dst
  * (widen_merge, layout_ops.cpp:120-146); read-only lanes stay bit-exact. */
 SF_API sf_status sf_b200_scatter_merge(const sf_view* src, const void* src_dev, const sf_view* dst,

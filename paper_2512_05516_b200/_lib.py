@@ -88,6 +88,7 @@ SYMBOLS = [
     ("sf_b200_gather_kernel", i32, [P, P, P, P, s, f64, i32, P]),
     ("sf_b200_convert", i32, [P, P, P, P, P]),
     ("sf_b200_scatter_merge", i32, [P, P, P, P, s, P]),
+    ("sf_b200_permute", i32, [P, P, P, P, P]),
     ("sf_b200_run_kernel", i32, [P, P, s, f64, u64, i32, i32, P]),
     ("sf_b200_density_cells", i32, [P, P, P, i32, u64, P, P, P, C.c_float, i32, i32, i32, i32, u64, P, P]),
     ("sf_b200_force_cells", i32, [P] * 6 + [i32, u64, P, P, P, C.c_float] + [i32] * 4 + [u64, P, P, P]),

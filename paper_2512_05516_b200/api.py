@@ -222,6 +222,14 @@ def widen_merge(narrowed: PackedBuffer, original: PackedBuffer, kernel: str) -> 
 scatter_merge = widen_merge
 
 
+def permute(src: PackedBuffer, perm, out: Optional[PackedBuffer] = None) -> PackedBuffer:
+    """Record k of the result = record perm[k] of src (every lane; perm: int32
+    cuda tensor of src.view.count entries, e.g. bin_particles' perm)."""
+    out = out if out is not None else PackedBuffer.empty(src.view)
+    check(lib().sf_b200_permute(src.view.handle, _ptr(src.data), _ptr(out.data), _ptr(perm), _stream()))
+    return out
+
+
 def run_kernel(buf: PackedBuffer, kernel: str, dt: float = 1e-3, buffer_size: int = 64,
                per_access: bool = False, math: int = SF_MATH_FP64_EXACT) -> None:
     """run_kernel_chunked (sph.cpp:286-308) in place on the device.  `kernel`:

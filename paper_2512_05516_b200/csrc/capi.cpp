@@ -237,6 +237,14 @@ sf_status sf_b200_convert(const sf_view* src, const void* sp, const sf_view* dst
     });
 }
 
+sf_status sf_b200_permute(const sf_view* v, const void* src_dev, void* dst_dev, const int32_t* perm, void* stream) {
+    if (!v) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        permute(v->v, src_dev, dst_dev, perm, static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
 sf_status sf_b200_scatter_merge(const sf_view* src, const void* sp, const sf_view* dst, void* dp, const char* k,
                                 void* stream) {
     if (!src || !dst || !sp || !dp || !k) return fail(SF_INVALID_ARG, "null argument");

@@ -1553,6 +1553,40 @@ __global__ void __launch_bounds__(R) k_update_rec_tile(uint8_t* __restrict__ buf
     write_back_chunks(tile, g, nrec, stride, wlo, whi);
 }
 
+// ----------------------------------------------------------------- k_permute
+// dst record k = src record perm[k], stream by stream (SoA: each field's
+// lanes; AoS: the whole record), in the widest aligned unit.  For the
+// near-identity permutations of a cell re-sort the loads stay coherent.
+template <typename T>
+__device__ __forceinline__ void copy_units(const uint8_t* __restrict__ s, uint8_t* __restrict__ d, uint32_t eb) {
+    for (uint32_t o = 0; o < eb; o += sizeof(T)) *reinterpret_cast<T*>(d + o) = *reinterpret_cast<const T*>(s + o);
+}
+
+__global__ void __launch_bounds__(256) k_permute(const __grid_constant__ PermutePlan P, const uint8_t* __restrict__ src,
+                                                 uint8_t* __restrict__ dst, const int32_t* __restrict__ perm) {
+    const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (k >= P.count) return;
+    const uint64_t i = uint64_t(perm[k]);
+    for (int q = 0; q < P.n; ++q) {
+        const uint32_t eb = P.eb[q];
+        const uint8_t* s = src + P.base[q] + i * eb;
+        uint8_t* d = dst + P.base[q] + k * eb;
+        switch (P.unit[q]) {
+            case 8: copy_units<uint64_t>(s, d, eb); break;
+            case 4: copy_units<uint32_t>(s, d, eb); break;
+            case 2: copy_units<uint16_t>(s, d, eb); break;
+            default: copy_units<uint8_t>(s, d, eb); break;
+        }
+    }
+}
+
+cudaError_t launch_permute(const PermutePlan& p, const void* src, void* dst, const int32_t* perm, cudaStream_t st) {
+    if (p.count == 0) return cudaSuccess;
+    k_permute<<<unsigned((p.count + 255) / 256), 256, 0, st>>>(p, static_cast<const uint8_t*>(src),
+                                                               static_cast<uint8_t*>(dst), perm);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate) {
     if (p.count == 0) {
         *degenerate = false;

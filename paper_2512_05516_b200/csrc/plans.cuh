@@ -95,6 +95,15 @@ struct RecSeq {
     int n;
 };
 
+// ---- record permutation (dst record k = src record perm[k]) -----------------
+struct PermutePlan {
+    uint64_t count = 0;
+    int n = 0;                     // element streams (AoS: 1, the whole record)
+    uint64_t base[kMaxStreams];    // bytes
+    uint32_t eb[kMaxStreams];      // element bytes per record
+    uint8_t unit[kMaxStreams];     // 8 / 4 / 2 / 1: widest aligned copy unit
+};
+
 // ---- SPH density over 64-particle neighbour buffers (sph.cpp:176-199) -------
 struct DensityPlan {
     Lanes x, m, h, rho;

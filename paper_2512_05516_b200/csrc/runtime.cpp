@@ -263,4 +263,34 @@ void run_kernel(const View& v, void* p, const std::string& kernel, double dt, ui
     count_launches(1);
 }
 
+void permute(const View& v, const void* src, void* dst, const int32_t* perm, cudaStream_t st) {
+    require_device();
+    if (v.count && (!src || !dst || !perm)) throw std::invalid_argument("null argument");
+    if (src == dst) throw std::invalid_argument("permute: source and destination must not alias");
+    if (!v.byte_aligned()) throw std::invalid_argument("permute needs a byte-aligned view");
+    PermutePlan p;
+    p.count = v.count;
+    auto unit = [](uint64_t base, uint64_t eb) {
+        for (uint8_t u : {8, 4, 2})
+            if (base % u == 0 && eb % u == 0) return u;
+        return uint8_t(1);
+    };
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst);
+    if (v.layout == Layout::AoS) {
+        p.n = 1;
+        p.base[0] = 0;
+        p.eb[0] = uint32_t(v.record_bits() / 8);
+        p.unit[0] = unit(a, p.eb[0]);
+    } else {
+        for (size_t q = 0; q < v.subset.size(); ++q) {
+            p.base[p.n] = v.lane_base(int(q)) / 8;
+            p.eb[p.n] = uint32_t(uint64_t(v.arity(int(q))) * v.width(int(q)) / 8);
+            p.unit[p.n] = unit(a | p.base[p.n], p.eb[p.n]);
+            ++p.n;
+        }
+    }
+    check_cuda(launch_permute(p, src, dst, perm, st), "permute launch");
+    count_launches(1);
+}
+
 }  // namespace sfb

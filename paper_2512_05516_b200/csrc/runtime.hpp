@@ -19,6 +19,8 @@ cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_byt
 cudaError_t launch_density_buffer(const DensityPlan& p, void* buf, cudaStream_t st);
 cudaError_t launch_update_rec(int xb, int yb, int arity, void* buf, uint64_t n, uint32_t stride, uint32_t xoff,
                               uint32_t yoff, double dt, uint8_t op, uint8_t math, cudaStream_t st);
+cudaError_t launch_permute(const PermutePlan& p, const void* src, void* dst, const int32_t* perm, cudaStream_t st);
+void permute(const View& v, const void* src, void* dst, const int32_t* perm, cudaStream_t st);
 cudaError_t launch_update_rec_tile(void* buf, uint64_t n, uint32_t stride, const RecSeq& seq, double dt,
                                    uint8_t math, uint32_t wlo, uint32_t whi, cudaStream_t st);
 cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint32_t stride, const RecOps& ops,

@@ -356,6 +356,7 @@ class PeerBlocks:
         _mark("bin")
         api.bin_particles(x.float().contiguous(), (self.x_origin, 0.0, 0.0), self.cell, (self.nx, self.ny, self.nz),
                           cell_start=cs, perm=self.perm[:max(n, 1)])
+        _mark("pack")
         api.cells_pack(x.contiguous(), m.contiguous(), h.contiguous(), self.perm, pos, mass, hmax, self.prec)
         self._barrier()  # every block of this step is complete
         _mark("pairs")
@@ -405,9 +406,13 @@ class ShardedState:
     uniform storage precision `prec` (32 or 16; positions included)."""
 
     def __init__(self, n_global: int, slab: Slab, prec: int = 32, seed: int = 7, device="cuda",
-                 h: Optional[float] = None, halo: str = "peer", group=None):
+                 h: Optional[float] = None, halo: str = "peer", group=None, reorder_every: int = 0):
+        """reorder_every = k > 0: every k-th density also permutes the whole
+        state into that density's cell order (peer halo), so the next steps'
+        binning and pack gathers stay coherent (particles keep their ids)."""
         from . import api
         self.api, self.slab, self.prec, self.device = api, slab, prec, device
+        self.reorder_every, self._densities = reorder_every, 0
         if halo not in ("peer", "nccl"):
             raise ValueError("halo must be 'peer' (neighbour blocks read in place) or 'nccl' (ghost rows sent)")
         self.halo = halo
@@ -563,11 +568,29 @@ class ShardedState:
         self.stream("du").copy_(du.to(self.stream("du").dtype))
         _mark("end2")
 
+    def reorder_by_density(self):
+        """Permute every field into the cell order of the last density call
+        (its perm: sorted position -> particle) with one sf_b200_permute."""
+        last = self._peer.last if self._peer is not None else None
+        if last is None or last["n"] != self.n or self.n == 0:
+            return
+        view = self.buf.view
+        out = self.api.PackedBuffer(view, torch.empty(view.nbytes + 16, dtype=torch.uint8, device=self.device))
+        self.buf = self.api.permute(self.buf, last["perm"][: self.n], out=out)
+        self._peer.last = None  # its perm indexes the old order
+        self._binning = None
+
+    def maybe_reorder(self):
+        self._densities += 1
+        if self.reorder_every > 0 and self._peer is not None and self._densities % self.reorder_every == 0:
+            self.reorder_by_density()
+
     def full_step(self, dt=1e-3, group=None):
         """The reference timestep order (density -> force -> kick -> drift,
         pipelines.cpp / bench.cpp kernel lists), then migration."""
         self.density(group)
         self.force(group)
+        self.maybe_reorder()  # after the force: it still uses the density's perm
         self.kick_drift(dt)
         self.migrate(group)
 
@@ -588,3 +611,4 @@ class ShardedState:
         self.kick_drift(dt)
         self.migrate(group)
         self.density(group)
+        self.maybe_reorder()

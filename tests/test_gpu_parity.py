@@ -947,3 +947,19 @@ def test_random_fused_gather_kernel_matches_live_reference(seed):
     src = dev(ob, api.View(P, n, "aos"))
     got = api.gather_kernel(src, api.View(P, n, "soa", k, T), k, 1e-3)
     np.testing.assert_array_equal(host(got), want, err_msg="%s T=%d %s" % (S.text(), T, k))
+
+
+@pytest.mark.parametrize("layout,prec", [("aos", None), ("soa", None), ("soa", 16), ("aos", api.SF_PREC_NATIVE)])
+def test_permute_records(layout, prec):
+    """sf_b200_permute: record k of the result = record perm[k], every lane."""
+    n = 12345
+    ob, P, src = default_aos(n=n)
+    v = api.View(P, n, layout, None, api.SF_PREC_STORED if prec is None else prec)
+    buf = api.convert(src, v)
+    perm = torch.randperm(n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)).int()
+    out = api.permute(buf, perm)
+    back = api.convert(out, api.View(P, n, "aos", None, api.SF_PREC_STORED if prec is None else prec))
+    orig = api.convert(buf, back.view)
+    rb = back.view.nbytes // n
+    np.testing.assert_array_equal(host(back)[: n * rb].reshape(n, rb), host(orig)[: n * rb].reshape(n, rb)[
+        perm.cpu().numpy()])
