@@ -156,6 +156,12 @@ def test_gpu_entry_points_fail_loudly_without_device():
     st = L.lib().sf_b200_gather(src.handle, C.cast(buf, C.c_void_p), dst.handle, C.cast(out, C.c_void_p), None)
     assert st == L.SF_ERROR
     assert "no CUDA device" in L.lib().sf_last_error().decode()
+    perm = (C.c_int32 * 128)(*range(128))
+    st = L.lib().sf_b200_permute(src.handle, C.cast(buf, C.c_void_p), C.cast(out, C.c_void_p),
+                                 C.cast(perm, C.c_void_p), None)
+    assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
+    st = L.lib().sf_b200_run_kernel(src.handle, C.cast(buf, C.c_void_p), b"kick,drift", 1e-3, 64, 0, 0, None)
+    assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
 
 
 def test_plain_c_consumer_links_and_runs(tmp_path):
