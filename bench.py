@@ -114,6 +114,48 @@ def cpu_reference_rate(n_per_thread, threads, prec, seed=42):
     return n_per_thread * threads / secs, secs
 
 
+def cpu_c1_rate(n, threads, dt=1e-3):
+    """C1 on the unmodified reference itself (oracle/_ref): kick then drift in
+    place on the default AoS (run_kernel_chunked, 64-particle buffers, `threads`
+    host threads), the full 1M-particle workload."""
+    import time
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.RefLib.available():
+        raise RuntimeError("oracle/_ref/libref_driver.so missing (run `make -C oracle`)")
+    R = O.RefLib()
+    h = R.from_ics(n, 42, 0, "", None, 43, dt)
+    R.run_kernel(h, "kick", 64, dt, threads=threads)  # warm-up: pages touched, threads spawned once
+    t0 = time.perf_counter()
+    R.run_kernel(h, "kick", 64, dt, threads=threads)
+    R.run_kernel(h, "drift", 64, dt, threads=threads)
+    secs = time.perf_counter() - t0
+    R.free(h)
+    return n / secs, secs
+
+
+def cpu_c3_port_rate(n_total, sample=1 << 16, seed=5):
+    """C3's cell-linked density on the CPU: the oracle's C restatement
+    (oracle/soa_oracle.c or_density_cells, one core) on a sub-box holding
+    `sample` particles at C3's number density and smoothing length."""
+    import time
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2512_05516_b200.sharded import grid_for
+    h, _, _ = grid_for(n_total)
+    side = (sample / n_total) ** (1.0 / 3.0)
+    ncell = max(1, int(side / (2 * h)))
+    rng = np.random.default_rng(seed)
+    x = rng.random((sample, 3)) * side
+    m = np.full(sample, 1.0 / n_total)
+    hh = np.full(sample, h)
+    t0 = time.perf_counter()
+    O.density_cells(x.reshape(-1), m, hh, 0.0, side, side / ncell)
+    secs = time.perf_counter() - t0
+    return sample / secs, secs
+
+
 def _bench_kernels_csv(lib_path, particles, threads):
     """Run a library's sf_run_bench_kernels (bench.cpp:269-316 semantics)."""
     import ctypes as C
@@ -401,12 +443,27 @@ def other_arm(args):
         res = getattr(W, args.workload)(args, peak, kind)
     launches = api.launch_count() - l0
     clocks = sampler.stop()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload in ("c1", "c3"):
+        try:
+            if args.workload == "c1":
+                threads = os.cpu_count() or 1
+                rate, secs = cpu_c1_rate(1 << 20, threads)
+                cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": "the full C1 workload: kick then drift on 1M default-AoS particles, %.3f s" % secs}
+            else:
+                rate, secs = cpu_c3_port_rate(1 << 22)
+                cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": "65536 particles at C3's density and h in a sub-box (fewer neighbours at its "
+                                 "faces), cell-linked density of the oracle's C restatement, %.2f s" % secs}
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "unavailable: %s" % ex}
     if rank == 0:
         line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f64" if
                 args.workload in ("c1", "c4") else "f32", "data": "synthetic (uniform random, device RNG)",
-                "config": res["config"], "roofline": res["roofline"], "cpu_baseline": None, "e2e": None,
+                "config": res["config"], "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": None,
                 "gpu_launches": launches, "clocks": clocks, "impl": "b200", "workload": args.workload}
         for k in ("kernels", "phases_ms", "particles_local"):
             if k in res:
