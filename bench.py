@@ -444,9 +444,20 @@ def other_arm(args):
     launches = api.launch_count() - l0
     clocks = sampler.stop()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and args.workload in ("c1", "c3"):
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload in ("c1", "c3", "c4", "c5"):
         try:
-            if args.workload == "c1":
+            if args.workload == "c4":  # extrapolated per particle from a <= 16M sample
+                threads = os.cpu_count() or 1
+                rate, secs = cpu_c1_rate(1 << 22, threads)
+                cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": "extrapolated per particle: the reference's kick then drift on a 4M-particle "
+                                 "host AoS (no transfers: the data is already where the CPU computes), %.3f s" % secs}
+            elif args.workload == "c5":
+                rate, secs = cpu_c3_port_rate(args.c5_n)
+                cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": "extrapolated per particle: cell-linked density of the oracle's C restatement on "
+                                 "65536 particles at C5's density and h (one core), %.2f s" % secs}
+            elif args.workload == "c1":
                 threads = os.cpu_count() or 1
                 rate, secs = cpu_c1_rate(1 << 20, threads)
                 cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
