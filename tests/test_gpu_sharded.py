@@ -379,3 +379,27 @@ def test_state_reorder_keeps_the_physics():
     np.testing.assert_array_equal(runs[0]["id"], runs[1]["id"])
     for f in ("x", "v", "rho", "a", "u"):
         np.testing.assert_allclose(runs[1][f], runs[0][f], rtol=2e-4, atol=1e-6, err_msg=f)
+
+
+@pytest.mark.parametrize("workload", ["c2", "c5"])
+def test_bench_under_torchrun_two_ranks_one_device(workload, tmp_path):
+    """bench.py under torchrun with 2 ranks (both on cuda:0 over gloo,
+    SFB_BENCH_ONE_DEVICE=1): one JSON line from rank 0, n_gpus = 2, the
+    whole-job value over both ranks (C2 at its full 16M per rank, C5 small)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    extra = ["--no-e2e", "--no-cpu"] if workload == "c2" else \
+        ["--workload", "c5", "--c5-n", str(1 << 20), "--no-cpu"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(29600 + (workload == "c5")), os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3"] + extra
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, SFB_BENCH_ONE_DEVICE="1"), cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
