@@ -5,8 +5,8 @@ binary16 storage of position/velocity, fused into drift, 16M particles.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 One step = one pass of the hot path over the whole 16M-particle population:
-the default 88-B AoS (f64 x, f32 v, ...) in HBM -> k_gather_multi (each CTA's
-records staged in shared memory by one TMA bulk copy, RNE narrowing to
+the default 88-B AoS (f64 x, f32 v, ...) in HBM -> k_gather_xv_staged (each
+CTA's records staged in shared memory by one TMA bulk copy, RNE narrowing to
 binary16, drift x += v*dt in binary64) ->
 SoA binary16 {x', v}.  Under torchrun every rank runs its own 16M particles
 (weak scaling: particles shard with no data-path collective); timing is the
@@ -324,7 +324,7 @@ def b200_arm(args):
     peak, peak_kind = peaks()
     achieved = ALG_BYTES * n / (ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_kind": peak_kind, "kernel": "k_gather_multi<staged> (fused gather+drift, %s)" % prec_name,
+                "peak_kind": peak_kind, "kernel": "k_gather_xv_staged (CTA records staged by TMA, fused gather+drift, %s)" % prec_name,
                 "algorithmic_bytes_per_particle": ALG_BYTES,
                 "traffic": traffic_from_profiles("gather_drift_%s" % args.prec)}
     if roofline["traffic"]:  # the DRAM bytes ncu measured per launch, over the same launch time
@@ -385,7 +385,7 @@ def b200_arm(args):
         ok = bool(torch.equal(got, out.data[: dst_v.nbytes]))
         e2e = {"value": n * world / float(s_t.item()), "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"] * world,
                "d2h_bytes_per_step": m["d2h_bytes"] * world, "chunk_particles": args.chunk, "matches_device_result": ok,
-               "path": "sf_b200_run_host(mode 2): pinned AoS, whole records H2D || k_gather_multi (fused drift) || "
+               "path": "sf_b200_run_host(mode 2): pinned AoS, whole records H2D || k_gather_xv_staged (fused drift) || "
                        "D2H SoA, 3-stream chunk pipeline"}
         hb.free()
         hs.free()

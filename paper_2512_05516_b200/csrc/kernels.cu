@@ -6,9 +6,11 @@
 //                    shared memory by per-warp 1-D TMA bulk copies (cp.async.bulk,
 //                    UBLKCP) through an mbarrier ring; lanes extracted with
 //                    funnel shifts (any bit offset/width); 16-B SoA stores.
-//   k_gather_multi   AoS -> SoA for every plan of plain 16/32/64-bit lanes
-//                    (the C2 drift set fused with drift, full records, kick /
-//                    density sets): each CTA pulls its 256 records into shared
+//   k_gather_xv_staged  the C2 plan (x f64x3 [+ drift], v f32x3 -> fp16/bf16/
+//                    fp32) on a staged CTA tile, formats fixed at compile time.
+//   k_gather_multi   AoS -> SoA for every other plan of plain 16/32/64-bit
+//                    lanes (full records, kick / density sets, the gather
+//                    fused with kick): each CTA pulls its 256 records into shared
 //                    memory with one TMA bulk copy, then one thread per record
 //                    converts every stream from there (staged; the direct
 //                    typed-load variant remains for unaligned sources).
@@ -1045,6 +1047,57 @@ struct ProcXV {
     }
 };
 
+// The C2 plan ({x f64x3 -> D [+ drift with v], v f32x3 -> D}) on the staged
+// CTA tile with every format fixed at compile time: no per-stream dispatch.
+template <int DB>
+__global__ void __launch_bounds__(256) k_gather_xv_staged(const __grid_constant__ GatherPlan P,
+                                                          const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int db = Ieee<DB>::w / 8;
+    const uint64_t n = P.count, rbytes = P.record_bits >> 3, r0 = uint64_t(blockIdx.x) * 256;
+    const uint32_t nrec = uint32_t(min(uint64_t(256), n - r0));
+    stage_tile<256>(smem, src + r0 * rbytes, uint32_t(nrec * rbytes));
+    if (threadIdx.x >= nrec) return;
+    const GStream& gx = P.s[0];
+    const GStream& gv = P.s[1];
+    const uint64_t r = r0 + threadIdx.x;
+    const uint8_t* rp = smem + 128 + threadIdx.x * rbytes;
+    uint8_t* ox = dst + gx.dst_base + r * 3 * db;
+    uint8_t* ov = dst + gv.dst_base + r * 3 * db;
+    uint64_t xq[3], vq[3];
+    bool bad = false;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        const uint64_t xs = *reinterpret_cast<const uint64_t*>(rp + (gx.src_off >> 3) + 8 * l);
+        const uint32_t vs = *reinterpret_cast<const uint32_t*>(rp + (gv.src_off >> 3) + 4 * l);
+        bad |= Ieee<B_F64>::nan(xs) | Ieee<B_F32>::nan(vs);
+        xq[l] = Ieee<DB>::from(bits_to_f64(xs));
+        vq[l] = cvt_plain<B_F32, DB>(vs);
+    }
+    if (gx.op != OP_COPY) {
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            double v;
+            if (P.math == MATH_FP64_EXACT) v = __dadd_rn(Ieee<DB>::f64(xq[l]), __dmul_rn(Ieee<DB>::f64(vq[l]), P.dt));
+            else v = double(__fadd_rn(float(Ieee<DB>::f64(xq[l])), __fmul_rn(float(Ieee<DB>::f64(vq[l])), float(P.dt))));
+            bad |= isnan(v);
+            xq[l] = Ieee<DB>::from(v);
+        }
+    }
+    if (bad) {  // NaN operands / results: the exact per-lane rule for this record
+        if (gx.op != OP_COPY) stream_fast<B_F64, DB, B_F32>(rp, 0, gx, 0, 1, P.dt, P.math, ox);
+        else stream_fast<B_F64, DB, -1>(rp, 0, gx, 0, 1, P.dt, P.math, ox);
+        stream_fast<B_F32, DB, -1>(rp, 0, gv, 0, 1, P.dt, P.math, ov);
+        return;
+    }
+    using TD = typename std::conditional<db == 4, uint32_t, uint16_t>::type;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        reinterpret_cast<TD*>(ox)[l] = TD(xq[l]);
+        reinterpret_cast<TD*>(ov)[l] = TD(vq[l]);
+    }
+}
+
 template <class Proc>
 __global__ void __launch_bounds__(512, 1) k_gather_warp(const __grid_constant__ GatherPlan P,
                                                         const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
@@ -1441,6 +1494,21 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
                                                src_bytes);
         return cudaGetLastError();
     };
+    const bool xv_plan = p.proc == PROC_XV_F16 || p.proc == PROC_XV_BF16 || p.proc == PROC_XV_F32;
+    if (xv_plan && env_int("SFB_GATHER_XV_STAGED", 1) && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) & 7) == 0 && p.record_bits / 8 <= kRecTileMaxStride) {
+        const size_t xsm = 128 + 256 * size_t(p.record_bits / 8);
+        const unsigned g = unsigned((p.count + 255) / 256);
+        auto xgo = [&](auto kern) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(xsm));
+            if (e != cudaSuccess) return e;
+            kern<<<g, 256, xsm, st>>>(p, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst));
+            return cudaGetLastError();
+        };
+        if (p.proc == PROC_XV_F16) return xgo(k_gather_xv_staged<B_F16>);
+        if (p.proc == PROC_XV_BF16) return xgo(k_gather_xv_staged<B_BF16>);
+        return xgo(k_gather_xv_staged<B_F32>);
+    }
     // many thin COPY streams: direct typed loads, one thread per record
     static const int min_streams = env_int("SFB_GATHER_MULTI_MIN", 1);  // tuning override (3: thin plans via TMA tiles)
     const bool xv = p.proc == PROC_XV_F16 || p.proc == PROC_XV_BF16 || p.proc == PROC_XV_F32;

@@ -10,8 +10,8 @@ summ() {  # summ <key> <header>
 }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/launches.log 2>&1
 echo "launches $?"
-timeout 900 $NCU -k regex:k_gather_multi -s 5 -c 1 -o /tmp/prof/gather python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_gather.log 2>&1
-echo "gather $?"; summ gather "C2 headline step: k_gather_multi<staged> (16M records, 88-B AoS -> SoA binary16 {x,v}, drift fused)"
+timeout 900 $NCU -k regex:k_gather_xv_staged -s 5 -c 1 -o /tmp/prof/gather python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_gather.log 2>&1
+echo "gather $?"; summ gather "C2 headline step: k_gather_xv_staged (16M records, 88-B AoS -> SoA binary16 {x,v}, drift fused)"
 timeout 900 $NCU -k regex:k_scatter_tile -s 3 -c 1 -o /tmp/prof/scatter python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_scatter.log 2>&1
 echo "scatter $?"; summ scatter "C2 scatter-back: k_scatter_tile (binary16 x -> f64 x lanes of the 16M-record AoS)"
 timeout 900 $NCU -k regex:k_gather_multi -s 3 -c 1 -o /tmp/prof/gather_multi python scripts/probe_gather_one.py all > gpurun_out/ncu_gmulti.log 2>&1
