@@ -477,8 +477,9 @@ __device__ __forceinline__ void stage_tile(uint8_t* smem, const uint8_t* g, uint
         if (bulk) tma_bulk_g2s(tile, g, bulk, bar);
     }
     for (uint32_t b = bulk + threadIdx.x; b < bytes; b += T) tile[b] = g[b];
-    __syncthreads();
-    mbar_wait(bar, 0);
+    __syncthreads();                          // the barrier is initialised, the tail is written
+    if (threadIdx.x < 32) mbar_wait(bar, 0);  // one warp polls the TMA barrier ...
+    __syncthreads();                          // ... the others sleep at the CTA barrier (fewer issued instructions)
 }
 
 // After every thread updated its record in the tile: each thread stores the
