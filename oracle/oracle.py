@@ -69,6 +69,8 @@ def lib():
             ("or_density_buffer", None, [P, P, P, u64, u64, i, P]),
             ("or_density_cells", None, [P, P, P, u64, d, d, d, P]),
             ("or_force_cells", i, [P] * 6 + [u64, d, d, d] + [P] * 4),
+            ("or_density_cells_at", None, [P, P, P, u64, d, d, d, P, u64, P]),
+            ("or_force_cells_at", i, [P] * 6 + [u64, d, d, d, P, u64] + [P] * 4),
             ("or_dw_dr", d, [d, d]),
             ("or_random_ics", None, [u64, u64, u64, d] + [P] * 12),
             ("or_fmt_width", i, [i]),
@@ -444,6 +446,28 @@ def force_cells(x, v, m, h, rho, P, lo: float, hi: float, cell: float):
                             _p(a), _p(du), _p(sa), _p(sd)) != 0:
         raise ArithmeticError("force: degenerate state, rho == 0")
     return a.reshape(n, 3), du, sa, sd
+
+
+def density_cells_at(x, m, h, lo: float, hi: float, cell: float, homes) -> np.ndarray:
+    """or_density_cells for the listed homes (indices into x/m/h) only."""
+    x = np.ascontiguousarray(x, np.float64); m = np.ascontiguousarray(m, np.float64)
+    h = np.ascontiguousarray(h, np.float64)
+    homes = np.ascontiguousarray(homes, np.uint64)
+    rho = np.zeros(len(homes), np.float64)
+    lib().or_density_cells_at(_p(x), _p(m), _p(h), len(m), lo, hi, cell, _p(homes), len(homes), _p(rho))
+    return rho
+
+
+def force_cells_at(x, v, m, h, rho, P, lo: float, hi: float, cell: float, homes):
+    """or_force_cells for the listed homes only: (a[k,3], du[k], a_scale[k], du_scale[k])."""
+    x, v, m, h, rho, P = (np.ascontiguousarray(t, np.float64) for t in (x, v, m, h, rho, P))
+    homes = np.ascontiguousarray(homes, np.uint64)
+    k = len(homes)
+    a = np.zeros(3 * k); du = np.zeros(k); sa = np.zeros(k); sd = np.zeros(k)
+    if lib().or_force_cells_at(_p(x), _p(v), _p(m), _p(h), _p(rho), _p(P), len(m), lo, hi, cell, _p(homes), k,
+                               _p(a), _p(du), _p(sa), _p(sd)) != 0:
+        raise ArithmeticError("force: degenerate state, rho == 0")
+    return a.reshape(k, 3), du, sa, sd
 
 
 def w(r: float, h: float) -> float:

@@ -298,16 +298,30 @@ static uint64_t cells_candidates(const CellList* L, uint64_t i, uint64_t** cand,
 /* Cell-linked density: density_kernel's sum (sph.cpp:176-199) over every
  * particle of the 27 cells (side >= 2 h_max) in ascending index — the terms
  * beyond the support are exactly +0.0, so this equals the all-pairs sum. */
+static double density_home(const CellList* L, const double* x, const double* m, const double* h, uint64_t i,
+                           uint64_t** cand, uint64_t* cap) {
+    uint64_t nn = cells_candidates(L, i, cand, cap);
+    double acc = 0.0;
+    for (uint64_t t = 0; t < nn; ++t) acc += pair_term(x, m, h, i, (*cand)[t]);
+    return acc;
+}
+
 void or_density_cells(const double* x, const double* m, const double* h, uint64_t n,
                       double lo, double hi, double cell, double* rho) {
     CellList L = cells_build(x, n, lo, hi, cell);
     uint64_t cap = 1024, *cand = malloc(cap * sizeof(uint64_t));
-    for (uint64_t i = 0; i < n; ++i) {
-        uint64_t nn = cells_candidates(&L, i, &cand, &cap);
-        double acc = 0.0;
-        for (uint64_t t = 0; t < nn; ++t) acc += pair_term(x, m, h, i, cand[t]);
-        rho[i] = acc;
-    }
+    for (uint64_t i = 0; i < n; ++i) rho[i] = density_home(&L, x, m, h, i, &cand, &cap);
+    free(cand);
+    cells_free(&L);
+}
+
+/* The same sum for the listed homes only (every particle stays a candidate):
+ * the parity check of a large population on a sample of homes. */
+void or_density_cells_at(const double* x, const double* m, const double* h, uint64_t n, double lo, double hi,
+                         double cell, const uint64_t* homes, uint64_t nh, double* rho) {
+    CellList L = cells_build(x, n, lo, hi, cell);
+    uint64_t cap = 1024, *cand = malloc(cap * sizeof(uint64_t));
+    for (uint64_t k = 0; k < nh; ++k) rho[k] = density_home(&L, x, m, h, homes[k], &cand, &cap);
     free(cand);
     cells_free(&L);
 }
@@ -329,6 +343,39 @@ double or_dw_dr(double r, double h) {
  * |P_i/rho_i^2| sum_j |m_j (v_i - v_j) . grad W_ij| are the magnitudes the
  * sums cancel from (the scale a floating-point tolerance is relative to).
  * Returns -1 when some rho is 0 (the reference's domain_error), else 0. */
+static void force_home(const CellList* L, const double* x, const double* v, const double* m, const double* h,
+                       const double* rho, const double* P, uint64_t i, uint64_t** cand, uint64_t* cap, double* a,
+                       double* du, double* a_scale, double* du_scale) {
+    uint64_t nn = cells_candidates(L, i, cand, cap);
+    const double pi = P[i] / (rho[i] * rho[i]);
+    double acc[3] = {0.0, 0.0, 0.0}, compr = 0.0, sa = 0.0, sd = 0.0;
+    for (uint64_t t = 0; t < nn; ++t) {
+        const uint64_t j = (*cand)[t];
+        if (j == i) continue;
+        const double d0 = x[3 * i] - x[3 * j], d1 = x[3 * i + 1] - x[3 * j + 1], d2 = x[3 * i + 2] - x[3 * j + 2];
+        const double hij = 0.5 * (h[i] + h[j]);
+        const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+        if (r != 0.0) {
+            const double sc = or_dw_dr(r, hij) / r;
+            g0 = sc * d0; g1 = sc * d1; g2 = sc * d2;
+        }
+        const double pf = pi + P[j] / (rho[j] * rho[j]);
+        acc[0] -= m[j] * pf * g0;
+        acc[1] -= m[j] * pf * g1;
+        acc[2] -= m[j] * pf * g2;
+        const double dv = (v[3 * i] - v[3 * j]) * g0 + (v[3 * i + 1] - v[3 * j + 1]) * g1 +
+                          (v[3 * i + 2] - v[3 * j + 2]) * g2;
+        compr += m[j] * dv;
+        sa += fabs(m[j] * pf) * sqrt(g0 * g0 + g1 * g1 + g2 * g2);
+        sd += fabs(m[j] * dv);
+    }
+    for (int l = 0; l < 3; ++l) a[l] = acc[l];
+    *du = pi * compr;
+    *a_scale = sa;
+    *du_scale = fabs(pi) * sd;
+}
+
 int or_force_cells(const double* x, const double* v, const double* m, const double* h, const double* rho,
                    const double* P, uint64_t n, double lo, double hi, double cell, double* a, double* du,
                    double* a_scale, double* du_scale) {
@@ -336,36 +383,23 @@ int or_force_cells(const double* x, const double* v, const double* m, const doub
         if (rho[i] == 0.0) return -1;
     CellList L = cells_build(x, n, lo, hi, cell);
     uint64_t cap = 1024, *cand = malloc(cap * sizeof(uint64_t));
-    for (uint64_t i = 0; i < n; ++i) {
-        uint64_t nn = cells_candidates(&L, i, &cand, &cap);
-        const double pi = P[i] / (rho[i] * rho[i]);
-        double acc[3] = {0.0, 0.0, 0.0}, compr = 0.0, sa = 0.0, sd = 0.0;
-        for (uint64_t t = 0; t < nn; ++t) {
-            const uint64_t j = cand[t];
-            if (j == i) continue;
-            const double d0 = x[3 * i] - x[3 * j], d1 = x[3 * i + 1] - x[3 * j + 1], d2 = x[3 * i + 2] - x[3 * j + 2];
-            const double hij = 0.5 * (h[i] + h[j]);
-            const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
-            if (r != 0.0) {
-                const double sc = or_dw_dr(r, hij) / r;
-                g0 = sc * d0; g1 = sc * d1; g2 = sc * d2;
-            }
-            const double pf = pi + P[j] / (rho[j] * rho[j]);
-            acc[0] -= m[j] * pf * g0;
-            acc[1] -= m[j] * pf * g1;
-            acc[2] -= m[j] * pf * g2;
-            const double dv = (v[3 * i] - v[3 * j]) * g0 + (v[3 * i + 1] - v[3 * j + 1]) * g1 +
-                              (v[3 * i + 2] - v[3 * j + 2]) * g2;
-            compr += m[j] * dv;
-            sa += fabs(m[j] * pf) * sqrt(g0 * g0 + g1 * g1 + g2 * g2);
-            sd += fabs(m[j] * dv);
-        }
-        for (int l = 0; l < 3; ++l) a[3 * i + l] = acc[l];
-        du[i] = pi * compr;
-        a_scale[i] = sa;
-        du_scale[i] = fabs(pi) * sd;
-    }
+    for (uint64_t i = 0; i < n; ++i)
+        force_home(&L, x, v, m, h, rho, P, i, &cand, &cap, a + 3 * i, du + i, a_scale + i, du_scale + i);
+    free(cand);
+    cells_free(&L);
+    return 0;
+}
+
+/* or_force_cells for the listed homes only (outputs indexed by list slot). */
+int or_force_cells_at(const double* x, const double* v, const double* m, const double* h, const double* rho,
+                      const double* P, uint64_t n, double lo, double hi, double cell, const uint64_t* homes,
+                      uint64_t nh, double* a, double* du, double* a_scale, double* du_scale) {
+    for (uint64_t i = 0; i < n; ++i)
+        if (rho[i] == 0.0) return -1;
+    CellList L = cells_build(x, n, lo, hi, cell);
+    uint64_t cap = 1024, *cand = malloc(cap * sizeof(uint64_t));
+    for (uint64_t k = 0; k < nh; ++k)
+        force_home(&L, x, v, m, h, rho, P, homes[k], &cand, &cap, a + 3 * k, du + k, a_scale + k, du_scale + k);
     free(cand);
     cells_free(&L);
     return 0;

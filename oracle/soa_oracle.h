@@ -69,10 +69,16 @@ void or_density_buffer(const double* x, const double* m, const double* h, uint64
  * all-pairs sum over any candidate superset. */
 void or_density_cells(const double* x, const double* m, const double* h, uint64_t n,
                       double box_lo, double box_hi, double cell, double* rho);
+/* The same sums for the listed homes only (every particle a candidate). */
+void or_density_cells_at(const double* x, const double* m, const double* h, uint64_t n, double lo, double hi,
+                         double cell, const uint64_t* homes, uint64_t nh, double* rho);
 double or_dw_dr(double r, double h);
 int or_force_cells(const double* x, const double* v, const double* m, const double* h, const double* rho,
                    const double* P, uint64_t n, double lo, double hi, double cell, double* a, double* du,
                    double* a_scale, double* du_scale);
+int or_force_cells_at(const double* x, const double* v, const double* m, const double* h, const double* rho,
+                      const double* P, uint64_t n, double lo, double hi, double cell, const uint64_t* homes,
+                      uint64_t nh, double* a, double* du, double* a_scale, double* du_scale);
 
 /* sph.cpp:325-349 (mt19937_64 + libstdc++ uniform_real_distribution);
  * accel_seed != 0 additionally draws a ~ U(-1,1)^3, du ~ U(-1,1). */

@@ -240,6 +240,44 @@ def run_kernel(buf: PackedBuffer, kernel: str, dt: float = 1e-3, buffer_size: in
                                    int(per_access), math, _stream()))
 
 
+def _prec_dtype(prec: int):
+    import torch
+    if prec in (SF_PREC_NATIVE, 32):
+        return torch.float32
+    if prec == 16:
+        return torch.float16
+    if prec == SF_PREC_BF16:
+        return torch.bfloat16
+    raise L.SfInvalidArg(L.SF_INVALID_ARG, "precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16")
+
+
+def _streams(prec: int, **tensors):
+    """The kernels reinterpret each stream's bytes in `prec`: every tensor
+    must be a contiguous CUDA tensor of that dtype."""
+    want = _prec_dtype(prec)
+    for name, t in tensors.items():
+        if not t.is_cuda:
+            raise L.SfInvalidArg(L.SF_INVALID_ARG, f"{name} must be a CUDA tensor")
+        if not t.is_contiguous():
+            raise L.SfInvalidArg(L.SF_INVALID_ARG, f"{name} must be contiguous")
+        if t.dtype != want:
+            raise L.SfInvalidArg(L.SF_INVALID_ARG, f"{name} is {t.dtype}, precision code {prec} needs {want}")
+
+
+def _int32s(**tensors):
+    import torch
+    for name, t in tensors.items():
+        if t is not None and (not t.is_cuda or not t.is_contiguous() or t.dtype != torch.int32):
+            raise L.SfInvalidArg(L.SF_INVALID_ARG, f"{name} must be a contiguous int32 CUDA tensor")
+
+
+def _f32s(**tensors):
+    import torch
+    for name, t in tensors.items():
+        if t is not None and (not t.is_cuda or not t.is_contiguous() or t.dtype != torch.float32):
+            raise L.SfInvalidArg(L.SF_INVALID_ARG, f"{name} must be a contiguous float32 CUDA tensor")
+
+
 def bin_particles(x, lo, cell: float, dims, cell_start=None, perm=None):
     """Counting sort into cells (x-major ids), stable by particle index.
     x: (n,3) float32 cuda tensor.  Returns (cell_start[ncell+1], perm[n])."""
@@ -269,6 +307,9 @@ def density_cells(x, m, h, cell_start, perm, lo, cell: float, dims, n_home=None,
     n = m.shape[0]
     n_home = n if n_home is None else n_home
     rho = rho if rho is not None else torch.zeros(max(n, 1), dtype=torch.float32, device=m.device)
+    _streams(prec, x=x, m=m, h=h)
+    _int32s(cell_start=cell_start, perm=perm)
+    _f32s(rho=rho)
     lo_arr = (C.c_float * 3)(*[float(v) for v in lo])
     check(lib().sf_b200_density_cells(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
                                       _ptr(cell_start), C.cast(lo_arr, C.c_void_p), float(cell), nx, ny, nz, reach,
@@ -290,6 +331,9 @@ def force_cells(x, v, m, h, rho, P, cell_start, perm, lo, cell: float, dims, n_h
     n_home = n if n_home is None else n_home
     a = a if a is not None else torch.zeros((max(n, 1), 3), dtype=torch.float32, device=m.device)
     du = du if du is not None else torch.zeros(max(n, 1), dtype=torch.float32, device=m.device)
+    _streams(prec, x=x, v=v, m=m, h=h, rho=rho, P=P)
+    _int32s(cell_start=cell_start, perm=perm)
+    _f32s(a=a, du=du)
     lo_arr = (C.c_float * 3)(*[float(t) for t in lo])
     check(lib().sf_b200_force_cells(_ptr(x), _ptr(v), _ptr(m), _ptr(h), _ptr(rho), _ptr(P), prec, n,
                                     _ptr(perm) if perm is not None else None, _ptr(cell_start),
@@ -303,6 +347,9 @@ def cells_pack(x, m, h, perm, pos, mass, hmax, prec: int = SF_PREC_NATIVE):
     caller-owned float4 pos (n,4), mass (n,) and hmax (>= 2 int32 words: the h
     range, [0] bits of the largest h, [1] ~bits of the smallest)."""
     n = m.shape[0]
+    _streams(prec, x=x, m=m, h=h)
+    _int32s(perm=perm)
+    _f32s(pos=pos, mass=mass)
     check(lib().sf_b200_cells_pack(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
                                    _ptr(pos), _ptr(mass), _ptr(hmax), _stream()))
 
@@ -335,6 +382,9 @@ def force_pack(v, m, rho, P, perm, vel, pf, prec: int = SF_PREC_NATIVE):
     """(v, m) -> float4 vel (n,4) and P/rho^2 -> pf (n,) in perm's order;
     rho == 0 raises SfError (domain error)."""
     n = m.shape[0]
+    _streams(prec, v=v, m=m, rho=rho, P=P)
+    _int32s(perm=perm)
+    _f32s(vel=vel, pf=pf)
     check(lib().sf_b200_force_pack(_ptr(v), _ptr(m), _ptr(rho), _ptr(P), prec, n,
                                    _ptr(perm) if perm is not None else None, _ptr(vel), _ptr(pf), _stream()))
 

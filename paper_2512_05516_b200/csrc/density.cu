@@ -106,97 +106,6 @@ struct CellGrid {
 // at C5 (128M) fell to 46% (91% uncapped; 54 -> 46 ms).
 static unsigned home_grid(uint64_t n) { return unsigned((n + 255) / 256); }
 
-__global__ void __launch_bounds__(256) k_pairs(const float4* __restrict__ pos,
-                                               const float* __restrict__ mass, const int32_t* __restrict__ cell_start,
-                                               const int32_t* __restrict__ perm, CellGrid G, int64_t n,
-                                               float* __restrict__ rho) {
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i_home = perm ? perm[k] : k;
-        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
-        const float4 pi = (pos[k]);
-        // the same float formula bin_particles used, so the cell matches
-        const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
-        const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
-        const int iz = min(max(int(floorf((pi.z - G.loz) * G.inv_cell)), 0), G.nz - 1);
-        const int z0 = max(iz - G.reach, 0), z1 = min(iz + G.reach, G.nz - 1);
-        float acc = 0.0f;
-        for (int jx = max(ix - G.reach, 0); jx <= min(ix + G.reach, G.nx - 1); ++jx)
-            for (int jy = max(iy - G.reach, 0); jy <= min(iy + G.reach, G.ny - 1); ++jy) {
-                const int64_t c0 = (int64_t(jx) * G.ny + jy) * G.nz;
-                const int b = __ldg(cell_start + c0 + z0), e = __ldg(cell_start + c0 + z1 + 1);
-                for (int j = b; j < e; ++j) {
-                    const float4 pj = (pos[j]);
-                    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-                    const float r2 = dx * dx + dy * dy + dz * dz;
-                    const float hij = 0.5f * (pi.w + pj.w);
-                    if (r2 < 4.0f * hij * hij) {
-                        const float inv_h = __frcp_rn(hij);
-                        const float q = sqrtf(r2) * inv_h;
-                        if (q < 2.0f) acc += __ldg(mass + j) * w_f32(q, inv_h);
-                    }
-                }
-            }
-        rho[i_home] = acc;
-    }
-}
-
-// Same pair loop with the reach fixed at compile time: the (2R+1) run bounds
-// of a neighbour row are loaded together (independent loads in flight), and
-// candidates are consumed two at a time.
-template <int R>
-__global__ void __launch_bounds__(256) k_pairs_r(const float4* __restrict__ pos,
-                                                 const float* __restrict__ mass,
-                                                 const int32_t* __restrict__ cell_start,
-                                                 const int32_t* __restrict__ perm, CellGrid G, int64_t n,
-                                                 float* __restrict__ rho) {
-    constexpr int W = 2 * R + 1;
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i_home = perm ? perm[k] : k;
-        if (i_home >= G.n_home) continue;  // ghosts: neighbours only
-        const float4 pi = (pos[k]);
-        const int ix = min(max(int(floorf((pi.x - G.lox) * G.inv_cell)), 0), G.nx - 1);
-        const int iy = min(max(int(floorf((pi.y - G.loy) * G.inv_cell)), 0), G.ny - 1);
-        const int iz = min(max(int(floorf((pi.z - G.loz) * G.inv_cell)), 0), G.nz - 1);
-        const int z0 = max(iz - R, 0), z1 = min(iz + R, G.nz - 1);
-        float acc = 0.0f;
-        auto pair = [&](const float4 pj, int j) {
-            const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-            const float r2 = dx * dx + dy * dy + dz * dz;
-            const float s = pi.w + pj.w;  // 2 h_ij: the support radius
-            if (r2 < s * s) {             // == r2 < 4 h_ij^2 bit for bit (power-of-two rescale)
-                const float inv_h = 2.0f * __frcp_rn(s);
-                const float q = sqrtf(r2) * inv_h;
-                if (q < 2.0f) acc += __ldg(mass + j) * w_f32(q, inv_h);
-            }
-        };
-#pragma unroll 1
-        for (int dxi = -R; dxi <= R; ++dxi) {
-            const int jx = ix + dxi;
-            if (jx < 0 || jx >= G.nx) continue;
-            int b[W], e[W];
-#pragma unroll
-            for (int t = 0; t < W; ++t) {
-                const int jy = iy - R + t;
-                const bool ok = jy >= 0 && jy < G.ny;
-                const int64_t c0 = (int64_t(jx) * G.ny + (ok ? jy : 0)) * G.nz;
-                b[t] = ok ? __ldg(cell_start + c0 + z0) : 0;
-                e[t] = ok ? __ldg(cell_start + c0 + z1 + 1) : 0;
-            }
-#pragma unroll
-            for (int t = 0; t < W; ++t) {
-                int j = b[t];
-                for (; j + 1 < e[t]; j += 2) {
-                    const float4 p0 = (pos[j]), p1 = (pos[j + 1]);
-                    pair(p0, j);
-                    pair(p1, j + 1);
-                }
-                if (j < e[t]) pair((pos[j]), j);
-            }
-        }
-        rho[i_home] = acc;
-    }
-}
-
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -368,11 +277,6 @@ __global__ void __launch_bounds__(256) k_pairs_c(const BlockSet B, const int32_t
     }
 }
 
-static int env_int_d(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
-
 static void launch_pairs(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach, float* rho,
                          cudaStream_t st) {
     const unsigned grid = home_grid(uint64_t(n));
@@ -406,21 +310,11 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
     else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
     else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
-    // SFB_PAIRS=0 selects the unculled per-run loop (round-1 kernel) for comparison
-    const unsigned hgrid = home_grid(n);
-    if (env_int_d("SFB_PAIRS", 1) != 0) {
-        BlockSet B{};
-        B.b[0] = CellBlock{pos, mass, cell_start, hmax, 0, nx, lo[0]};
-        B.nb = 1;
-        B.NX = nx;
-        launch_pairs(B, perm, G, nn, reach, rho, st);
-    } else if (reach == 1) {
-        k_pairs_r<1><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
-    } else if (reach == 2) {
-        k_pairs_r<2><<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
-    } else {
-        k_pairs<<<blocks, 256, 0, st>>>(pos, mass, cell_start, perm, G, nn, rho);
-    }
+    BlockSet B{};
+    B.b[0] = CellBlock{pos, mass, cell_start, hmax, 0, nx, lo[0]};
+    B.nb = 1;
+    B.NX = nx;
+    launch_pairs(B, perm, G, nn, reach, rho, st);
     check_cuda(cudaGetLastError(), "density_cells launch");
     count_launches(2);
     check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
@@ -642,15 +536,10 @@ __global__ void __launch_bounds__(256) k_force_c(const ForceBlockSet B, const in
 static void launch_force(const ForceBlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
                          float* a, float* du, cudaStream_t st) {
     const unsigned grid = home_grid(uint64_t(n));
-    auto go = [&](auto u) {
-        constexpr int U = decltype(u)::value;
-        if (reach == 1) k_force_c<1, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-        else if (reach == 2) k_force_c<2, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-        else if (reach == 3) k_force_c<3, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-        else k_force_c<4, U><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-    };
-    if (env_int_d("SFB_FORCE_UNROLL", 2) == 2) go(std::integral_constant<int, 2>{});
-    else go(std::integral_constant<int, 1>{});
+    if (reach == 1) k_force_c<1, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+    else if (reach == 2) k_force_c<2, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+    else if (reach == 3) k_force_c<3, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+    else k_force_c<4, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
 }
 
 // (v, m) and P/rho^2 of a packed block, in its cell-sorted order; rho == 0 sets *zero

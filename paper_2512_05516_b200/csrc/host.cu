@@ -41,6 +41,7 @@ struct DeviceSlots {
     std::vector<void*> aos, soa;
     std::vector<cudaStream_t> streams;
     size_t aos_bytes = 0, soa_bytes = 0;
+    int device = -1;  // the device the slots and streams belong to
     ~DeviceSlots() {
         for (void* p : aos) cudaFree(p);
         for (void* p : soa) cudaFree(p);
@@ -113,8 +114,15 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
     static thread_local std::unique_ptr<DeviceSlots> pool;
     const size_t aos_bytes = size_t((chunk * rb + 7) / 8) + 16;
     const size_t soa_bytes = size_t(with_count(dst, chunk).total_bytes()) + 16;
-    if (!pool || pool->aos_bytes < aos_bytes || pool->soa_bytes < soa_bytes) {
+    if (!pool || pool->device != dev || pool->aos_bytes < aos_bytes || pool->soa_bytes < soa_bytes) {
+        if (pool && pool->device != dev) {  // free the old device's slots on that device
+            int cur = dev;
+            check_cuda(cudaSetDevice(pool->device), "set device");
+            pool.reset();
+            check_cuda(cudaSetDevice(cur), "set device");
+        }
         pool.reset(new DeviceSlots());
+        pool->device = dev;
         pool->aos_bytes = aos_bytes;
         pool->soa_bytes = soa_bytes;
         for (int s = 0; s < slots; ++s) {

@@ -311,10 +311,6 @@ __device__ __forceinline__ uint64_t axpy_ieee(uint64_t xq, uint64_t yq, double d
     return Ieee<DB>::from(r);
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 void count_launches(uint64_t n);  // runtime.cpp
 int num_sms();                    // runtime.cpp
 
@@ -441,7 +437,7 @@ static void launch_convert_ieee_s(const CStream& c, uint64_t n, const uint8_t* s
     // sector read-patch-write for 8-B lanes in wide records (neighbouring records' sectors disjoint)
     const uint64_t span = uint64_t(c.dst.arity) * 8;
     if (ieee_code(c.dst.fmt) == B_F64 && c.dst.arity <= 3 && c.dst.stride / 8 >= span + 64 &&
-        (reinterpret_cast<uintptr_t>(dst) & 31) == 0 && env_int("SFB_SCATTER_SECTORS", 1)) {
+        (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
         const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
         if (c.dst.arity == 3)
             k_scatter_sectors<SB, 3><<<g, 256, 0, st>>>(src, c.src.base / 8, c.src.stride / 8, dst, c.dst.base / 8,
@@ -733,7 +729,7 @@ static uint8_t scatter_kind(const CStream& c) {
 // k_scatter_tile for a plan whose destination is one AoS record layout (every
 // stream inside the same record stride); false when it does not qualify.
 static bool launch_scatter_tile(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st, cudaError_t* err) {
-    if (!env_int("SFB_SCATTER_TILE", 1) || src == dst || p.n == 0 || (reinterpret_cast<uintptr_t>(dst) & 31) ||
+    if (src == dst || p.n == 0 || (reinterpret_cast<uintptr_t>(dst) & 31) ||
         (reinterpret_cast<uintptr_t>(src) & 7))
         return false;
     const uint64_t S = p.s[0].dst.stride;
@@ -970,81 +966,6 @@ struct ProcGeneric {
             warp_store(dst + g.dst_base + rec0 * g.arity * db, out, recs * g.arity * db, db, lane);
             __syncwarp();
         }
-    }
-};
-
-// ProcXV<DB>: the drift-set shape (view.cpp proc_kind) — stream 0 = x (f64 x3,
-// copied or drifted with stream 1's source as operand), stream 1 = v
-// (f32 x3), both to DB.  One record per lane, all six lanes in registers;
-// NaN operands / NaN results redo the tile through the exact path.
-template <int DB>
-struct ProcXV {
-    __device__ static void tile(const uint8_t* tile, const GatherPlan& P, uint32_t lane, uint32_t recs, uint64_t rec0,
-                                uint8_t* out, uint8_t* dst) {
-        constexpr int db = Ieee<DB>::w / 8;
-        const GStream& gx = P.s[0];
-        const GStream& gv = P.s[1];
-        const uint32_t rbytes = P.record_bits >> 3;
-        uint8_t* ox = out;
-        uint8_t* ov = out + 32 * 3 * db;
-        const bool axpy = gx.op != OP_COPY;
-        bool bad = false;
-        if (lane < recs) {
-            const uint8_t* rp = tile + lane * rbytes;
-            uint64_t xs[3];
-            uint32_t vs[3];
-            uint64_t xq[3], vq[3];
-#pragma unroll
-            for (int l = 0; l < 3; ++l) {
-                xs[l] = *reinterpret_cast<const uint64_t*>(rp + (gx.src_off >> 3) + 8 * l);
-                vs[l] = *reinterpret_cast<const uint32_t*>(rp + (gv.src_off >> 3) + 4 * l);
-            }
-#pragma unroll
-            for (int l = 0; l < 3; ++l) {
-                bad |= Ieee<B_F64>::nan(xs[l]) | Ieee<B_F32>::nan(vs[l]);
-                xq[l] = Ieee<DB>::from(bits_to_f64(xs[l]));
-                if constexpr (DB == B_F16) {
-                    const __half h = __float2half_rn(bits_to_f32(vs[l]));
-                    vq[l] = *reinterpret_cast<const uint16_t*>(&h);
-                } else if constexpr (DB == B_BF16) {
-                    const __nv_bfloat16 h = __float2bfloat16_rn(bits_to_f32(vs[l]));
-                    vq[l] = *reinterpret_cast<const uint16_t*>(&h);
-                } else {
-                    vq[l] = vs[l];
-                }
-            }
-            if (axpy) {
-#pragma unroll
-                for (int l = 0; l < 3; ++l) {
-                    double r;
-                    if (P.math == MATH_FP64_EXACT)
-                        r = __dadd_rn(Ieee<DB>::f64(xq[l]), __dmul_rn(Ieee<DB>::f64(vq[l]), P.dt));
-                    else
-                        r = double(__fadd_rn(float(Ieee<DB>::f64(xq[l])), __fmul_rn(float(Ieee<DB>::f64(vq[l])), float(P.dt))));
-                    bad |= isnan(r);
-                    xq[l] = Ieee<DB>::from(r);
-                }
-            }
-#pragma unroll
-            for (int l = 0; l < 3; ++l) {
-                if constexpr (db == 4) {
-                    reinterpret_cast<uint32_t*>(ox)[3 * lane + l] = uint32_t(xq[l]);
-                    reinterpret_cast<uint32_t*>(ov)[3 * lane + l] = uint32_t(vq[l]);
-                } else {
-                    reinterpret_cast<uint16_t*>(ox)[3 * lane + l] = uint16_t(xq[l]);
-                    reinterpret_cast<uint16_t*>(ov)[3 * lane + l] = uint16_t(vq[l]);
-                }
-            }
-        }
-        if (__any_sync(0xffffffffu, bad)) {
-            if (axpy) stream_fast<B_F64, DB, B_F32>(tile, rbytes, gx, lane, recs, P.dt, P.math, ox);
-            else stream_fast<B_F64, DB, -1>(tile, rbytes, gx, lane, recs, P.dt, P.math, ox);
-            stream_fast<B_F32, DB, -1>(tile, rbytes, gv, lane, recs, P.dt, P.math, ov);
-        }
-        __syncwarp();
-        warp_store(dst + gx.dst_base + rec0 * 3 * db, ox, recs * 3 * db, db, lane);
-        warp_store(dst + gv.dst_base + rec0 * 3 * db, ov, recs * 3 * db, db, lane);
-        __syncwarp();
     }
 };
 
@@ -1373,11 +1294,10 @@ __device__ __forceinline__ double dwdr_exact(double r, double h) {
     return __dmul_rn(norm, __dmul_rn(__dmul_rn(-0.75, t), t));
 }
 
-__device__ int g_force_degenerate;  // set when a particle has rho == 0 (domain_error)
 
 // force_kernel (sph.cpp:201-245): symmetric pressure force and du, j ascending,
 // self pair skipped; PerAccess quantizes a after every neighbour.
-__global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf) {
+__global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf, int* __restrict__ degenerate) {
     extern __shared__ double sf[];
     const uint32_t bs = P.bs;
     double* sx = sf;            // 3 bs
@@ -1399,7 +1319,7 @@ __global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf
     sP[i] = ld_lane(buf, P.P, gi, 0);
     __syncthreads();
     const double rho_i = srho[i];
-    if (rho_i == 0.0) atomicOr(&g_force_degenerate, 1);
+    if (rho_i == 0.0) atomicOr(degenerate, 1);
     const double pi_rho2 = __ddiv_rn(sP[i], __dmul_rn(rho_i, rho_i));
     double acc[3] = {0.0, 0.0, 0.0}, compr = 0.0;
     for (uint32_t j = 0; j < bs; ++j) {
@@ -1416,7 +1336,7 @@ __global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf
             g2 = __dmul_rn(s, d2);
         }
         const double mj = sm[j], rho_j = srho[j];
-        if (rho_j == 0.0) atomicOr(&g_force_degenerate, 1);
+        if (rho_j == 0.0) atomicOr(degenerate, 1);
         const double pf = __dadd_rn(pi_rho2, __ddiv_rn(sP[j], __dmul_rn(rho_j, rho_j)));
         const double mpf = __dmul_rn(mj, pf);
         acc[0] = __dsub_rn(acc[0], __dmul_rn(mpf, g0));
@@ -1442,7 +1362,7 @@ cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cud
     if (p.count == 0 || p.n == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     if (launch_scatter_tile(p, src, dst, st, &err)) return err;  // into AoS records: one staged pass
-    bool typed = env_int("SFB_CONVERT_TYPED", 1) != 0;
+    bool typed = true;
     for (uint32_t i = 0; i < p.n && typed; ++i) typed = convert_ieee_ok(p.s[i], src, dst);
     if (typed && src != dst) {  // per stream; in place (src == dst) keeps the one-pass generic kernel
         const uint64_t want = (p.count + 4 * 256 - 1) / (4 * 256);
@@ -1476,12 +1396,10 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
                           int /*ctas_per_sm*/) {
     if (plan.count == 0 || plan.n == 0) return cudaSuccess;
     GatherPlan p = plan;
-    // tuning overrides (ring depth per warp, warps per CTA) for sweeps
-    p.stages = uint8_t(std::min(8, std::max(2, env_int("SFB_GATHER_STAGES", kWStages))));
+    p.stages = uint8_t(kWStages);
     const size_t per_warp = gather_warp_bytes(p);
     const size_t budget = 220 * 1024;
     int warps = int(std::min<size_t>(16, (budget - 1024) / per_warp));
-    warps = std::min(warps, std::max(1, env_int("SFB_GATHER_WARPS", warps)));
     if (warps < 1) return cudaErrorInvalidValue;
     const size_t smem = 128 * ((size_t(warps) * p.stages * 8 + 127) / 128) + size_t(warps) * per_warp;
     const uint64_t ntiles = (p.count + p.tile_recs - 1) / p.tile_recs;
@@ -1496,7 +1414,7 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
         return cudaGetLastError();
     };
     const bool xv_plan = p.proc == PROC_XV_F16 || p.proc == PROC_XV_BF16 || p.proc == PROC_XV_F32;
-    if (xv_plan && env_int("SFB_GATHER_XV_STAGED", 1) && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+    if (xv_plan && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(dst) & 7) == 0 && p.record_bits / 8 <= kRecTileMaxStride) {
         const size_t xsm = 128 + 256 * size_t(p.record_bits / 8);
         const unsigned g = unsigned((p.count + 255) / 256);
@@ -1510,12 +1428,9 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
         if (p.proc == PROC_XV_BF16) return xgo(k_gather_xv_staged<B_BF16>);
         return xgo(k_gather_xv_staged<B_F32>);
     }
-    // many thin COPY streams: direct typed loads, one thread per record
-    static const int min_streams = env_int("SFB_GATHER_MULTI_MIN", 1);  // tuning override (3: thin plans via TMA tiles)
-    const bool xv = p.proc == PROC_XV_F16 || p.proc == PROC_XV_BF16 || p.proc == PROC_XV_F32;
-    if ((min_streams <= 1 || (!xv && int(p.n) >= min_streams)) &&
-        env_int("SFB_GATHER_MULTI", 1) && (reinterpret_cast<uintptr_t>(src) & 7) == 0 &&
-        (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+    // any plan of plain IEEE lanes: one thread per record (staged CTA tile, or
+    // direct typed loads for records wider than the tile limit)
+    if ((reinterpret_cast<uintptr_t>(src) & 7) == 0 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
         bool ok = true;
         for (uint32_t i = 0; i < p.n && ok; ++i) ok = (p.s[i].mkind = multi_kind(p.s[i], p.record_bits)) != 0;
         if (ok)  // group equal kinds (every stream writes its own SoA range, so the order is free)
@@ -1524,8 +1439,7 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
             // one thread per record, uncapped grid: CTAs in flight cover one compact record range
             const int mb = int((p.count + 255) / 256);
             const size_t rbytes = p.record_bits / 8, smem = 128 + 256 * rbytes;
-            if (p.record_bits % 8 == 0 && rbytes <= kRecTileMaxStride && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
-                env_int("SFB_GATHER_MULTI_STAGED", 1)) {
+            if (p.record_bits % 8 == 0 && rbytes <= kRecTileMaxStride && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
                 cudaError_t e = cudaFuncSetAttribute(k_gather_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      int(smem));
                 if (e != cudaSuccess) return e;
@@ -1537,12 +1451,7 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
             return cudaGetLastError();
         }
     }
-    switch (p.proc) {
-        case PROC_XV_F16: return go(k_gather_warp<ProcXV<B_F16>>);
-        case PROC_XV_BF16: return go(k_gather_warp<ProcXV<B_BF16>>);
-        case PROC_XV_F32: return go(k_gather_warp<ProcXV<B_F32>>);
-        default: return go(k_gather_warp<ProcGeneric>);
-    }
+    return go(k_gather_warp<ProcGeneric>);  // truncated / bit-packed lanes
 }
 
 __device__ __forceinline__ LaneFmt ieee_fmt(int b) { return b == B_BF16 ? fmt_bf16() : fmt_native(base_width(b)); }
@@ -1656,19 +1565,40 @@ cudaError_t launch_permute(const PermutePlan& p, const void* src, void* dst, con
     return cudaGetLastError();
 }
 
+// Opt a kernel into more than the default 48 KB of dynamic shared memory,
+// once per (kernel, device).
+template <typename K>
+static cudaError_t smem_opt_in(K kern, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
+
+// rho == 0 anywhere -> *degenerate (the reference's domain_error).  The flag
+// is a stream-ordered allocation of this launch, so concurrent calls on other
+// streams or threads never see each other's flag.
 cudaError_t launch_force_buffer(const ForcePlan& p, void* buf, cudaStream_t st, bool* degenerate) {
-    if (p.count == 0) {
-        *degenerate = false;
-        return cudaSuccess;
+    *degenerate = false;
+    if (p.count == 0) return cudaSuccess;
+    static std::atomic<uint64_t> attr_done{0};
+    cudaError_t e = smem_opt_in(k_force_buffer, int(10 * 1024 * sizeof(double)), attr_done);  // bs <= 1024 threads
+    if (e != cudaSuccess) return e;
+    int* flag_dev = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&flag_dev), sizeof(int), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(flag_dev, 0, sizeof(int), st)) == cudaSuccess) {
+        k_force_buffer<<<unsigned(p.count / p.bs), p.bs, 10 * p.bs * sizeof(double), st>>>(
+            p, static_cast<uint8_t*>(buf), flag_dev);
+        e = cudaGetLastError();
     }
-    int zero = 0, flag = 0;
-    cudaError_t e = cudaMemcpyToSymbolAsync(g_force_degenerate, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return e;
-    k_force_buffer<<<unsigned(p.count / p.bs), p.bs, 10 * p.bs * sizeof(double), st>>>(p, static_cast<uint8_t*>(buf));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    e = cudaMemcpyFromSymbolAsync(&flag, g_force_degenerate, sizeof(int), 0, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(st);
+    int flag = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(flag_dev, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     *degenerate = flag != 0;
     return e;
 }
@@ -1708,26 +1638,14 @@ cudaError_t launch_update_rec_multi(int xb, int yb, void* buf, uint64_t n, uint3
 cudaError_t launch_update_rec_tile(void* buf, uint64_t n, uint32_t stride, const RecSeq& seq, double dt,
                                    uint8_t math, uint32_t wlo, uint32_t whi, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    static const int R = env_int("SFB_REC_TILE_RECS", 128) == 256 ? 256 : 128;  // records (threads) per CTA
-    static std::atomic<uint64_t> attr_done{0};  // per device: the >48 KB shared-memory opt-in
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    // 128 records (threads) per CTA: 32..256 measured flat at C1
+    constexpr int R = 128;
+    static std::atomic<uint64_t> attr_done{0};
+    cudaError_t e = smem_opt_in(k_update_rec_tile<R>, int(128 + R * kRecTileMaxStride), attr_done);
     if (e != cudaSuccess) return e;
-    const uint64_t bit = 1ull << (dev & 63);
-    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
-        e = cudaFuncSetAttribute(k_update_rec_tile<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(128 + 128 * kRecTileMaxStride));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_update_rec_tile<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(128 + 256 * kRecTileMaxStride));
-        if (e != cudaSuccess) return e;
-        attr_done.fetch_or(bit, std::memory_order_release);
-    }
     const size_t smem = 128 + size_t(R) * stride;
     const unsigned blocks = unsigned((n + R - 1) / R);
-    uint8_t* b = static_cast<uint8_t*>(buf);
-    if (R == 128) k_update_rec_tile<128><<<blocks, 128, smem, st>>>(b, n, stride, seq, dt, math, wlo, whi);
-    else k_update_rec_tile<256><<<blocks, 256, smem, st>>>(b, n, stride, seq, dt, math, wlo, whi);
+    k_update_rec_tile<R><<<blocks, R, smem, st>>>(static_cast<uint8_t*>(buf), n, stride, seq, dt, math, wlo, whi);
     return cudaGetLastError();
 }
 

@@ -129,12 +129,8 @@ bool rec_op_ok(const View& v, const CStream& c, const void* p) {
 // The ops of one or more kick/drift kernels in one shared-memory pass over the
 // AoS records (k_update_rec_tile); false when the layout does not qualify.
 bool rec_tile(const View& v, void* p, const std::vector<CStream>& ops, double dt, uint8_t math, cudaStream_t st) {
-    static const bool on = [] {
-        const char* e = std::getenv("SFB_REC_TILE");
-        return !e || std::atoi(e) != 0;
-    }();
     const uint64_t stride = v.record_bits() / 8;
-    if (!on || v.layout != Layout::AoS || !v.byte_aligned() || ops.empty() || ops.size() > size_t(kMaxSeq) ||
+    if (v.layout != Layout::AoS || !v.byte_aligned() || ops.empty() || ops.size() > size_t(kMaxSeq) ||
         stride == 0 || stride > kRecTileMaxStride || (reinterpret_cast<uintptr_t>(p) & 31) != 0)
         return false;
     for (const auto& c : ops)

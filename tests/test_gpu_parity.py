@@ -999,3 +999,23 @@ def test_random_cell_density_and_force_vs_oracle(seed):
     want_a, want_du, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rd, Pd, 0.0, 1.0, 1.0 / nc)
     assert np.all(np.linalg.norm(a.double().cpu().numpy() - want_a, axis=1) <= FORCE_TOL * sa)
     assert np.all(np.abs(du.double().cpu().numpy() - want_du) <= FORCE_TOL * sd + 1e-30)
+
+
+@pytest.mark.skipif(not O.RefLib.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("bs", [616, 1024])
+def test_force_large_buffers_match_live_reference(bs):
+    """Buffer-mode density + force with buffers above the 48 KB default of
+    dynamic shared memory (force stages 80 B per particle): bit for bit."""
+    n = bs * 4
+    R = O.RefLib()
+    h = R.from_ics(n, 42, 0, "", None, 43, 1e-3)
+    start = R.bytes(h)
+    R.run_kernel(h, "density", bs, 1e-3)
+    R.run_kernel(h, "force", bs, 1e-3)
+    want = R.bytes(h)
+    R.free(h)
+    P = api.Schema.default()
+    buf = api.PackedBuffer.from_host(api.View(P, n, "aos"), start)
+    api.run_kernel(buf, "density", 1e-3, buffer_size=bs)
+    api.run_kernel(buf, "force", 1e-3, buffer_size=bs)
+    np.testing.assert_array_equal(host(buf), want)

@@ -216,3 +216,20 @@ def test_cell_oracles_pinned_to_reference_all_pairs():
     assert np.array_equal(out[:, 13:16], a) and np.array_equal(out[:, 16], du)
     assert np.all(sa > 0) and np.all(sd >= 0)
     R.free(hb)
+
+
+def test_cell_oracle_subsets_equal_full_population():
+    """or_density_cells_at / or_force_cells_at (the large-size parity
+    checkers) equal the full-population oracle at the listed homes."""
+    rng = np.random.default_rng(4)
+    n = 4000
+    x = rng.random((n, 3)).reshape(-1)
+    m, h = rng.uniform(0.5, 1.5, n) / n, rng.uniform(0.04, 0.06, n)
+    v, rho, P = rng.uniform(-1, 1, 3 * n), rng.uniform(0.5, 1.5, n), rng.uniform(0.2, 1.0, n)
+    homes = rng.choice(n, 300, replace=False)
+    full = O.density_cells(x, m, h, 0.0, 1.0, 0.125)
+    np.testing.assert_array_equal(O.density_cells_at(x, m, h, 0.0, 1.0, 0.125, homes), full[homes])
+    fa = O.force_cells(x, v, m, h, rho, P, 0.0, 1.0, 0.125)
+    sa = O.force_cells_at(x, v, m, h, rho, P, 0.0, 1.0, 0.125, homes)
+    for a, b in zip(fa, sa):
+        np.testing.assert_array_equal(a[homes], b)
