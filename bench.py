@@ -14,6 +14,13 @@ max over ranks.  `e2e` is the same step through the C ABI with HOST buffers
 (pinned AoS in, SoA out, chunked H2D/compute/D2H pipeline inside the timed
 region).  `--impl reference` times the unmodified reference (oracle/_ref) on
 this host's cores for the same composition.
+
+`--gpus N` (N > 1) without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL).  The default line also
+carries the other BASELINE configs and the paper's measurements as extra
+keys (skip them with --no-extras): configs.c1 / c3 / c4 (each with its own
+roofline and cpu_baseline), sharded_c5 (the 128M cell-sharded timestep at
+every N, strong scaling, per-phase ms), soa_vs_aos, transform and timestep.
 """
 import argparse
 import json
@@ -156,6 +163,28 @@ def cpu_c3_port_rate(n_total, sample=1 << 16, seed=5):
     return sample / secs, secs
 
 
+def cpu_reference_kernels_rate(n, kernels, threads, T=32, layout="soa", seed=42):
+    """The unmodified reference's own kernels (run_kernel_chunked, 64-particle
+    buffers, binary64) on `threads` host threads over an n-particle population
+    stored at T (x kept f64) and unpacked to `layout`: particles per second of
+    the whole kernel list (e.g. density,force,kick,drift = one timestep)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.RefLib.available():
+        raise RuntimeError("oracle/_ref/libref_driver.so missing (run `make -C oracle`)")
+    R = O.RefLib()
+    h = R.from_ics(n, seed, T, "x", None, 43, 1e-3)
+    u = R.op(h, "unpack")
+    buf = R.op(u, "aos_to_soa") if layout == "soa" else u
+    R.run_kernel(buf, kernels[0], 64, 1e-3, threads=threads)  # warm-up: pages touched
+    t0 = time.perf_counter()
+    for k in kernels:
+        R.run_kernel(buf, k, 64, 1e-3, threads=threads)
+    secs = time.perf_counter() - t0
+    R.free(*([h, u, buf] if buf is not u else [h, u]))
+    return n / secs, secs
+
+
 def _bench_kernels_csv(lib_path, particles, threads):
     """Run a library's sf_run_bench_kernels (bench.cpp:269-316 semantics)."""
     import ctypes as C
@@ -245,7 +274,7 @@ def reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference random_initial_conditions, seed 42+thread)",
-            "config": config(N_DEFAULT, world, "binary16"),
+            "config": dict(config(N_DEFAULT, world, "binary16"), reference_sample_particles_per_step=total),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -406,17 +435,184 @@ def b200_arm(args):
         except Exception as ex:
             cpu["per_mode"] = {"unavailable": str(ex)}
 
+    extras = {}
+    if not args.no_extras:
+        del out, src
+        torch.cuda.empty_cache()
+        extras = run_extras(args, world, rank, peak, peak_kind)
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform random records, device RNG)",
                 "config": config(n, world, prec_name), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "impl": "b200", "scatter_back": scatter}
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+FP32_LANES_PER_SM = 128  # FFMA lanes per SM (B200): FP32 peak = SMs x 128 x 2 flop x clock
+
+
+def fp32_peak_tflops(clock_mhz=None):
+    import torch
+    props = torch.cuda.get_device_properties(0)
+    mhz = clock_mhz or 1965.0
+    return props.multi_processor_count * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
+
+
+def ncu_metrics(name):
+    """Per-kernel ncu metrics committed under profiles/ (issue activity, SIMD
+    efficiency, L2 hit rate, occupancy); None when not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "kernel_metrics.json")) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def compute_roofline(kernel, pairs, flops_per_pair, ms, metrics_key):
+    """Useful-flop roofline of an issue-bound pair loop: in-support pairs x
+    flops per pair / kernel time against the FP32 (non-tensor) peak."""
+    ach = pairs * flops_per_pair / (ms * 1e-3) / 1e12
+    peak = fp32_peak_tflops()
+    rl = {"bound": "fp32 issue (FFMA + MUFU, no tensor-core contraction)", "achieved": ach, "peak": peak,
+          "unit": "TFLOP/s", "frac": ach / peak, "kernel": kernel, "flops_per_pair": flops_per_pair,
+          "pairs_per_s": pairs / (ms * 1e-3),
+          "peak_kind": "148 SMs x 128 FFMA lanes x 2 flop x 1965 MHz (B200 max SM clock)", "traffic": None}
+    m = ncu_metrics(metrics_key)
+    if m:
+        rl["ncu"] = m
+    return rl
+
+
+def run_extras(args, world, rank, peak, peak_kind):
+    """The other BASELINE configs and the paper's measurements, as extra keys
+    of the default line.  N=1: everything; N>1: the sharded C5 only (all
+    ranks take part)."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "benchmarks"))
+    import workloads as W
+    ex = {}
+
+    def guard(name, fn, into=ex):
+        t0 = time.time()
+        try:
+            r = fn()
+        except Exception as e:  # reported, never fatal
+            r = {"unavailable": "%s: %s" % (type(e).__name__, str(e)[:300])}
+        r["bench_seconds"] = round(time.time() - t0, 2)
+        into[name] = r
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    threads = os.cpu_count() or 1
+    sub = argparse.Namespace(**vars(args))
+    sub.steps, sub.warmup = min(args.steps, 10), max(3, min(args.warmup, 3))
+    if world == 1:
+        configs = {}
+
+        def c1():
+            r = W.c1(sub, peak, peak_kind)
+            if not args.no_cpu:
+                rate, secs = cpu_c1_rate(1 << 20, threads)
+                r["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                                     "sample": "the full C1 workload: the reference's kick then drift on 1M "
+                                               "default-AoS particles, %.3f s" % secs}
+            return r
+
+        def c3():
+            r = W.c3(sub, peak, peak_kind)
+            k = r["kernels"]
+            pairs = k["fp32"]["pairs_in_support"]
+            r["roofline"] = compute_roofline("k_pairs_c (fp32, reach %d)" % args.refine, pairs, 24,
+                                             k["fp32"]["density_ms"], "pairs_c3_fp32")
+            r["roofline_force"] = compute_roofline("k_force_c (fp32)", pairs, 40, k["force_fp32"]["force_ms"],
+                                                   "force_c3_fp32")
+            r["hbm_frac_fp32"] = k["fp32"]["hbm_GBps_algorithmic"] / peak
+            if not args.no_cpu:
+                rate, secs = cpu_reference_kernels_rate(1 << 20, ["density"], threads, T=32, layout="soa")
+                r["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                                     "sample": "the reference's own density_kernel (64-particle buffers, "
+                                               "binary64, 64 pairs per particle) on a 1M-particle T=32 SoA, "
+                                               "%d threads, %.2f s" % (threads, secs)}
+                prate, psecs = cpu_c3_port_rate(1 << 22)
+                r["cpu_baseline"]["port_cell_linked"] = {
+                    "value": prate, "cores": 1, "kind": "port",
+                    "sample": "cell-linked density of the oracle's C restatement, 65536 particles at C3's "
+                              "density and h, one core, %.2f s" % psecs}
+            return r
+
+        def c4():
+            pk = W.pcie_peaks()
+            r = W.c4(sub, peak, peak_kind)
+            ach = r["roofline"]["achieved"]
+            r["roofline"].update({"peak": pk["bidirectional_GBps"], "frac": ach / pk["bidirectional_GBps"],
+                                  "peak_kind": "measured: " + pk["method"]})
+            r["pcie"] = pk
+            if not args.no_cpu:
+                rate, secs = cpu_c1_rate(1 << 22, threads, kernels=("drift",))
+                r["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                                     "sample": "extrapolated per particle: the reference's drift step on a "
+                                               "4M-particle host AoS (no transfers), %.3f s" % secs}
+            return r
+
+        guard("c1", c1, configs)
+        guard("c3", c3, configs)
+        guard("c4", c4, configs)
+        ex["configs"] = configs
+        guard("soa_vs_aos", lambda: W.soa_vs_aos(sub))
+        guard("transform", lambda: W.transform_placement(sub, ROOT))
+        guard("timestep", lambda: W.timestep_pipeline(sub))
+    guard("sharded_c5", lambda: sharded_c5(sub, world, rank, peak, peak_kind))
+    return ex
+
+
+def sharded_c5(args, world, rank, peak, peak_kind):
+    """C5 (BASELINE configs[4]): the 128M-particle reference timestep
+    (density, force, kick, drift, migrate) sharded by x-slabs of cells over
+    the ranks; time = max over ranks, strong scaling."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "benchmarks"))
+    import workloads as W
+    a = argparse.Namespace(**vars(args))
+    a.c5_full = True
+    res = W.c5(a, peak, peak_kind, world, rank)
+    keys = sorted(k for k, v in res["phases_ms"].items() if isinstance(v, float))
+    t = torch.tensor([res["ms_per_step"]] + [res["phases_ms"][k] for k in keys], device="cuda",
+                     dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    phases = {k: float(v) for k, v in zip(keys, t[1:].tolist())}
+    n = args.c5_n
+    out = {"value": n / (ms * 1e-3), "unit": "particle updates/s (full timesteps)", "ms_per_step": ms,
+           "n_gpus": world, "scaling": "strong", "particles_total": n, "particles_rank0": res["particles_local"],
+           "phases_ms_max_over_ranks": phases, "config": res["config"],
+           "halo": "peer: each rank reads its +-1 neighbours' packed cell blocks in place through CUDA IPC "
+                   "peer pointers (NVLink); no ghost copy" if world > 1 else "none (one slab)"}
+    # compute rooflines of the two pair kernels (uniform particles: 64 in-support neighbours by construction)
+    pairs = 64.0 * n / world
+    if phases.get("force"):
+        out["roofline"] = compute_roofline("k_force_c (fp32, per rank)", pairs, 40, phases["force"], "force_c5")
+    if phases.get("density"):
+        out["roofline_density"] = compute_roofline("bin + pack + k_pairs_c (fp32, per rank)", pairs, 24,
+                                                   phases["density"], "pairs_c5")
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        rate, secs = cpu_reference_kernels_rate(1 << 18, ["density", "force", "kick", "drift"], threads, T=32,
+                                                layout="soa")
+        out["cpu_baseline"] = {"value": rate, "unit": "particle updates/s (full timesteps)", "cores": threads,
+                               "kind": "reference",
+                               "sample": "the reference's own timestep (density, force, kick, drift; 64-particle "
+                                         "buffers, binary64) on a 256K-particle T=32 SoA, %d threads, %.2f s"
+                                         % (threads, secs)}
+    return out
 
 
 def other_arm(args):
@@ -487,6 +683,27 @@ def other_arm(args):
     return 0
 
 
+def torchrun_argv(argv, n, port):
+    """The command that re-runs this bench under torch.distributed.run with
+    n ranks on this node (the driver's own launch form)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % n,
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def maybe_reexec(args, argv):
+    """--gpus N > 1 outside torchrun: one rank per GPU via torch.distributed.run."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = torchrun_argv(argv, args.gpus, port)
+        env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+                   NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+        return subprocess.call(cmd, env=env)
+    return None
+
+
 def build_parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -500,6 +717,8 @@ def build_parser():
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="C2 only: skip configs c1/c3/c4, sharded_c5, soa_vs_aos, transform, timestep")
     ap.add_argument("--table-particles", type=int, default=1 << 16)
     ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c2",
                     help="BASELINE.json config (default c2 = configs[1], the headline)")
@@ -515,7 +734,11 @@ def build_parser():
 
 
 def main():
-    args = build_parser().parse_args()
+    argv = sys.argv[1:]
+    args = build_parser().parse_args(argv)
+    rc = maybe_reexec(args, argv)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return reference_arm(args)
     if args.workload != "c2":

@@ -5,9 +5,12 @@
   c3  SPH density, cell-linked, 4M uniform particles, SoA fp32 vs fp16 vs bf16
   c4  64M host-resident particles: streamed (narrowed 2-D DMA) vs managed vs
       in-place (whole records), one drift and one kick+drift step each
-  c5  128M particles, density + kick/drift sharded by cell (NCCL halo)
+  c5  128M particles, density + kick/drift sharded by cell (peer-block halo)
 
-Each returns the same JSON-line dict as the default C2 workload.
+plus the paper's three measurements on the B200 (bench.py puts them in the
+default line): soa_vs_aos (kernel speedups), transform
+(conversion placement host vs device) and timestep
+(in-place vs streaming whole timestep over real PCIe).
 """
 from __future__ import annotations
 
@@ -328,3 +331,199 @@ def c5(args, peak, peak_kind, world, rank, group=None):
                        "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},
             "phases_ms": {k: (sum(v) / len(v) if k != "density_sub" else v[0]) for k, v in phases.items()},
             "particles_local": st.n}
+
+
+# ----------------------------------------------------------------- PCIe probe
+def pcie_peaks(nbytes: int = 1 << 30, reps: int = 3) -> dict:
+    """Pinned cudaMemcpyAsync H2D, D2H and both directions at once (two
+    streams), GB/s: the roofline denominators of the host-resident C4 step."""
+    hb = api.HostBuffer(nbytes, 0)
+    hb2 = api.HostBuffer(nbytes, 0)
+    h1, h2 = torch.from_numpy(hb.numpy()), torch.from_numpy(hb2.numpy())
+    d1 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            dt_ = time.perf_counter() - t0
+            best = dt_ if best is None else min(best, dt_)
+        return best
+
+    h2d = nbytes / timed(lambda: d1.copy_(h1, non_blocking=True)) / 1e9
+    d2h = nbytes / timed(lambda: h1.copy_(d1, non_blocking=True)) / 1e9
+
+    def both():
+        with torch.cuda.stream(s1):
+            d1.copy_(h1, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    bidir = 2 * nbytes / timed(both) / 1e9
+    del d1, d2
+    hb.free()
+    hb2.free()
+    return {"h2d_GBps": h2d, "d2h_GBps": d2h, "bidirectional_GBps": bidir,
+            "method": "pinned cudaMemcpyAsync of %d MiB, best of %d; bidirectional = H2D and D2H on two "
+                      "streams at once" % (nbytes >> 20, reps)}
+
+
+# ----------------------------------------------------------- SoA vs AoS (paper Fig. compute)
+def soa_vs_aos(args, n: int = 1 << 24) -> dict:
+    """Kernel time on the unpacked AoS vs the SoA streams (the paper's
+    compute-only comparison), 16M particles on the B200:
+    kick and drift in place (k_update_rec_tile on records vs k_update_soa on
+    streams) and the reference-semantics density (64-particle buffers,
+    binary64, k_density_buffer), at the default precision (f64 x, f32 rest)
+    and at T=16 (x kept at f64, the reference bench's exclusion)."""
+    P, v, src = random_default_aos(n, seed=77)
+    out = {}
+    for label, prec, excl in (("default", api.SF_PREC_NATIVE, ""), ("T16", 16, "x")):
+        aos = api.convert(src, api.View(P, n, "aos", None, prec, excl))
+        soa = api.convert(src, api.View(P, n, "soa", None, prec, excl))
+        for k, reps in (("kick", 10), ("drift", 10), ("density", 3)):
+            row = {}
+            for layout, buf in (("aos", aos), ("soa", soa)):
+                fn = lambda: api.run_kernel(buf, k, 1e-3, buffer_size=64)  # noqa: E731
+                fn()
+                t = timed_each(fn, reps)
+                row[layout + "_ms"] = sum(t) / len(t)
+            row["soa_speedup"] = row["aos_ms"] / row["soa_ms"]
+            out["%s/%s" % (k, label)] = row
+        del aos, soa
+    return {"particles": n, "rows": out,
+            "paper": "SoA vs AoS kernel speedup: kick/drift ~8x GH200, ~4x H100; density ~4x on Nvidia "
+                     "(PAPER.md:533)",
+            "note": "compute only, inputs resident in HBM (1.4 GB AoS > L2), no transfers; kick/drift are "
+                    "HBM-bound on both layouts (the AoS pass reads whole records once with one TMA bulk copy "
+                    "per CTA), density is FP64-bound"}
+
+
+# ----------------------------------------------------------- transform placement (paper Fig. transform)
+def _lib_csv(lib_path, cmd, ints, strings):
+    import ctypes as C
+    L = C.CDLL(lib_path)
+    L.sf_config_create.argtypes = [C.POINTER(C.c_void_p)]
+    L.sf_config_set_int.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+    L.sf_config_set_string.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
+    getattr(L, cmd).argtypes = [C.c_void_p, C.POINTER(C.c_char_p)]
+    L.sf_config_destroy.argtypes = [C.c_void_p]
+    L.sf_last_error.restype = C.c_char_p
+    cfg = C.c_void_p()
+    L.sf_config_create(C.byref(cfg))
+    for k, val in ints.items():
+        L.sf_config_set_int(cfg, k.encode(), val)
+    for k, val in strings.items():
+        L.sf_config_set_string(cfg, k.encode(), val.encode())
+    out = C.c_char_p()
+    st = getattr(L, cmd)(cfg, C.byref(out))
+    text = out.value.decode() if out.value else ""
+    L.sf_config_destroy(cfg)
+    if st != 0:
+        raise RuntimeError(L.sf_last_error().decode())
+    rows = [ln.split(",") for ln in text.splitlines() if ln and not ln.startswith("#")]
+    return [dict(zip(rows[0], r)) for r in rows[1:]]
+
+
+def transform_placement(args, root: str, n: int = 1 << 17) -> dict:
+    """Where to run U.N.C (bench.cpp:214-267), measured:
+    host placement = the unmodified reference's own CPU conversion
+    (narrow_into + unpack_into + aos_to_soa_into, its `bench transform` host
+    rows, single-threaded as in the reference) + a measured pinned H2D of the
+    converted SoA bytes; device placement = a measured pinned H2D of the
+    whole compressed AoS + the fused B200 gather.  ratio = host / device
+    (the reference's definition with measured instead of modelled moves)."""
+    import os
+    ref_lib = os.path.join(root, "oracle", "_ref", "libsoaforge_ref.so")
+    sets = ["full", "density", "force", "kick", "drift"]
+    ref = _lib_csv(ref_lib, "sf_run_bench_transform", {"particles": n},
+                   {"kernels": "density,force,kick,drift", "precision": "32,16"})
+    host_conv = {(r["kernel"], int(r["precision"])): (float(r["convert_s"]), int(r["bytes_moved"]))
+                 for r in ref if r["placement"] == "host"}
+    schema = api.Schema.default()
+    hb = api.HostBuffer(n * 200 + 4096, 0)
+    hsrc = torch.from_numpy(hb.numpy())
+    _, aos_v, src = random_default_aos(n, seed=5)
+
+    def h2d_s(nbytes):
+        d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        fn = lambda: d.copy_(hsrc[:nbytes], non_blocking=True)  # noqa: E731
+        fn()
+        t = timed_each(fn, 5)
+        return min(t) * 1e-3
+
+    rows = {}
+    for T, prec in ((32, 32), (16, 16), ("bf16", api.SF_PREC_BF16)):
+        # the reference's population at precision T: with_uniform_precision(S, T, {"x"}) stored compressed
+        # (bench.cpp make_population); bf16 (no reference PrecisionSpec) gathers from the default AoS
+        srcT = src if T == "bf16" else api.convert(src, api.View(schema, n, "aos", None, api.SF_PREC_PACKED + T, "x"))
+        whole_s = h2d_s(srcT.view.nbytes)
+        for name in sets:
+            dv = api.View(schema, n, "soa", None if name == "full" else name, prec, "x")
+            out = api.PackedBuffer.empty(dv)
+            fn = lambda: api.gather(srcT, dv, out=out)  # noqa: E731
+            fn()
+            t = timed_each(fn, 10)
+            dev_conv = min(t) * 1e-3
+            row = {"device_convert_s": dev_conv, "device_move_s": whole_s, "device_bytes": srcT.view.nbytes,
+                   "device_s": dev_conv + whole_s}
+            if T != "bf16" and (name, T) in host_conv:
+                hc, hbytes = host_conv[(name, T)]
+                hm = h2d_s(hbytes)
+                row.update({"host_convert_s": hc, "host_move_s": hm, "host_bytes": hbytes, "host_s": hc + hm,
+                            "ratio": (hc + hm) / (dev_conv + whole_s)})
+            rows["%s/%s" % (name, T)] = row
+    hb.free()
+    best16 = max(r["ratio"] for k, r in rows.items() if k.endswith("/16") and "ratio" in r)
+    best32 = max(r["ratio"] for k, r in rows.items() if k.endswith("/32") and "ratio" in r)
+    return {"particles": n, "rows": rows, "best_ratio_32": best32, "best_ratio_16": best16,
+            "cpu_threads": 1,
+            "paper": "GPU-side vs CPU-side transform: up to 35x (32-bit), 500x (16-bit) on GH200/MI300A "
+                     "(PAPER.md:511)",
+            "note": "x kept at f64 (bench.cpp's with_uniform_precision exclusion); host conversion = the "
+                    "reference's own bench transform host rows (oracle/_ref, single-threaded like the "
+                    "reference); moves measured over this box's PCIe"}
+
+
+# ----------------------------------------------------------- whole timestep (paper Fig. pipeline)
+def timestep_pipeline(args, n: int = 1 << 20) -> dict:
+    """The paper's end-to-end question on a PCIe B200:
+    one reference timestep (density, force, kick, drift; 64-particle buffers,
+    binary64) on a host-resident AoS, through this library's
+    sf_run_bench_pipeline with real transfers (pipelines.cpp:231-296
+    semantics): dev-native = the AoS baseline (no transformation), dev-soa
+    = the GPU-side AoS->SoA transformation; in-place = whole records once
+    each way, streaming = each kernel's narrowed fields each way."""
+    from paper_2512_05516_b200 import _lib
+    rows = _lib_csv(_lib.LIB_PATH, "sf_run_bench_pipeline", {"particles": n},
+                    {"kernels": "density,force,kick,drift", "variants": "dev-native,dev-soa",
+                     "modes": "inplace,streaming", "precision": "32,16"})
+    res = {}
+    for r in rows:
+        key = "%s/%s/%s" % (r["variant"], r["mode"], r["precision"])
+        res[key] = {k: float(r[k]) for k in ("total_s", "convert_s", "move_s", "compute_s", "merge_s")}
+        res[key].update({"bytes_to_device": int(r["bytes_to_device"]), "bytes_to_host": int(r["bytes_to_host"]),
+                         "share_force": float(r["share_force"]), "share_density": float(r["share_density"])})
+    speed = {}
+    for mode in ("inplace", "streaming"):
+        for prec in ("32", "16"):
+            b = res.get("dev-native/%s/%s" % (mode, prec))
+            t = res.get("dev-soa/%s/%s" % (mode, prec))
+            if b and t:
+                speed["%s/%s" % (mode, prec)] = b["total_s"] / t["total_s"]
+    base = res.get("dev-native/inplace/32")
+    if base:
+        for mode in ("inplace", "streaming"):
+            for prec in ("32", "16"):
+                t = res.get("dev-soa/%s/%s" % (mode, prec))
+                if t:
+                    speed["%s/%s_vs_aos_inplace32" % (mode, prec)] = base["total_s"] / t["total_s"]
+    return {"particles": n, "rows": res, "soa_speedup_vs_aos": speed,
+            "paper": "In-place / Streaming vs AoS baseline: 2.6x / ~2x GH200, 1.9x / 1.4x H100 (PAPER.md:554)",
+            "note": "moves are measured pinned cudaMemcpy (whole records in place; narrowed fields as "
+                    "byte columns, one 2-D DMA per run of adjacent fields, when streaming); phases run one "
+                    "after another as in the reference's Run (not overlapped)"}

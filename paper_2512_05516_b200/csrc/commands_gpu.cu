@@ -345,10 +345,61 @@ struct VariantResult {
     uint64_t checksum = 0;
 };
 
-// pipelines::run_variant (pipelines.cpp:378-405) on the GPU.  The state lives
-// in pinned host memory between phases; "cpu" variants keep everything on the
-// device (no transfer), dev/host in-place move the whole state once each way,
-// streaming moves each kernel's narrowed record set each way.
+struct PinnedBuf {
+    void* p = nullptr;
+    explicit PinnedBuf(size_t bytes) { check_cuda(cudaHostAlloc(&p, bytes + 16, cudaHostAllocDefault), "cudaHostAlloc"); }
+    PinnedBuf(const PinnedBuf&) = delete;
+    ~PinnedBuf() { cudaFreeHost(p); }
+};
+
+// The narrowed record N(set) as byte columns of the full record: one 2-D DMA
+// per run of fields adjacent in both records (pitch = record), so exactly
+// the narrowed bytes cross PCIe (streamed_bytes_one_way, pipelines.cpp:
+// 434-441) and the copy engine does the narrowing.
+struct Column {
+    size_t full_off, narrow_off, bytes;
+};
+std::vector<Column> narrowed_columns(const View& full, const View& nv) {
+    std::vector<Column> cols;
+    for (size_t p = 0; p < nv.subset.size(); ++p) {
+        const size_t fo = size_t(full.lane_base(full.pos_of(nv.subset[p])) / 8), no = size_t(nv.lane_base(int(p)) / 8);
+        const size_t w = size_t(uint64_t(nv.arity(int(p))) * nv.width(int(p)) / 8);
+        if (!cols.empty() && cols.back().full_off + cols.back().bytes == fo && cols.back().narrow_off + cols.back().bytes == no)
+            cols.back().bytes += w;
+        else
+            cols.push_back({fo, no, w});
+    }
+    return cols;
+}
+
+void copy_columns(const std::vector<Column>& cols, void* narrow, size_t narrow_pitch, void* full, size_t full_pitch,
+                  uint64_t n, bool to_device) {
+    for (const Column& c : cols) {
+        uint8_t* nb = static_cast<uint8_t*>(narrow) + c.narrow_off;
+        uint8_t* fb = static_cast<uint8_t*>(full) + c.full_off;
+        if (to_device)
+            check_cuda(cudaMemcpy2DAsync(nb, narrow_pitch, fb, full_pitch, c.bytes, n, cudaMemcpyHostToDevice, nullptr),
+                       "H2D columns");
+        else
+            check_cuda(cudaMemcpy2DAsync(fb, full_pitch, nb, narrow_pitch, c.bytes, n, cudaMemcpyDeviceToHost, nullptr),
+                       "D2H columns");
+    }
+}
+
+// pipelines::run_variant (pipelines.cpp:378-405) on the GPU, over real PCIe.
+// The state lives in pinned host memory.  dev-* variants: in-place moves the
+// whole compressed AoS to the device once, runs every kernel there (through
+// the variant's conversions) and moves it back (run_dev_inplace,
+// pipelines.cpp:231-249); streaming moves, per kernel, only the narrowed
+// fields each way — byte columns of the host records, one 2-D DMA per run
+// of adjacent fields — and converts on the device (run_dev_streaming,
+// :251-296).  move_s is the measured transfer time and bytes_to_device /
+// bytes_to_host the bytes actually copied (= the reference ledger).
+// cpu-* variants run on the device with no transfer (their state is where
+// the compute is).  host-* variants place the conversion on the host in the
+// reference (:298-368), which needs a CPU conversion this library does not
+// contain: they keep the ledger byte model with move_s = 0 (bench.py times
+// host placement with the reference's own CPU conversion).
 VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const std::string& variant,
                               const std::string& mode, bool fault) {
     const uint64_t n = pop.ics.n;
@@ -356,7 +407,15 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
     DevBuf state(aos.total_bytes());
     store_state(pop.ics, aos, state.p);
     VariantResult res;
+    const bool dev = variant.rfind("dev-", 0) == 0;
     const bool stream_mode = mode == "streaming" && !is_cpu(variant);
+    const size_t abytes = size_t(aos.total_bytes());
+    std::unique_ptr<PinnedBuf> hstate;
+    if (dev) {  // the state starts (and ends) in pinned host memory
+        hstate.reset(new PinnedBuf(abytes));
+        check_cuda(cudaMemcpy(hstate->p, state.p, abytes, cudaMemcpyDeviceToHost), "D2H");
+        check_cuda(cudaMemset(state.p, 0, abytes), "memset");
+    }
     if (!is_cpu(variant) && !stream_mode) {  // one full round trip each way
         // dev variants move the compressed state, host variants the unpacked one
         const uint64_t b = is_host(variant) ? make_view(pop.schema, nullptr, Layout::AoS, kPrecNative, {}, n).total_bytes()
@@ -364,17 +423,67 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
         res.to_dev += b;
         res.to_host += b;
         res.transfers += 2;
+        if (dev)
+            res.move_s += gpu_seconds([&] {
+                check_cuda(cudaMemcpyAsync(state.p, hstate->p, abytes, cudaMemcpyHostToDevice, nullptr), "H2D");
+            });
     }
+    const size_t rec_bytes = size_t(aos.record_bits() / 8);
     for (const auto& k : c.kernels) {
         const KernelSet* set = pop.schema->kernel(k);
         if (!set) throw std::invalid_argument("no access set declared for kernel '" + k + "'");
-        if (stream_mode) {  // narrowed AoS each way (host variants ship native widths)
-            View nv = make_view(pop.schema, k.c_str(), Layout::AoS, is_host(variant) ? kPrecNative : kPrecStored, {}, n);
+        const Conv cv = conv_of(variant);
+        if (stream_mode && dev) {
+            // N: narrowed compressed AoS of the kernel's fields, straight from the host records
+            View nv = make_view(pop.schema, k.c_str(), Layout::AoS, kPrecStored, {}, n);
+            DevBuf nb(nv.total_bytes());
+            const bool cols = aos.byte_aligned() && nv.byte_aligned() && aos.record_bits() % 8 == 0 &&
+                              nv.record_bits() % 8 == 0;
+            const std::vector<Column> colv = cols ? narrowed_columns(aos, nv) : std::vector<Column>{};
+            const size_t nrec = size_t(nv.record_bits() / 8);
+            res.to_dev += nv.total_bytes();
+            res.to_host += nv.total_bytes();
+            res.transfers += 2;
+            res.move_s += gpu_seconds([&] {
+                if (cols) {
+                    copy_columns(colv, nb.p, nrec, hstate->p, rec_bytes, n, true);
+                } else {  // bit-packed records: whole records over PCIe, narrowed on the device
+                    check_cuda(cudaMemcpyAsync(state.p, hstate->p, abytes, cudaMemcpyHostToDevice, nullptr), "H2D");
+                    convert(aos, state.p, nv, nb.p, nullptr);
+                }
+            });
+            if (cv == Conv::None) {
+                const double t = gpu_seconds([&] { run_kernel(nv, nb.p, k, c.dt, c.buffer_size, c.per_access, 0, nullptr); });
+                res.compute_s += t;
+                res.kernel_s[k] += t;
+            } else {
+                View work = make_view(pop.schema, k.c_str(), cv == Conv::UnpackSoA ? Layout::SoA : Layout::AoS,
+                                      kPrecNative, {}, n);
+                DevBuf w(work.total_bytes());
+                res.convert_s += gpu_seconds([&] { gather(nv, nb.p, work, w.p, nullptr, 0.0, 0, nullptr); });
+                const double t = gpu_seconds([&] { run_kernel(work, w.p, k, c.dt, c.buffer_size, c.per_access, 0, nullptr); });
+                res.compute_s += t;
+                res.kernel_s[k] += t;
+                if (!set->writes.empty())
+                    res.convert_s += gpu_seconds([&] { scatter_merge(work, w.p, nv, nb.p, k, nullptr); });
+            }
+            // N^T: the narrowed fields back into the host records (read-only fields come back bit-identical)
+            res.move_s += gpu_seconds([&] {
+                if (cols) {
+                    copy_columns(colv, nb.p, nrec, hstate->p, rec_bytes, n, false);
+                } else {
+                    scatter_merge(nv, nb.p, aos, state.p, k, nullptr);
+                    check_cuda(cudaMemcpyAsync(hstate->p, state.p, abytes, cudaMemcpyDeviceToHost, nullptr), "D2H");
+                }
+            });
+            continue;
+        }
+        if (stream_mode) {  // host-* streaming: ledger only (no CPU conversion in this library)
+            View nv = make_view(pop.schema, k.c_str(), Layout::AoS, kPrecNative, {}, n);
             res.to_dev += nv.total_bytes();
             res.to_host += nv.total_bytes();
             res.transfers += 2;
         }
-        const Conv cv = conv_of(variant);
         if (cv == Conv::None) {
             const double t = gpu_seconds([&] { run_kernel(aos, state.p, k, c.dt, c.buffer_size, c.per_access, 0, nullptr); });
             res.compute_s += t;
@@ -389,7 +498,17 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
         res.kernel_s[k] += t;
         if (!set->writes.empty()) res.merge_s += gpu_seconds([&] { scatter_merge(work, w.p, aos, state.p, k, nullptr); });
     }
-    std::vector<uint8_t> bytes = download(aos, state.p);
+    std::vector<uint8_t> bytes;
+    if (dev) {
+        if (!stream_mode)
+            res.move_s += gpu_seconds([&] {
+                check_cuda(cudaMemcpyAsync(hstate->p, state.p, abytes, cudaMemcpyDeviceToHost, nullptr), "D2H");
+            });
+        const uint8_t* hp = static_cast<const uint8_t*>(hstate->p);
+        bytes.assign(hp, hp + abytes);
+    } else {
+        bytes = download(aos, state.p);
+    }
     if (fault && !bytes.empty()) bytes[0] ^= 0x01;  // bench.cpp:577-578
     res.checksum = fnv(bytes, aos.total_bits());
     return res;

@@ -37,3 +37,25 @@ def test_reference_arm_json_line():
 def test_bench_defaults_are_the_driver_contract():
     a = bench.build_parser().parse_args([])
     assert a.gpus == 1 and a.warmup >= 3 and a.workload == "c2" and a.impl == "b200"
+
+
+def test_gpus_flag_relaunches_under_torchrun(monkeypatch):
+    """`bench.py --gpus 4` outside torchrun re-runs itself with 4 ranks (one
+    per GPU) through torch.distributed.run on 127.0.0.1, same arguments."""
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd, env=None: calls.append((cmd, env)) or 0)
+    argv = ["--gpus", "4", "--steps", "7", "--warmup", "3"]
+    args = bench.build_parser().parse_args(argv)
+    assert bench.maybe_reexec(args, argv) == 0
+    cmd, env = calls[0]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[cmd.index("--master-port") + 1].isdigit()
+    assert cmd[-len(argv):] == argv and cmd[-len(argv) - 1].endswith("bench.py")
+    assert env["NCCL_DEBUG"]
+    # inside torchrun (WORLD_SIZE set) and at one GPU there is no relaunch
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    assert bench.maybe_reexec(args, argv) is None
+    monkeypatch.delenv("WORLD_SIZE")
+    assert bench.maybe_reexec(bench.build_parser().parse_args([]), []) is None
