@@ -7,6 +7,8 @@ import os
 
 import pytest
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 import oracle as O
 from paper_2512_05516_b200 import _lib as L
 
@@ -182,3 +184,16 @@ def test_ic_csv_errors_match_reference(libs, tmp_path):
         e2 = ref.sf_last_error()
         assert s1 == s2 != 0, (path, s1, s2)
         assert e1 == e2, (e1, e2)
+
+
+def test_reference_test_capi_links_and_passes():
+    """The reference's own unmodified tests/test_capi.cpp (built by
+    `make -C oracle ref` against the reference's soaforge.h and this repo's
+    libsoaforge_b200.so): every case passes on the GPU library."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_capi_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/test_capi_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "6 test cases, 0 failed checks" in r.stdout
