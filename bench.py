@@ -579,9 +579,7 @@ def sharded_c5(args, world, rank, peak, peak_kind):
     import torch
     sys.path.insert(0, os.path.join(ROOT, "benchmarks"))
     import workloads as W
-    a = argparse.Namespace(**vars(args))
-    a.c5_full = True
-    res = W.c5(a, peak, peak_kind, world, rank)
+    res = W.c5(args, peak, peak_kind, world, rank)
     keys = sorted(k for k, v in res["phases_ms"].items() if isinstance(v, float))
     t = torch.tensor([res["ms_per_step"]] + [res["phases_ms"][k] for k in keys], device="cuda",
                      dtype=torch.float64)
@@ -595,7 +593,8 @@ def sharded_c5(args, world, rank, peak, peak_kind):
            "n_gpus": world, "scaling": "strong", "particles_total": n, "particles_rank0": res["particles_local"],
            "phases_ms_max_over_ranks": phases, "config": res["config"],
            "halo": "peer: each rank reads its +-1 neighbours' packed cell blocks in place through CUDA IPC "
-                   "peer pointers (NVLink); no ghost copy" if world > 1 else "none (one slab)"}
+                   "peer pointers (NVLink); no ghost copy, no NCCL on the data path" if world > 1 else
+                   "none (one slab)", "migrated_per_step": res.get("sent_per_step")}
     # compute rooflines of the two pair kernels (uniform particles: 64 in-support neighbours by construction)
     pairs = 64.0 * n / world
     if phases.get("force"):
@@ -724,10 +723,6 @@ def build_parser():
                     help="BASELINE.json config (default c2 = configs[1], the headline)")
     ap.add_argument("--c4-n", type=int, default=1 << 26)
     ap.add_argument("--c5-n", type=int, default=1 << 27)
-    ap.add_argument("--c5-reorder", type=int, default=0,
-                    help="C5: permute the state into the density's cell order every k-th step (0: never)")
-    ap.add_argument("--c5-full", action="store_true",
-                    help="C5 with the full reference timestep (density, force, kick, drift)")
     ap.add_argument("--refine", type=int, default=2,
                     help="C3/C5 binning cells per density cell side (searched with reach = refine)")
     return ap

@@ -256,81 +256,45 @@ def c4(args, peak, peak_kind):
 
 # ----------------------------------------------------------------------- C5
 def c5(args, peak, peak_kind, world, rank, group=None):
+    """One rank of the C5 timestep through the C++ shard (sf_b200_shard_step):
+    density, force, kick, drift, then migration, one library call per step;
+    phase times from the library's own CUDA events (waits on the neighbours
+    included)."""
     from paper_2512_05516_b200.sharded import ShardedState, Slab, grid_for
     n = args.c5_n
     h, nc, cell = grid_for(n)
     slab = Slab(nc, cell, rank, world)
-    st = ShardedState(n, slab, prec=32, h=h, reorder_every=args.c5_reorder)
-    st.sort_by_cell()  # particles start in cell order; --c5-reorder k keeps them there every k-th step
+    st = ShardedState(n, slab, prec=32, h=h, group=group, refine=args.refine)
+    st.sort_by_cell()  # particles start in cell order; the shard's migration keeps the stayers in it
+    st.stream("P").copy_(st.stream("rho") * (2.0 / 3.0) * st.stream("u"))  # EOS pressure, P = (gamma-1) rho u
+    kernels = "density,force,kick,drift"
     for _ in range(max(1, min(args.warmup, 2))):
-        st.full_step(group=group) if args.c5_full else st.step(group=group)
+        st.full_step(1e-3, timed=True)
     torch.cuda.synchronize()
-    phases = {"kick_drift": [], "migrate": [], "density": [], "reorder": []}
-    if args.c5_full:
-        phases["force"] = []
-    times = []
+    runs = []
     for _ in range(max(2, min(args.steps, 5))):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        ev[0].record()
-        if args.c5_full:  # the reference's timestep order: density, force, kick+drift, migrate
-            st.density(group)
-            ev[1].record()
-            st.force(group)
-            ev[2].record()
-            st.maybe_reorder()
-            ev[3].record()
-            st.kick_drift()
-            ev[4].record()
-            st.migrate(group)
-            ev[5].record()
-            ev[5].synchronize()
-            phases["density"].append(ev[0].elapsed_time(ev[1]))
-            phases["force"].append(ev[1].elapsed_time(ev[2]))
-            phases["reorder"].append(ev[2].elapsed_time(ev[3]))
-            phases["kick_drift"].append(ev[3].elapsed_time(ev[4]))
-            phases["migrate"].append(ev[4].elapsed_time(ev[5]))
-            times.append(ev[0].elapsed_time(ev[5]))
-            continue
-        st.kick_drift()
-        ev[1].record()
-        st.migrate(group)
-        ev[2].record()
-        st.density(group)
-        ev[3].record()
-        st.maybe_reorder()
-        ev[4].record()
-        ev[4].synchronize()
-        phases["kick_drift"].append(ev[0].elapsed_time(ev[1]))
-        phases["migrate"].append(ev[1].elapsed_time(ev[2]))
-        phases["density"].append(ev[2].elapsed_time(ev[3]))
-        phases["reorder"].append(ev[3].elapsed_time(ev[4]))
-        times.append(ev[0].elapsed_time(ev[4]))
-    ms = sum(times) / len(times)
-    # one more step with sub-phase events (not part of the timed mean)
-    import paper_2512_05516_b200.sharded as SH
-    SH.PHASES.clear()
-    SH.PHASES["_on"] = True
-    st.step(group=group)
-    torch.cuda.synchronize()
-    ev = SH.PHASES.pop("_events", [])
-    SH.PHASES.clear()
-    sub = {}
-    for (a, ea), (_, eb) in zip(ev, ev[1:]):
-        sub[a] = sub.get(a, 0.0) + ea.elapsed_time(eb)
-    phases["density_sub"] = [sub]
-    return {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
-            "roofline": {"bound": "compute (density)", "achieved": None, "peak": peak, "unit": "GB/s",
-                         "frac": None, "kernel": "k_pairs_c + k_update_soa (kick/drift)"},
-            "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + %skick/drift sharded by cell "
-                                   "with NCCL halo exchange" % (n >> 20, "force + " if args.c5_full else ""),
-                       "particles_total": n, "step": "full (density, force, kick, drift, migrate)" if args.c5_full
-                       else "kick, drift, migrate, density",
-                       "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)"},
-            "phases_ms": {k: (sum(v) / len(v) if k != "density_sub" else v[0]) for k, v in phases.items()},
-            "particles_local": st.n}
+        runs.append(st.full_step(1e-3, timed=True))
+    keys = ["step_ms"] + [k + "_ms" for k in kernels.split(",")] + ["migrate_ms"]
+    avg = {k: sum(r[k] for r in runs) / len(runs) for k in keys}
+    phases = {"density": avg["density_ms"], "force": avg["force_ms"],
+              "kick_drift": avg["kick_ms"] + avg["drift_ms"], "migrate": avg["migrate_ms"]}
+    ms = avg["step_ms"]
+    out = {"value": n / (ms * 1e-3), "ms_per_step": ms, "local_ms": ms,
+           "roofline": {"bound": "compute (density, force)", "achieved": None, "peak": peak, "unit": "GB/s",
+                        "frac": None, "kernel": "k_pairs_c + k_force_c"},
+           "config": {"workload": "C5 (BASELINE configs[4]): %dM-particle density + force + kick/drift sharded by "
+                                  "cell over %d GPU(s), halo read in place from the neighbours' blocks" % (n >> 20, world),
+                      "particles_total": n, "step": "full reference timestep (density, force, kick, drift) + migration, "
+                                                    "one sf_b200_shard_step call",
+                      "cells_per_side": nc, "h": h, "storage": "SoA binary32 (default schema, T=32)",
+                      "halo": "peer blocks over CUDA IPC (NVLink), device-side epoch ordering" if world > 1 else
+                              "none (one slab)"},
+           "phases_ms": phases, "particles_local": st.n, "sent_per_step": runs[-1]["sent"]}
+    st.close()
+    return out
 
 
 # ----------------------------------------------------------------- PCIe probe

@@ -215,6 +215,47 @@ SF_API sf_status sf_b200_force_cells(const void* x, const void* v, const void* m
                                      const int32_t* perm, const int32_t* cell_start, const float* lo,
                                      float cell, int nx, int ny, int nz, int reach, uint64_t n_home,
                                      float* a_out, float* du_out, void* stream);
+/* One rank of the cell-sharded timestep (BASELINE C5; replaces the
+ * reference's threaded run_kernel_chunked, sph.cpp:286-308, for a
+ * population decomposed over the GPUs of one node).  The rank owns the
+ * x-slab of cell layers [rank*nc/world, (rank+1)*nc/world) of an nc^3 grid
+ * of cells of side `cell` (>= 2 h_max) over the unit box, binned `refine`
+ * times finer (reach = refine).  Its particles live on the device as an SoA
+ * of the default schema at T=32 (x included), at a fixed `capacity`.
+ *
+ * Setup (host, once): sf_b200_shard_create on every rank; exchange the
+ * 64-byte sf_b200_shard_handle of every rank with any transport (MPI,
+ * torch.distributed, files) and pass all of them, rank order, to
+ * sf_b200_shard_connect; sf_b200_shard_load the rank's particles (a
+ * reference SoA buffer of `count` particles, T=32, every field).
+ *
+ * sf_b200_shard_step runs `kernels` (a list of density, force, kick, drift,
+ * the reference's timestep order "density,force,kick,drift") and then
+ * migrates the particles whose x-layer left the slab to the +-1 neighbour.
+ * The halo is read in place: density and force take the neighbours' packed
+ * cell blocks through CUDA IPC peer pointers (NVLink).  Ranks order each
+ * other on the device (release/acquire epoch words in peer memory), so a
+ * step has no host barrier; with world > 1 it synchronises `stream` once to
+ * read the new particle count.  rho == 0 in the force -> SF_ERROR (domain
+ * error); an outbox / capacity overflow -> SF_ERROR.
+ * metrics (optional, 9 doubles): particles after the step, step ms, ms of
+ * each listed kernel (4 slots, list order), migration ms, particles sent,
+ * step number. */
+typedef struct sf_shard sf_shard;
+SF_API sf_status sf_b200_shard_create(int rank, int world, int cells_per_side, double cell, int refine,
+                                      uint64_t capacity, sf_shard** out);
+SF_API void sf_b200_shard_destroy(sf_shard* shard);
+SF_API sf_status sf_b200_shard_handle(sf_shard* shard, uint8_t handle[SF_IPC_HANDLE_BYTES]);
+SF_API sf_status sf_b200_shard_connect(sf_shard* shard, const uint8_t* handles /* world x 64 bytes */);
+SF_API sf_status sf_b200_shard_load(sf_shard* shard, const void* soa_dev, uint64_t count, void* stream);
+/* Device pointer of one field's stream of the current state (binary32 lanes,
+ * int64 for id; valid until the next step), the particle count and the
+ * field's bytes per particle. */
+SF_API sf_status sf_b200_shard_field(sf_shard* shard, const char* field, void** dev, uint64_t* count,
+                                     int* bytes_per_particle);
+SF_API sf_status sf_b200_shard_step(sf_shard* shard, const char* kernels, double dt, void* stream,
+                                    double* metrics);
+
 /* Counting sort of particles into cells (x-major cell id), stable in
  * particle index: writes perm[n] (sorted position -> original index) and
  * cell_start[ncell+1].  scratch must hold sf_b200_bin_scratch_bytes(). */

@@ -101,6 +101,13 @@ SYMBOLS = [
     ("sf_b200_ipc_handle", i32, [P, P]),
     ("sf_b200_ipc_open", i32, [P, PP]),
     ("sf_b200_ipc_close", i32, [P]),
+    ("sf_b200_shard_create", i32, [i32, i32, i32, f64, i32, u64, PP]),
+    ("sf_b200_shard_destroy", None, [P]),
+    ("sf_b200_shard_handle", i32, [P, P]),
+    ("sf_b200_shard_connect", i32, [P, P]),
+    ("sf_b200_shard_load", i32, [P, P, u64, P]),
+    ("sf_b200_shard_field", i32, [P, s, PP, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
+    ("sf_b200_shard_step", i32, [P, s, f64, P, C.POINTER(C.c_double)]),
     ("sf_b200_bin_particles", i32, [P, u64, P, C.c_float, i32, i32, i32, P, P, P, u64, P]),
     ("sf_b200_bin_scratch_bytes", u64, [u64, i32, i32, i32]),
     ("sf_b200_run_host", i32, [P, P, P, s, f64, i32, i32, u64, P, C.POINTER(C.c_double)]),

@@ -461,6 +461,79 @@ class DeviceBuffer:
             pass
 
 
+class Shard:
+    """One rank of the cell-sharded timestep (sf_b200_shard_*): an x-slab of
+    an nc^3 cell grid over the unit box, its particles an SoA of the default
+    schema at T=32 held by the library at a fixed capacity.  `exchange`
+    gathers every rank's 64-byte handle (rank order) — e.g. torch.distributed
+    all_gather_object; None for a single rank."""
+
+    FIELDS = ("x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt")
+
+    def __init__(self, rank: int, world: int, cells_per_side: int, cell: float, refine: int = 2,
+                 capacity: int = 0, exchange=None):
+        h = C.c_void_p()
+        check(lib().sf_b200_shard_create(rank, world, cells_per_side, float(cell), refine, int(capacity),
+                                         C.byref(h)))
+        self._h, self.rank, self.world = h, rank, world
+        mine = (C.c_uint8 * L.SF_IPC_HANDLE_BYTES)()
+        check(lib().sf_b200_shard_handle(self._h, C.cast(mine, C.c_void_p)))
+        every = exchange(bytes(mine)) if (exchange is not None and world > 1) else [bytes(mine)] * world
+        allh = (C.c_uint8 * (L.SF_IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(every))
+        check(lib().sf_b200_shard_connect(self._h, C.cast(allh, C.c_void_p)))
+
+    def load(self, soa: "PackedBuffer") -> None:
+        """The rank's particles: an SoA PackedBuffer of the default schema at
+        T=32 (x included, every field)."""
+        check(lib().sf_b200_shard_load(self._h, _ptr(soa.data), soa.view.count, _stream()))
+
+    @property
+    def count(self) -> int:
+        p, n, b = C.c_void_p(), C.c_uint64(), C.c_int()
+        check(lib().sf_b200_shard_field(self._h, b"x", C.byref(p), C.byref(n), C.byref(b)))
+        return n.value
+
+    def field(self, name: str):
+        """The field's stream of the current state as a torch tensor (a view
+        of library memory, valid until the next step): (n, 3) float32 for
+        x / v / a, (n,) float32 for scalars, (n,) int64 for id."""
+        import torch
+        p, n, b = C.c_void_p(), C.c_uint64(), C.c_int()
+        check(lib().sf_b200_shard_field(self._h, name.encode(), C.byref(p), C.byref(n), C.byref(b)))
+        count, per = n.value, b.value
+        typestr = "<i8" if name == "id" else "<f4"
+        shape = (count, 3) if per == 12 else (count,)
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (p.value or 0, False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(_Iface(), device="cuda") if count else torch.empty(
+            shape, dtype=torch.int64 if name == "id" else torch.float32, device="cuda")
+
+    def step(self, kernels: str = "density,force,kick,drift", dt: float = 1e-3, timed: bool = False):
+        """One timestep (then migration).  timed: returns the metrics dict."""
+        m = (C.c_double * 9)() if timed else None
+        check(lib().sf_b200_shard_step(self._h, kernels.encode(), dt, _stream(), m))
+        if not timed:
+            return None
+        names = kernels.split(",")
+        out = {"particles": int(m[0]), "step_ms": m[1], "migrate_ms": m[6], "sent": int(m[7]), "step": int(m[8])}
+        for i, k in enumerate(names):
+            out[k + "_ms"] = m[2 + i]
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and L._lib is not None:
+            L._lib.sf_b200_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class HostBuffer:
     """Pinned (mode 0) or managed (mode 1) host memory for run_host."""
 

@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 SOURCES = ["schema.cpp", "view.cpp", "runtime.cpp", "commands.cpp", "capi.cpp", "kernels.cu", "density.cu",
-           "host.cu", "commands_gpu.cu"]
+           "host.cu", "commands_gpu.cu", "shard.cu"]
 
 
 def _headers():

@@ -18,6 +18,7 @@
 
 #include "commands.hpp"
 #include "runtime.hpp"
+#include "shard.hpp"
 #include "schema.hpp"
 #include "view.hpp"
 
@@ -384,6 +385,68 @@ sf_status sf_b200_ipc_close(void* p) {
     if (!p) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
         check_cuda(cudaIpcCloseMemHandle(p), "cudaIpcCloseMemHandle");
+        return SF_OK;
+    });
+}
+
+// ---------------------------------------------------------------- sharded step
+struct sf_shard {
+    sfb::Shard* s;
+};
+
+sf_status sf_b200_shard_create(int rank, int world, int cells_per_side, double cell, int refine, uint64_t capacity,
+                               sf_shard** out) {
+    if (!out) return fail(SF_INVALID_ARG, "null argument");
+    *out = nullptr;
+    return guarded([&] {
+        *out = new sf_shard{shard_create(rank, world, cells_per_side, cell, refine, capacity)};
+        return SF_OK;
+    });
+}
+
+void sf_b200_shard_destroy(sf_shard* s) {
+    if (!s) return;
+    shard_destroy(s->s);
+    delete s;
+}
+
+sf_status sf_b200_shard_handle(sf_shard* s, uint8_t* handle) {
+    if (!s || !handle) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        shard_handle(s->s, handle);
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_shard_connect(sf_shard* s, const uint8_t* handles) {
+    if (!s || !handles) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        shard_connect(s->s, handles);
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_shard_load(sf_shard* s, const void* soa_dev, uint64_t count, void* stream) {
+    if (!s || (count && !soa_dev)) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        shard_load(s->s, soa_dev, count, static_cast<cudaStream_t>(stream));
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_shard_field(sf_shard* s, const char* field, void** dev, uint64_t* count, int* bytes_per_particle) {
+    if (!s || !field || !dev) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        *dev = shard_field(s->s, field, bytes_per_particle);
+        if (count) *count = shard_count(s->s);
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_shard_step(sf_shard* s, const char* kernels, double dt, void* stream, double* metrics) {
+    if (!s || !kernels) return fail(SF_INVALID_ARG, "null argument");
+    return guarded([&] {
+        shard_step(s->s, split_names(kernels), dt, static_cast<cudaStream_t>(stream), metrics);
         return SF_OK;
     });
 }

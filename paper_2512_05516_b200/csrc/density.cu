@@ -600,23 +600,32 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
     check_cuda(cudaFreeAsync(pf, st), "cudaFreeAsync");
 }
 
-void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
-                const int32_t* perm, void* vel, float* pf, cudaStream_t st) {
+// (v, m) and P/rho^2 into a block, stream-ordered: rho == 0 anywhere sets *zero (no host sync)
+void force_pack_async(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
+                      const int32_t* perm, void* vel, float* pf, unsigned* zero, cudaStream_t st) {
     require_device();
     if (n >= (1ull << 31)) throw std::invalid_argument("force_pack: n must be < 2^31 per device");
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
     if (sp < 0) throw std::invalid_argument("force_pack precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
     if (n == 0) return;
     if (reinterpret_cast<uintptr_t>(vel) & 15) throw std::invalid_argument("vel must be 16-byte aligned");
-    unsigned* zero = nullptr;
-    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&zero), sizeof(unsigned), st), "cudaMallocAsync");
-    check_cuda(cudaMemsetAsync(zero, 0, sizeof(unsigned), st), "memset");
     float4* v4 = static_cast<float4*>(vel);
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
     if (sp == SP_F32) k_pack_vel<SP_F32><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
     else if (sp == SP_F16) k_pack_vel<SP_F16><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
     else k_pack_vel<SP_BF16><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
+    check_cuda(cudaGetLastError(), "force_pack launch");
     count_launches(1);
+}
+
+void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
+                const int32_t* perm, void* vel, float* pf, cudaStream_t st) {
+    require_device();
+    if (n == 0) return;
+    unsigned* zero = nullptr;
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&zero), sizeof(unsigned), st), "cudaMallocAsync");
+    check_cuda(cudaMemsetAsync(zero, 0, sizeof(unsigned), st), "memset");
+    force_pack_async(v, m, rho, pr, prec, n, perm, vel, pf, zero, st);
     unsigned flag = 0;
     check_cuda(cudaMemcpyAsync(&flag, zero, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
     check_cuda(cudaFreeAsync(zero, st), "cudaFreeAsync");
@@ -762,6 +771,9 @@ static void exclusive_scan(int32_t* a, int64_t n, int32_t* scratch, cudaStream_t
     k_scan_apply<<<unsigned(tiles), kScanT, 0, st>>>(a, n, tiles > 1 ? scratch : nullptr);
     count_launches(1);
 }
+
+void exclusive_scan_i32(int32_t* a, int64_t n, int32_t* scratch, cudaStream_t st) { exclusive_scan(a, n, scratch, st); }
+uint64_t scan_scratch_bytes(int64_t n) { return 4 * (2 * (uint64_t(n) / kScanTile + 64) + 64) + 256; }
 
 // Pass 2: every particle to its slot, no atomics.
 __global__ void k_place(const int32_t* __restrict__ cid, const int32_t* __restrict__ rank, uint64_t n,

@@ -72,6 +72,8 @@ struct ForceBlockDesc {
     float x_origin;
     int32_t reserved;
 };
+void force_pack_async(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
+                      const int32_t* perm, void* vel, float* pf, unsigned* zero, cudaStream_t st);
 void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
                 const int32_t* perm, void* vel, float* pf, cudaStream_t st);
 void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
@@ -81,6 +83,9 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
                  int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
                  int nx, int ny, int nz, int reach, uint64_t n_home, float* a, float* du, cudaStream_t st);
 uint64_t bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
+// exclusive prefix sum of n int32 in place (a[n-1] holds the last element's offset); scratch of scan_scratch_bytes
+void exclusive_scan_i32(int32_t* a, int64_t n, int32_t* scratch, cudaStream_t st);
+uint64_t scan_scratch_bytes(int64_t n);
 void bin_particles(const float* x, uint64_t n, const float* lo, float cell, int nx, int ny, int nz,
                    int32_t* cell_start, int32_t* perm, void* scratch, uint64_t scratch_bytes, cudaStream_t st);
 

@@ -16,9 +16,16 @@ Rank r owns layers [x0, x1).  One step:
 
 `full_step` runs the reference's timestep order instead: density, the
 cell-linked force (its halo: the neighbours' (x, h, v, m, P/rho^2)), kick,
-drift, migrate.  With halo="peer" (default) neither halo is copied: each
-rank's packed cell block is read in place by its neighbours through CUDA IPC
-peer pointers (PeerBlocks); halo="nccl" sends ghost rows instead.
+drift, migrate.
+
+halo="peer" (default) is a thin caller of the C++ shard behind the C ABI
+(sf_b200_shard_*, csrc/shard.cu): the whole step — binning, packing, the
+density and force reading the neighbours' packed cell blocks in place
+through CUDA IPC peer pointers, kick, drift, and migration through
+peer-memory outboxes, ordered between ranks by device-side epoch words —
+is one library call; this module only exchanges the 64-byte handles once.
+halo="nccl" keeps a Python orchestration that sends ghost rows with NCCL
+point-to-point (torch.distributed), for fp16 state and for comparison.
 
 NVSwitch makes every peer equidistant, so slab r simply maps to rank r.  The
 exchange uses only neighbour point-to-point traffic; there is no collective
@@ -258,167 +265,41 @@ def _align(v: int, a: int = 256) -> int:
     return (v + a - 1) // a * a
 
 
-class PeerBlocks:
-    """Density across ranks with no ghost copy (the fused halo).
+def _handle_exchange(group):
+    """All ranks' 64-byte shard handles in rank order, over the process group."""
+    import torch.distributed as dist
 
-    Every rank bins and packs its own particles into ONE persistent device
-    allocation [cell_start | pos (float4) | mass | hmax] and exposes it to
-    its +-1 neighbours by CUDA IPC handle (exchanged over the process group
-    when a buffer is (re)allocated).  The density kernel then reads the
-    neighbours' boundary columns in place through the mapped peer pointers —
-    NVLink loads issued by the pair loop itself, overlapping its arithmetic —
-    so the step has no send/recv and no staging copy.  Two barriers order the
-    ranks: after every rank has packed (its block is complete before a
-    neighbour reads it) and before a rank overwrites its block (every
-    neighbour has finished reading the previous one).  The same code serves
-    ranks on one device (CUDA IPC between processes of one GPU, the tests)."""
-
-    def __init__(self, slab: Slab, refine: int = 2, prec: Optional[int] = None, group=None):
-        from . import api
-        self.api, self.slab, self.refine, self.group = api, slab, refine, group
-        self.prec = api.SF_PREC_NATIVE if prec is None else prec
-        self.NX = self.ny = self.nz = slab.nc * refine
-        self.cell = slab.cell / refine
-        self.x0, self.nx = slab.x0 * refine, (slab.x1 - slab.x0) * refine
-        self.x_origin = self.x0 * self.cell
-        self.ncell = self.nx * self.ny * self.nz
-        self.cap, self.buf, self.peers, self.perm, self.last = 0, None, {}, None, None
-
-    @staticmethod
-    def layout(ncell: int, cap: int):
-        """Byte offsets of pos, mass, hmax, vel, pf and the total size."""
-        pos = _align(4 * (ncell + 1))
-        mass = pos + 16 * cap
-        hmax = _align(mass + 4 * cap)
-        vel = hmax + 256
-        pf = vel + 16 * cap
-        return pos, mass, hmax, vel, pf, _align(pf + 4 * cap)
-
-    def _barrier(self):
-        if self.slab.world > 1:
-            import torch.distributed as dist
-            torch.cuda.synchronize()
-            dist.barrier(group=self.group)
-
-    def _ensure(self, n: int):
-        import torch.distributed as dist
-        grow = n > self.cap
-        retired = None
-        if grow:
-            retired = self.buf  # freed only after every neighbour has unmapped it
-            self.cap = max(int(n * 1.2) + 1024, 1024)
-            self.buf = self.api.DeviceBuffer(self.layout(self.ncell, self.cap)[-1])
-        if self.slab.world == 1:
-            if retired is not None:
-                retired.free()
-            return
-        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
-        flag = torch.tensor([int(grow)], device=dev)
-        dist.all_reduce(flag, group=self.group)
-        if int(flag.item()) == 0:
-            return
-        info = (self.buf.ipc_handle(), self.cap, self.x0, self.nx, self.ncell, self.x_origin)
-        every = [None] * self.slab.world
-        dist.all_gather_object(every, info, group=self.group)
-        for r, old in list(self.peers.items()):
-            old[0].free()  # unmap the neighbour's previous block
-        self.peers = {}
-        for r in (self.slab.rank - 1, self.slab.rank + 1):
-            if 0 <= r < self.slab.world:
-                hd, cap, x0, nx, ncell, xo = every[r]
-                self.peers[r] = (self.api.DeviceBuffer(handle=hd), cap, x0, nx, ncell, xo)
-        dist.barrier(group=self.group)  # every mapping of the retired blocks is closed
-        if retired is not None:
-            retired.free()
-
-    def _peer_block(self, r, force=False):
-        mapped, cap, x0, nx, ncell, xo = self.peers[r]
-        pos, mass, hmax, vel, pf, _ = self.layout(ncell, cap)
-        base = mapped.ptr
-        if force:
-            return self.api.force_block(base + pos, base + vel, base + pf, base, base + hmax, x0, nx, xo)
-        return self.api.cell_block(base + pos, base + mass, base, base + hmax, x0, nx, xo)
-
-    def __call__(self, x, m, h, out=None) -> torch.Tensor:
-        """rho of this rank's particles (x, m, h in particle order), into `out`
-        (fp32, n) when given."""
-        api = self.api
-        n = m.shape[0]
-        self._barrier()  # the neighbours are done reading the previous block
-        self._ensure(n)
-        posb, massb, hmaxb, _, _, _ = self.layout(self.ncell, self.cap)
-        cs = self.buf.tensor(0, (self.ncell + 1,), torch.int32)
-        pos = self.buf.tensor(posb, (self.cap, 4), torch.float32)[:n]
-        mass = self.buf.tensor(massb, (self.cap,), torch.float32)[:n]
-        hmax = self.buf.tensor(hmaxb, (4,), torch.int32)
-        if self.perm is None or self.perm.shape[0] < n:
-            self.perm = torch.empty(max(self.cap, 1), dtype=torch.int32, device="cuda")
-        _mark("bin")
-        api.bin_particles(x.float().contiguous(), (self.x_origin, 0.0, 0.0), self.cell, (self.nx, self.ny, self.nz),
-                          cell_start=cs, perm=self.perm[:max(n, 1)])
-        _mark("pack")
-        api.cells_pack(x.contiguous(), m.contiguous(), h.contiguous(), self.perm, pos, mass, hmax, self.prec)
-        self._barrier()  # every block of this step is complete
-        _mark("pairs")
-        blocks = [api.cell_block(pos, mass, cs, hmax, self.x0, self.nx, self.x_origin)]
-        blocks += [self._peer_block(r) for r in sorted(self.peers)]
-        rho = api.density_cells_blocks(blocks, n, self.perm, (0.0, 0.0), self.cell, self.NX, self.ny, self.nz,
-                                       reach=self.refine, rho=out)
-        self.last = {"cs": cs, "perm": self.perm[:max(n, 1)], "n": n}  # valid until the next call
-        _mark("store")
-        return rho[:n]
-
-    def force(self, v, m, rho, P, a=None, du=None):
-        """(a, du) of this rank's particles, after __call__ in the same step
-        (same positions: the block's cell list and pos are reused); the
-        neighbours' (pos, vel, P/rho^2) are read in place."""
-        api = self.api
-        n = m.shape[0]
-        if self.last is None or self.last["n"] != n:
-            raise RuntimeError("PeerBlocks.force needs the density of the same particles first")
-        self._barrier()  # the neighbours are done reading the previous vel / pf
-        posb, _, hmaxb, velb, pfb, _ = self.layout(self.ncell, self.cap)
-        cs = self.buf.tensor(0, (self.ncell + 1,), torch.int32)
-        pos = self.buf.tensor(posb, (self.cap, 4), torch.float32)
-        hmax = self.buf.tensor(hmaxb, (4,), torch.int32)
-        vel = self.buf.tensor(velb, (self.cap, 4), torch.float32)[:max(n, 1)]
-        pf = self.buf.tensor(pfb, (self.cap,), torch.float32)[:max(n, 1)]
-        api.force_pack(v.contiguous(), m.contiguous(), rho.contiguous(), P.contiguous(), self.perm, vel, pf,
-                       self.prec)
-        self._barrier()  # every (vel, pf) of this step is complete
-        blocks = [api.force_block(pos, vel, pf, cs, hmax, self.x0, self.nx, self.x_origin)]
-        blocks += [self._peer_block(r, force=True) for r in sorted(self.peers)]
-        a, du = api.force_cells_blocks(blocks, n, self.perm, (0.0, 0.0), self.cell, self.NX, self.ny, self.nz,
-                                       reach=self.refine, a=a, du=du)
-        return a[:n], du[:n]
-
-    def close(self):
-        for old in self.peers.values():
-            old[0].free()
-        self.peers = {}
-        if self.buf is not None:
-            self.buf.free()
-            self.buf = None
+    def run(mine: bytes):
+        every = [None] * dist.get_world_size(group)
+        dist.all_gather_object(every, mine, group=group)
+        return every
+    return run
 
 
 class ShardedState:
-    """One rank's particles: SoA buffer of the reference's default schema at
-    uniform storage precision `prec` (32 or 16; positions included)."""
+    """One rank's particles: SoA of the reference's default schema at uniform
+    storage precision `prec` (32 or 16; positions included).  halo="peer"
+    (default, prec 32): the state lives in the C++ shard (api.Shard) and every
+    step is one library call; halo="nccl": the Python ghost-row path."""
+
+    NAMES = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
 
     def __init__(self, n_global: int, slab: Slab, prec: int = 32, seed: int = 7, device="cuda",
-                 h: Optional[float] = None, halo: str = "peer", group=None, reorder_every: int = 0):
-        """reorder_every = k > 0: every k-th density also permutes the whole
-        state into that density's cell order (peer halo), so the next steps'
-        binning and pack gathers stay coherent (particles keep their ids)."""
+                 h: Optional[float] = None, halo: str = "peer", group=None, refine: int = 2,
+                 capacity: Optional[int] = None):
         from . import api
-        self.api, self.slab, self.prec, self.device = api, slab, prec, device
-        self.reorder_every, self._densities = reorder_every, 0
+        self.api, self.slab, self.prec, self.device, self.group = api, slab, prec, device, group
         if halo not in ("peer", "nccl"):
             raise ValueError("halo must be 'peer' (neighbour blocks read in place) or 'nccl' (ghost rows sent)")
-        self.halo = halo
-        self._peer = PeerBlocks(slab, 2, {32: api.SF_PREC_NATIVE, 16: 16}[prec], group) if halo == "peer" else None
+        if halo == "peer" and prec != 32:
+            raise ValueError("the C++ shard holds binary32 state (C5 storage); use halo='nccl' for prec 16")
+        self.halo, self.refine = halo, refine
         self.schema = api.Schema.default()
         self.h = h if h is not None else grid_for(n_global)[0]
+        # one capacity for every rank (the shards check it when they connect)
+        self.capacity = capacity or (3 * n_global) // (2 * slab.world) + (1 << 16)
+        self._shard = None
+        self.last_metrics = None
         n = n_global // slab.world
         g = torch.Generator(device=device).manual_seed(seed + slab.rank)
         x = torch.rand(n, 3, generator=g, device=device, dtype=torch.float64)
@@ -442,34 +323,52 @@ class ShardedState:
     def view(self, n):
         return self.api.View(self.schema, n, "soa", None, self.prec)
 
-    NAMES = ["x", "id", "v", "u", "m", "h", "rho", "P", "cs", "a", "du", "dt"]
+    @property
+    def n(self) -> int:
+        return self._shard.count if self._shard is not None else self._n
 
     def set_fields(self, fields):
+        if self._shard is not None:
+            raise RuntimeError("the state already lives in the C++ shard")
         self._binning = None
         n = fields["id"].shape[0]
-        self.n = n
+        self._n = n
         self.buf = self.api.PackedBuffer.empty(self.view(n), self.device)
         for name, t in fields.items():
             _, _, w, _ = self.buf.view.lane(name)
             dt = torch.int64 if name == "id" else FIELD_DTYPES[w]
             self.stream_bytes(name).copy_(t.to(dt).contiguous().view(torch.uint8).reshape(n, -1))
 
+    def shard(self):
+        """The C++ shard (created and loaded on first use; halo='peer')."""
+        if self._shard is None:
+            s = self.slab
+            exchange = _handle_exchange(self.group) if s.world > 1 else None
+            self._shard = self.api.Shard(s.rank, s.world, s.nc, s.cell, self.refine, self.capacity, exchange)
+            self._shard.load(self.buf)
+            self.buf = None
+        return self._shard
+
     def stream_bytes(self, name) -> torch.Tensor:
         """The field's stream as (n, bytes per particle) uint8 — valid at any
         offset (the reference SoA packs streams back to back, so e.g. the
         int64 id stream of an odd particle count is not 8-byte aligned)."""
+        if self._shard is not None:
+            t = self._shard.field(name)
+            return t.contiguous().view(torch.uint8).reshape(t.shape[0], -1)
         base, stride, w, ar = self.buf.view.lane(name)
-        nbytes = self.n * ar * w // 8
-        return self.buf.data[base // 8: base // 8 + nbytes].view(self.n, ar * w // 8)
+        nbytes = self._n * ar * w // 8
+        return self.buf.data[base // 8: base // 8 + nbytes].view(self._n, ar * w // 8)
 
     def stream(self, name) -> torch.Tensor:
-        """Typed view of a float field's stream (their offsets stay aligned:
-        every stream before them is a multiple of the float width)."""
+        """Typed view of a field's stream ((n, 3) for x / v / a)."""
+        if self._shard is not None:
+            return self._shard.field(name)
         base, stride, w, ar = self.buf.view.lane(name)
         dt = torch.int64 if name == "id" else FIELD_DTYPES[w]
-        nbytes = self.n * ar * w // 8
+        nbytes = self._n * ar * w // 8
         t = self.buf.data[base // 8: base // 8 + nbytes].view(dt)
-        return t.view(self.n, ar) if ar == 3 else t
+        return t.view(self._n, ar) if ar == 3 else t
 
     def rows(self) -> torch.Tensor:
         """All fields of every particle as one byte row (for migration)."""
@@ -488,17 +387,25 @@ class ShardedState:
         self.set_fields(fields)
 
     # -- the step ---------------------------------------------------------------
+    def _run(self, kernels: str, dt: float = 1e-3, timed: bool = False):
+        self.last_metrics = self.shard().step(kernels, dt, timed=timed)
+        return self.last_metrics
+
     def kick_drift(self, dt=1e-3):
+        if self.halo == "peer":  # the shard migrates right after the drift
+            self._run("kick,drift", dt)
+            return
         self._binning = None  # positions change
         self.api.run_kernel(self.buf, "kick", dt, buffer_size=1)
         self.api.run_kernel(self.buf, "drift", dt, buffer_size=1)
 
     def migrate(self, group=None):
-        """Particles whose layer left the slab move to the neighbour.  Only the
-        leaving particles are packed into rows and sent; the new SoA buffer is
-        written in one pass per field (kept particles gathered in order, then
-        the received rows) — no full row materialisation of the rank."""
-        if self.slab.world == 1:
+        """Particles whose layer left the slab move to the neighbour (the
+        peer-halo shard migrates inside every step; this is the nccl path's).
+        Only the leaving particles are packed into rows and sent; the new SoA
+        buffer is written in one pass per field (kept particles gathered in
+        order, then the received rows)."""
+        if self.slab.world == 1 or self.halo == "peer":
             return
         ix = self.slab.layer(self.stream("x")[:, 0])
         go_l, go_r = ix < self.slab.x0, ix >= self.slab.x1
@@ -510,8 +417,8 @@ class ShardedState:
         recv = torch.cat([rl, rr], dim=0)
         keep_buf = self.buf  # alive until every field is copied out
         nk = keep.numel()
-        self.n = nk + recv.shape[0]
-        self.buf = self.api.PackedBuffer.empty(self.view(self.n), self.device)
+        self._n = nk + recv.shape[0]
+        self.buf = self.api.PackedBuffer.empty(self.view(self._n), self.device)
         self._binning = None
         c = 0
         for k in self.NAMES:
@@ -523,81 +430,53 @@ class ShardedState:
         del keep_buf
 
     def density(self, group=None):
-        x, m, h = self.stream("x"), self.stream("m"), self.stream("h")
-        if self._peer is not None:  # fused halo: the neighbours' blocks are read in place
-            _mark("halo")
-            self._peer.group = group
-            dst = self.stream("rho")
-            direct = dst.dtype == torch.float32 and dst.is_contiguous() and self.n > 0
-            rho = self._peer(x, m, h, out=dst if direct else None)  # fp32 state: written in place
-            # at world 1 the own-block grid is the force's local grid: its binning is reusable
-            self._binning = self._peer.last if self.slab.world == 1 else None
-            if not direct:
-                dst.copy_(rho.to(dst.dtype))
-            _mark("end")
+        if self.halo == "peer":
+            self._run("density")
             return
+        x, m, h = self.stream("x"), self.stream("m"), self.stream("h")
         _mark("halo")
         gx, gm, gh = exchange_halo(x, m, h, self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
         self._binning = {}
-        rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec, keep=self._binning))
+        rho = density_with_ghosts(x, m, h, gx, gm, gh, self.slab, gpu_density_backend(prec, self.refine,
+                                                                                          keep=self._binning))
         self.stream("rho").copy_(rho.to(self.stream("rho").dtype))
         _mark("end")
 
     def force(self, group=None):
         """Cell-linked force with the neighbours' (x, v, m, h, rho, P) as
         ghosts (second halo, after every rank has its rho)."""
+        if self.halo == "peer":
+            self._run("force")
+            return
         names = ["x", "v", "m", "h", "rho", "P"]
         own = [self.stream(k) for k in names]
-        if self._peer is not None:  # fused halo: the neighbours' (pos, vel, P/rho^2) read in place
-            _mark("halo2")
-            sa, sd = self.stream("a"), self.stream("du")
-            direct = (sa.dtype == torch.float32 and sd.dtype == torch.float32 and sa.is_contiguous() and
-                      sd.is_contiguous() and self.n > 0)
-            a, du = self._peer.force(own[1], own[2], own[4], own[5], *((sa, sd) if direct else ()))
-            if not direct:
-                sa.copy_(a.to(sa.dtype))
-                sd.copy_(du.to(sd.dtype))
-            _mark("end2")
-            return
         _mark("halo2")
         ghosts = exchange_ghost_fields(own, own[0][:, 0], self.slab, group)
         prec = {32: self.api.SF_PREC_NATIVE, 16: 16}[self.prec]
-        a, du = force_with_ghosts(own, ghosts, self.slab, gpu_force_backend(prec, binning=self._binning))
+        a, du = force_with_ghosts(own, ghosts, self.slab, gpu_force_backend(prec, self.refine, binning=self._binning))
         self.stream("a").copy_(a.to(self.stream("a").dtype))
         self.stream("du").copy_(du.to(self.stream("du").dtype))
         _mark("end2")
 
-    def reorder_by_density(self):
-        """Permute every field into the cell order of the last density call
-        (its perm: sorted position -> particle) with one sf_b200_permute."""
-        last = self._peer.last if self._peer is not None else None
-        if last is None or last["n"] != self.n or self.n == 0:
-            return
-        view = self.buf.view
-        out = self.api.PackedBuffer(view, torch.empty(view.nbytes + 16, dtype=torch.uint8, device=self.device))
-        self.buf = self.api.permute(self.buf, last["perm"][: self.n], out=out)
-        self._peer.last = None  # its perm indexes the old order
-        self._binning = None
-
-    def maybe_reorder(self):
-        self._densities += 1
-        if self.reorder_every > 0 and self._peer is not None and self._densities % self.reorder_every == 0:
-            self.reorder_by_density()
-
-    def full_step(self, dt=1e-3, group=None):
+    def full_step(self, dt=1e-3, group=None, timed: bool = False):
         """The reference timestep order (density -> force -> kick -> drift,
         pipelines.cpp / bench.cpp kernel lists), then migration."""
+        if self.halo == "peer":
+            return self._run("density,force,kick,drift", dt, timed)
         self.density(group)
         self.force(group)
-        self.maybe_reorder()  # after the force: it still uses the density's perm
         self.kick_drift(dt)
         self.migrate(group)
+        return None
 
     def sort_by_cell(self, refine: int = 2):
-        """Reorder every field into cell order (the density binning's order), so
-        each step's permutation is near-identity and its gathers stay coherent
-        (particles move far less than a cell per step)."""
+        """Reorder every field into cell order (the density binning's order),
+        before the first step: each step's permutation is then near-identity
+        and its gathers stay coherent (the peer-halo shard keeps the order
+        itself: its migration rewrites the stayers in cell order)."""
+        if self._shard is not None:
+            raise RuntimeError("sort_by_cell runs before the first step")
         from . import api
         cell = self.slab.cell / refine
         lo_layer = self.slab.local_lo
@@ -608,7 +487,12 @@ class ShardedState:
         self.from_rows(self.rows()[p])
 
     def step(self, dt=1e-3, group=None):
+        """kick, drift, migrate, then density of the new positions."""
         self.kick_drift(dt)
         self.migrate(group)
         self.density(group)
-        self.maybe_reorder()
+
+    def close(self):
+        if self._shard is not None:
+            self._shard.close()
+            self._shard = None

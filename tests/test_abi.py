@@ -162,6 +162,17 @@ def test_gpu_entry_points_fail_loudly_without_device():
     assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
     st = L.lib().sf_b200_run_kernel(src.handle, C.cast(buf, C.c_void_p), b"kick,drift", 1e-3, 64, 0, 0, None)
     assert st == L.SF_ERROR and "no CUDA device" in L.lib().sf_last_error().decode()
+    with pytest.raises(L.SfError, match="no CUDA device"):
+        api.Shard(0, 1, 8, 0.125)
+
+
+def test_shard_argument_checks():
+    """sf_b200_shard_*: null arguments are SF_INVALID_ARG before any device work."""
+    lib = L.lib()
+    assert lib.sf_b200_shard_create(0, 1, 8, 0.125, 2, 1000, None) == L.SF_INVALID_ARG
+    assert lib.sf_b200_shard_step(None, b"density", 1e-3, None, None) == L.SF_INVALID_ARG
+    assert lib.sf_b200_shard_connect(None, None) == L.SF_INVALID_ARG
+    lib.sf_b200_shard_destroy(None)  # no-op, like the reference's *_destroy(NULL)
 
 
 def test_plain_c_consumer_links_and_runs(tmp_path):

@@ -186,48 +186,66 @@ def test_density_blocks_read_neighbours_in_place(world, refine):
         assert np.all(np.abs(du[: S[r]["n"]].double().cpu().numpy() - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
 
 
-def _peer_worker(rank, world, port, outdir, n):
-    import os
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    sys.path.insert(0, root)
-    sys.path.insert(0, os.path.join(root, "oracle"))
-    import torch.distributed as dist
-    from paper_2512_05516_b200.sharded import PeerBlocks
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)  # every rank on the one device: CUDA IPC between processes of one GPU
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _population(n):
     rng = np.random.default_rng(31)
     x = rng.random((n, 3))
     h, nc, cell = grid_for(n)
     m = rng.uniform(0.5, 1.5, n) / n
+    v = np.random.default_rng(32).uniform(-1, 1, (n, 3))
+    P = np.random.default_rng(33).uniform(0.2, 1.2, n)
+    return x, m, h, nc, cell, v, P
+
+
+def _shard_worker(rank, world, port, outdir, n):
+    """One rank of api.Shard (the C++ sharded step behind the C ABI): its
+    slab's particles of a shared population, density then force."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # every rank on the one device: CUDA IPC between processes of one GPU
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2512_05516_b200.sharded import _handle_exchange
+    x, m, h, nc, cell, v, P = _population(n)
     layer = np.minimum(np.floor(x[:, 0] / cell).astype(int), nc - 1)
     slab = Slab(nc, cell, rank, world)
     own = (layer >= slab.x0) & (layer < slab.x1)
-    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
-    pb = PeerBlocks(slab, 2)
-    rho = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))
-    rho2 = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))  # second step: buffers reused, no new handles
-    if rank == 0:
-        pb.cap = 0  # rank 0 reallocates its block: every rank re-exchanges handles and re-maps
-    rho3 = pb(t(x[own]), t(m[own]), t(np.full(own.sum(), h)))
-    assert torch.equal(rho3, rho2)
-    v = np.random.default_rng(32).uniform(-1, 1, (n, 3))
-    a, du = pb.force(t(v[own]), t(m[own]), rho2, rho2 * 0.7)
-    np.savez(os.path.join(outdir, f"p{rank}.npz"), own=own, rho=rho.cpu().numpy(), rho2=rho2.cpu().numpy(),
-             npeers=len(pb.peers), a=a.cpu().numpy(), du=du.cpu().numpy())
+    k = int(own.sum())
+    S = api.Schema.default()
+    buf = api.PackedBuffer.empty(api.View(S, k, "soa", None, 32))
+    vals = {"x": x[own], "id": np.nonzero(own)[0], "v": v[own], "u": np.ones(k), "m": m[own], "h": np.full(k, h),
+            "rho": np.ones(k), "P": P[own], "cs": np.zeros(k), "a": np.zeros((k, 3)), "du": np.zeros(k),
+            "dt": np.full(k, 1e-3)}
+    for name, arr in vals.items():
+        base, _, w, ar = buf.view.lane(name)
+        t = torch.tensor(arr, dtype=torch.int64 if name == "id" else torch.float32, device="cuda")
+        buf.data[base // 8: base // 8 + t.numel() * t.element_size()].copy_(t.reshape(-1).view(torch.uint8))
+    sh = api.Shard(rank, world, nc, cell, 2, 3 * n // world, _handle_exchange(None))
+    sh.load(buf)
+    sh.step("density")
+    rho = sh.field("rho").clone()
+    ids = sh.field("id").clone()
+    sh.step("density")  # again: epochs advance, the blocks are rebuilt in place
+    assert torch.equal(sh.field("rho"), rho)
+    m1 = sh.step("force", timed=True)
+    np.savez(os.path.join(outdir, f"p{rank}.npz"), id=ids.cpu().numpy(), rho=rho.cpu().numpy(),
+             a=sh.field("a").cpu().numpy(), du=sh.field("du").cpu().numpy(), n=sh.count,
+             force_ms=m1["force_ms"])
     torch.cuda.synchronize()
     dist.barrier()
-    pb.close()
+    sh.close()
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_peer_blocks_across_processes_cuda_ipc(tmp_path, world):
-    """PeerBlocks in `world` processes sharing one GPU: every rank maps its
-    neighbours' blocks by CUDA IPC handle (the multi-GPU mechanism) and the
-    per-rank densities equal the global oracle's."""
+def test_shard_across_processes_reads_neighbours_in_place(tmp_path, world):
+    """api.Shard in `world` processes sharing one GPU: each maps its
+    neighbours' blocks by CUDA IPC handle (the multi-GPU mechanism), the
+    ranks order each other with device-side epochs, and the per-rank density
+    and force equal the global oracle's."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -235,33 +253,25 @@ def test_peer_blocks_across_processes_cuda_ipc(tmp_path, world):
     port = s.getsockname()[1]
     s.close()
     n = 1 << 15
-    mp.spawn(_peer_worker, args=(world, port, str(tmp_path), n), nprocs=world, join=True)
-    rng = np.random.default_rng(31)
-    x = rng.random((n, 3))
-    h, nc, cell = grid_for(n)
-    m = rng.uniform(0.5, 1.5, n) / n
+    mp.spawn(_shard_worker, args=(world, port, str(tmp_path), n), nprocs=world, join=True)
+    x, m, h, nc, cell, v, P = _population(n)
     dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
     want = O.density_cells(dec(x).reshape(-1), dec(m), dec(np.full(n, h)), 0.0, 1.0, cell)
-    seen = np.zeros(n, bool)
-    rho_all = np.zeros(n)
-    for r in range(world):
-        d = np.load(tmp_path / f"p{r}.npz")
-        np.testing.assert_allclose(d["rho"], want[d["own"]], rtol=1e-5)
-        assert np.array_equal(d["rho"], d["rho2"])
-        assert int(d["npeers"]) == (1 if r in (0, world - 1) else 2)
-        seen |= d["own"]
-        rho_all[d["own"]] = d["rho"]
+    rho_all, seen = np.zeros(n), np.zeros(n, bool)
+    outs = [np.load(tmp_path / f"p{r}.npz") for r in range(world)]
+    for d in outs:
+        ids = d["id"]
+        np.testing.assert_allclose(d["rho"], want[ids], rtol=1e-5)
+        assert not seen[ids].any()
+        seen[ids] = True
+        rho_all[ids] = d["rho"]
     assert seen.all()
-    # the force read the neighbours' (pos, vel, P/rho^2) blocks in place
-    v = np.random.default_rng(32).uniform(-1, 1, (n, 3))
-    P = (torch.tensor(rho_all, dtype=torch.float32) * 0.7).double().numpy()
-    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(np.full(n, h)), rho_all, P,
-                                    0.0, 1.0, cell)
-    for r in range(world):
-        d = np.load(tmp_path / f"p{r}.npz")
-        own = d["own"]
-        assert np.all(np.linalg.norm(d["a"] - wa[own], axis=1) <= 2e-5 * sa[own])
-        assert np.all(np.abs(d["du"] - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(np.full(n, h)), rho_all,
+                                    dec(P), 0.0, 1.0, cell)
+    for d in outs:
+        ids = d["id"]
+        assert np.all(np.linalg.norm(d["a"] - wa[ids], axis=1) <= 2e-5 * sa[ids])
+        assert np.all(np.abs(d["du"] - wdu[ids]) <= 2e-5 * sd[ids] + 1e-30)
 
 
 def _state_worker(rank, world, port, outdir, n, full):
@@ -275,7 +285,7 @@ def _state_worker(rank, world, port, outdir, n, full):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     h, nc, cell = grid_for(n)
-    st = ShardedState(n, Slab(nc, cell, rank, world), prec=32, h=h)
+    st = ShardedState(n, Slab(nc, cell, rank, world), prec=32, h=h, group=None)
     for _ in range(3):  # large dt: particles cross slab planes every step
         if full:
             st.stream("P").copy_(st.stream("rho") * 0.7)
@@ -289,9 +299,10 @@ def _state_worker(rank, world, port, outdir, n, full):
     np.savez(os.path.join(outdir, f"s{rank}.npz"), id=st.stream_bytes("id").cpu().numpy().view(np.int64).ravel(),
              x=st.stream("x").double().cpu().numpy(), rho=st.stream("rho").double().cpu().numpy(),
              m=st.stream("m").double().cpu().numpy(), h=st.stream("h").double().cpu().numpy(),
-             inside=bool(((lay >= st.slab.x0) & (lay < st.slab.x1)).all()), n=st.n)
+             inside=bool(((lay >= st.slab.x0) & (lay < st.slab.x1)).all()), n=st.n,
+             sent=(st.last_metrics or {}).get("sent", -1))
     dist.barrier()
-    st._peer.close()
+    st.close()
     dist.destroy_process_group()
 
 
@@ -357,30 +368,6 @@ def test_uniform_h_path_is_bit_identical(refine):
     np.testing.assert_allclose(fast[:n].double().cpu().numpy(), want, rtol=1e-5)
 
 
-def test_state_reorder_keeps_the_physics():
-    """reorder_every=1 permutes the whole state into each density's cell order
-    (sf_b200_permute); particles keep their ids and, matched by id, every field
-    agrees with the unreordered run (summation order inside cells differs, so
-    fp32 sums agree to rounding)."""
-    n = 1 << 15
-    h, nc, cell = grid_for(n)
-    runs = []
-    for k in (0, 1):
-        st = ShardedState(n, Slab(nc, cell, 0, 1), prec=32, h=h, reorder_every=k)
-        st.sort_by_cell()
-        for _ in range(3):
-            st.full_step()
-        ids = st.stream("id").cpu().numpy()
-        order = np.argsort(ids)
-        runs.append({f: st.stream(f).double().cpu().numpy()[order] for f in ("x", "v", "rho", "a", "u")})
-        runs[-1]["id"] = ids[order]
-        if k:
-            assert not np.array_equal(ids, np.sort(ids))  # the state really was reordered
-    np.testing.assert_array_equal(runs[0]["id"], runs[1]["id"])
-    for f in ("x", "v", "rho", "a", "u"):
-        np.testing.assert_allclose(runs[1][f], runs[0][f], rtol=2e-4, atol=1e-6, err_msg=f)
-
-
 @pytest.mark.parametrize("workload", ["c2", "c5"])
 def test_bench_under_torchrun_two_ranks_one_device(workload, tmp_path):
     """bench.py under torchrun with 2 ranks (both on cuda:0 over gloo,
@@ -391,7 +378,7 @@ def test_bench_under_torchrun_two_ranks_one_device(workload, tmp_path):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    extra = ["--no-e2e", "--no-cpu"] if workload == "c2" else \
+    extra = ["--no-e2e", "--no-cpu", "--no-extras"] if workload == "c2" else \
         ["--workload", "c5", "--c5-n", str(1 << 20), "--no-cpu"]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(29600 + (workload == "c5")), os.path.join(root, "bench.py"), "--gpus", "2",
