@@ -492,8 +492,9 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
         }
         mark(int(2 * ki + 1));
     }
-    // nobody reads this rank's block after this point of the step
-    if (binned) signal(S, E_READ_DONE, st);
+    // nobody reads this rank's block after this point of the step (signalled every step, binned or not:
+    // a neighbour that bins in the next step waits for this epoch)
+    signal(S, E_READ_DONE, st);
     mark(8);
     uint64_t sent[2] = {0, 0};
     if (S->world > 1) {
