@@ -9,7 +9,7 @@
 //                ships narrowed records (streamed_bytes_one_way,
 //                pipelines.cpp:434-441) — here the narrowing is the DMA's
 //                own stride, no host-side gather.
-//   MANAGED  (1) cudaMallocManaged AoS (preferred location: host); per chunk
+//   MANAGED  (1) cudaMallocManaged AoS, no placement hints; per chunk
 //                cudaMemPrefetchAsync to the GPU, kernels run in place on the
 //                migrated pages, prefetch back.
 //   INPLACE  (2) pinned host AoS, whole records each way (the reference's
@@ -138,9 +138,18 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
         }
     }
     if (managed) {
+        // MANAGED_MAPPED keeps the pages on the host and maps them for the GPU; MANAGED migrates them with
+        // prefetches and runs best without hints (profiles/r02_managed_probe.log: 356 ms vs 418 ms with
+        // PreferredLocation = CPU + AccessedBy; the limiter is the migration back to the host, 25 GB/s
+        // against 57 GB/s of pinned D2H DMA)
         const size_t total = size_t((n * rb + 7) / 8);
-        check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId), "advise");
-        check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetAccessedBy, dev), "advise");
+        if (mode == 3) {
+            check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId), "advise");
+            check_cuda(cudaMemAdvise(host, total, cudaMemAdviseSetAccessedBy, dev), "advise");
+        } else {
+            check_cuda(cudaMemAdvise(host, total, cudaMemAdviseUnsetPreferredLocation, cudaCpuDeviceId), "advise");
+            check_cuda(cudaMemAdvise(host, total, cudaMemAdviseUnsetAccessedBy, dev), "advise");
+        }
     }
 
     cudaEvent_t t0, t1;

@@ -7,5 +7,5 @@ timeout 900 python bench.py --workload c3 --steps 20 --warmup 3 > gpurun_out/ben
 echo "bench c3 exit $?"
 timeout 900 python bench.py --workload c5 --steps 5 --warmup 2 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 echo "bench c5 exit $?"
-timeout 900 python bench.py --workload c5 --c5-full --steps 5 --warmup 2 > gpurun_out/bench_c5_full.json 2> gpurun_out/bench_c5_full.err
+timeout 900 python bench.py --workload c5 --steps 5 --warmup 2 > gpurun_out/bench_c5_full.json 2> gpurun_out/bench_c5_full.err
 echo "bench c5 full exit $?"

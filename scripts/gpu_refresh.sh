@@ -12,4 +12,4 @@ timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/r
 for w in c1 c3 c4 c5; do
   timeout 1200 python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/r01_bench_$w.json 2> gpurun_out/bench_$w.err; echo "$w $?"
 done
-timeout 1200 python bench.py --workload c5 --c5-full --steps 5 --warmup 2 > gpurun_out/r01_bench_c5_full.json 2>/dev/null; echo "c5 full $?"
+timeout 1200 python bench.py --workload c5 --steps 5 --warmup 2 > gpurun_out/r01_bench_c5_full.json 2>/dev/null; echo "c5 full $?"

@@ -97,7 +97,8 @@ def main():
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
         s = min(ts)
-        res[name] = {"ms": s * 1e3, "GBps_both_ways": 2 * v.nbytes / s / 1e9, "all_ms": [t * 1e3 for t in ts]}
+        res[name] = {"ms": s * 1e3, "GBps_both_ways": 2 * v.nbytes / s / 1e9, "GBps_one_way": v.nbytes / s / 1e9,
+                     "all_ms": [t * 1e3 for t in ts]}
         print(name, json.dumps(res[name]), flush=True)
 
     def prefetch_chunk(advise):
@@ -133,6 +134,18 @@ def main():
             d2h.wait_event(e2)
             prefetch(base + r0 * rb, cnt * rb, -1, d2h.cuda_stream)
 
+    def migrate_only(dev):
+        def body():
+            s = torch.cuda.current_stream()
+            prefetch(base, v.nbytes, dev, s.cuda_stream)
+        return body
+
+    def migrate_chunks(dev):
+        def body():
+            for k, (r0, cnt) in enumerate(chunks):
+                prefetch(base + r0 * rb, cnt * rb, dev, streams[k % 3].cuda_stream)
+        return body
+
     def pinned_inplace():
         api.run_host(v, pinned, api.View(P, N, "soa", "drift", 16), "drift", 1e-3, chunk=CHUNK, mode=2)
 
@@ -140,6 +153,13 @@ def main():
         api.run_host(v, managed, api.View(P, N, "soa", "drift", 16), "drift", 1e-3, chunk=CHUNK, mode=1)
 
     run("pinned_inplace", pinned_inplace)
+    # pure page migration, no kernels: the limiter of every managed variant
+    for rep in range(2):
+        run("migrate_whole_to_gpu_%d" % rep, migrate_only(0), reps=1)
+        run("migrate_whole_to_host_%d" % rep, migrate_only(-1), reps=1)
+    for rep in range(2):
+        run("migrate_chunks_to_gpu_%d" % rep, migrate_chunks(0), reps=1)
+        run("migrate_chunks_to_host_%d" % rep, migrate_chunks(-1), reps=1)
     run("run_host_mode1", managed_mode1)
     run("prefetch_chunk", prefetch_chunk(True))
     run("prefetch_chunk_na", prefetch_chunk(False))
