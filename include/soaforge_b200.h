@@ -154,21 +154,22 @@ SF_API sf_status sf_b200_density_cells(const void* x, const void* m, const void*
  * over its layers with lo = {x_origin, lo_yz[0], lo_yz[1]}) and packed
  * particles (sf_b200_cells_pack). */
 typedef struct sf_cell_block {
-    const void* pos;            /* float4 (x, y, z, h) per particle, cell-sorted */
-    const float* mass;          /* cell-sorted masses */
+    const void* pos;            /* float4 (x, y, z, m) per particle, cell-sorted */
+    const float* h;             /* cell-sorted smoothing lengths */
     const int32_t* cell_start;  /* nx*ny*nz + 1 entries */
     const uint32_t* hmax;       /* h range, 2 words: [0] largest h (float bits), [1] ~bits of the
-                                   smallest h (0 = unknown); equal ends select the uniform-h loop */
+                                   smallest h (0 = unknown); equal ends select the uniform-h loop,
+                                   which reads only pos */
     int32_t x0, nx;             /* global x-layers held by the block */
     float x_origin;             /* the lo[0] its binning used (layer x0 starts there) */
     int32_t reserved;           /* 0 */
 } sf_cell_block;
 #define SF_IPC_HANDLE_BYTES 64
 /* Packs x (3n), m, h (n) in `prec` through perm (sorted position -> particle)
- * into caller-owned pos_out (16*n bytes, 16-B aligned), mass_out (4*n) and
- * hmax_out (two words: the h range of sf_cell_block.hmax). */
+ * into caller-owned pos_out (float4 (x, y, z, m), 16*n bytes, 16-B aligned),
+ * h_out (4*n) and hmax_out (two words: the h range of sf_cell_block.hmax). */
 SF_API sf_status sf_b200_cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n,
-                                    const int32_t* perm, void* pos_out, float* mass_out,
+                                    const int32_t* perm, void* pos_out, float* h_out,
                                     uint32_t* hmax_out, void* stream);
 /* rho of the first n_home particles (particle order) of blocks[0] (n particles,
  * perm from its binning); candidates from every block. */
@@ -177,21 +178,20 @@ SF_API sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int n
                                               float cell, int nx_global, int ny, int nz, int reach,
                                               float* rho_out, void* stream);
 /* The force over the same blocks: a density block plus the same particles'
- * (v, m) as float4 and P/rho^2, packed in its cell-sorted order by
+ * (v, P/rho^2) as float4, packed in its cell-sorted order by
  * sf_b200_force_pack (rho == 0 -> SF_ERROR domain error; synchronizes). */
 typedef struct sf_force_block {
-    const void* pos;            /* the density block's float4 (x, y, z, h) */
-    const void* vel;            /* float4 (vx, vy, vz, m) */
-    const float* pf;            /* P / rho^2 */
+    const void* pos;            /* the density block's float4 (x, y, z, m) */
+    const void* vel;            /* float4 (vx, vy, vz, P/rho^2) */
+    const float* h;             /* the density block's smoothing lengths */
     const int32_t* cell_start;
     const uint32_t* hmax;       /* the density block's h range (2 words) */
     int32_t x0, nx;
     float x_origin;
     int32_t reserved;
 } sf_force_block;
-SF_API sf_status sf_b200_force_pack(const void* v, const void* m, const void* rho, const void* P, int prec,
-                                    uint64_t n, const int32_t* perm, void* vel_out, float* pf_out,
-                                    void* stream);
+SF_API sf_status sf_b200_force_pack(const void* v, const void* rho, const void* P, int prec, uint64_t n,
+                                    const int32_t* perm, void* vel_out, void* stream);
 SF_API sf_status sf_b200_force_cells_blocks(const sf_force_block* blocks, int nblocks, uint64_t n,
                                             const int32_t* perm, uint64_t n_home, const float* lo_yz,
                                             float cell, int nx_global, int ny, int nz, int reach,

@@ -19,13 +19,13 @@ SF_MODE_STREAMED, SF_MODE_MANAGED, SF_MODE_INPLACE, SF_MODE_MANAGED_MAPPED = 0, 
 
 class SfCellBlock(C.Structure):
     """sf_cell_block (include/soaforge_b200.h)."""
-    _fields_ = [("pos", C.c_void_p), ("mass", C.c_void_p), ("cell_start", C.c_void_p), ("hmax", C.c_void_p),
+    _fields_ = [("pos", C.c_void_p), ("h", C.c_void_p), ("cell_start", C.c_void_p), ("hmax", C.c_void_p),
                 ("x0", C.c_int32), ("nx", C.c_int32), ("x_origin", C.c_float), ("reserved", C.c_int32)]
 
 
 class SfForceBlock(C.Structure):
     """sf_force_block (include/soaforge_b200.h)."""
-    _fields_ = [("pos", C.c_void_p), ("vel", C.c_void_p), ("pf", C.c_void_p), ("cell_start", C.c_void_p),
+    _fields_ = [("pos", C.c_void_p), ("vel", C.c_void_p), ("h", C.c_void_p), ("cell_start", C.c_void_p),
                 ("hmax", C.c_void_p), ("x0", C.c_int32), ("nx", C.c_int32), ("x_origin", C.c_float),
                 ("reserved", C.c_int32)]
 
@@ -94,7 +94,7 @@ SYMBOLS = [
     ("sf_b200_force_cells", i32, [P] * 6 + [i32, u64, P, P, P, C.c_float] + [i32] * 4 + [u64, P, P, P]),
     ("sf_b200_cells_pack", i32, [P, P, P, i32, u64, P, P, P, P, P]),
     ("sf_b200_density_cells_blocks", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P]),
-    ("sf_b200_force_pack", i32, [P, P, P, P, i32, u64, P, P, P, P]),
+    ("sf_b200_force_pack", i32, [P, P, P, i32, u64, P, P, P]),
     ("sf_b200_force_cells_blocks", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P, P]),
     ("sf_b200_dev_alloc", i32, [u64, PP]),
     ("sf_b200_dev_free", i32, [P]),

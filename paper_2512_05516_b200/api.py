@@ -342,23 +342,24 @@ def force_cells(x, v, m, h, rho, P, cell_start, perm, lo, cell: float, dims, n_h
     return a, du
 
 
-def cells_pack(x, m, h, perm, pos, mass, hmax, prec: int = SF_PREC_NATIVE):
+def cells_pack(x, m, h, perm, pos, hs, hmax, prec: int = SF_PREC_NATIVE):
     """Pack x (n,3), m, h (n,) through perm (sorted position -> particle) into
-    caller-owned float4 pos (n,4), mass (n,) and hmax (>= 2 int32 words: the h
-    range, [0] bits of the largest h, [1] ~bits of the smallest)."""
+    caller-owned float4 pos (n,4) = (x, y, z, m), hs (n,) = h and hmax (>= 2
+    int32 words: the h range, [0] bits of the largest h, [1] ~bits of the
+    smallest)."""
     n = m.shape[0]
     _streams(prec, x=x, m=m, h=h)
     _int32s(perm=perm)
-    _f32s(pos=pos, mass=mass)
+    _f32s(pos=pos, hs=hs)
     check(lib().sf_b200_cells_pack(_ptr(x), _ptr(m), _ptr(h), prec, n, _ptr(perm) if perm is not None else None,
-                                   _ptr(pos), _ptr(mass), _ptr(hmax), _stream()))
+                                   _ptr(pos), _ptr(hs), _ptr(hmax), _stream()))
 
 
-def cell_block(pos, mass, cell_start, hmax, x0: int, nx: int, x_origin: float) -> "L.SfCellBlock":
+def cell_block(pos, hs, cell_start, hmax, x0: int, nx: int, x_origin: float) -> "L.SfCellBlock":
     """One sf_cell_block from device tensors or raw device addresses (ints);
     x_origin = the lo[0] the block's bin_particles used."""
     addr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
-    return L.SfCellBlock(addr(pos), addr(mass), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
+    return L.SfCellBlock(addr(pos), addr(hs), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
 
 
 def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,
@@ -378,20 +379,20 @@ def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: in
     return rho
 
 
-def force_pack(v, m, rho, P, perm, vel, pf, prec: int = SF_PREC_NATIVE):
-    """(v, m) -> float4 vel (n,4) and P/rho^2 -> pf (n,) in perm's order;
-    rho == 0 raises SfError (domain error)."""
-    n = m.shape[0]
-    _streams(prec, v=v, m=m, rho=rho, P=P)
+def force_pack(v, rho, P, perm, vel, prec: int = SF_PREC_NATIVE):
+    """(v, P/rho^2) -> float4 vel (n,4) in perm's order; rho == 0 raises
+    SfError (domain error)."""
+    n = rho.shape[0]
+    _streams(prec, v=v, rho=rho, P=P)
     _int32s(perm=perm)
-    _f32s(vel=vel, pf=pf)
-    check(lib().sf_b200_force_pack(_ptr(v), _ptr(m), _ptr(rho), _ptr(P), prec, n,
-                                   _ptr(perm) if perm is not None else None, _ptr(vel), _ptr(pf), _stream()))
+    _f32s(vel=vel)
+    check(lib().sf_b200_force_pack(_ptr(v), _ptr(rho), _ptr(P), prec, n,
+                                   _ptr(perm) if perm is not None else None, _ptr(vel), _stream()))
 
 
-def force_block(pos, vel, pf, cell_start, hmax, x0: int, nx: int, x_origin: float) -> "L.SfForceBlock":
+def force_block(pos, vel, hs, cell_start, hmax, x0: int, nx: int, x_origin: float) -> "L.SfForceBlock":
     addr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
-    return L.SfForceBlock(addr(pos), addr(vel), addr(pf), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
+    return L.SfForceBlock(addr(pos), addr(vel), addr(hs), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
 
 
 def force_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,

@@ -291,10 +291,10 @@ sf_status sf_b200_force_cells(const void* x, const void* v, const void* m, const
 static_assert(sizeof(sf_cell_block) == sizeof(CellBlockDesc), "sf_cell_block layout");
 
 sf_status sf_b200_cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
-                             void* pos_out, float* mass_out, uint32_t* hmax_out, void* stream) {
-    if ((n && (!x || !m || !h || !pos_out || !mass_out)) || !hmax_out) return fail(SF_INVALID_ARG, "null argument");
+                             void* pos_out, float* h_out, uint32_t* hmax_out, void* stream) {
+    if ((n && (!x || !m || !h || !pos_out || !h_out)) || !hmax_out) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
-        cells_pack(x, m, h, prec, n, perm, pos_out, mass_out, hmax_out, static_cast<cudaStream_t>(stream));
+        cells_pack(x, m, h, prec, n, perm, pos_out, h_out, hmax_out, static_cast<cudaStream_t>(stream));
         return SF_OK;
     });
 }
@@ -306,7 +306,7 @@ sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int nblocks,
     return guarded([&] {
         std::vector<CellBlockDesc> d(size_t(std::max(nblocks, 0)));
         for (int g = 0; g < nblocks; ++g)
-            d[g] = CellBlockDesc{blocks[g].pos,    blocks[g].mass,     blocks[g].cell_start, blocks[g].hmax,
+            d[g] = CellBlockDesc{blocks[g].pos,    blocks[g].h,        blocks[g].cell_start, blocks[g].hmax,
                                  blocks[g].x0,     blocks[g].nx,       blocks[g].x_origin,   0};
         density_cells_blocks(d.data(), nblocks, n, perm, n_home, lo_yz, cell, nx_global, ny, nz, reach, rho_out,
                              static_cast<cudaStream_t>(stream));
@@ -316,11 +316,11 @@ sf_status sf_b200_density_cells_blocks(const sf_cell_block* blocks, int nblocks,
 
 static_assert(sizeof(sf_force_block) == sizeof(ForceBlockDesc), "sf_force_block layout");
 
-sf_status sf_b200_force_pack(const void* v, const void* m, const void* rho, const void* P, int prec, uint64_t n,
-                             const int32_t* perm, void* vel_out, float* pf_out, void* stream) {
-    if (n && (!v || !m || !rho || !P || !vel_out || !pf_out)) return fail(SF_INVALID_ARG, "null argument");
+sf_status sf_b200_force_pack(const void* v, const void* rho, const void* P, int prec, uint64_t n, const int32_t* perm,
+                             void* vel_out, void* stream) {
+    if (n && (!v || !rho || !P || !vel_out)) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {
-        force_pack(v, m, rho, P, prec, n, perm, vel_out, pf_out, static_cast<cudaStream_t>(stream));
+        force_pack(v, rho, P, prec, n, perm, vel_out, static_cast<cudaStream_t>(stream));
         return SF_OK;
     });
 }
@@ -332,7 +332,7 @@ sf_status sf_b200_force_cells_blocks(const sf_force_block* blocks, int nblocks, 
     return guarded([&] {
         std::vector<ForceBlockDesc> d(size_t(std::max(nblocks, 0)));
         for (int g = 0; g < nblocks; ++g)
-            d[g] = ForceBlockDesc{blocks[g].pos,  blocks[g].vel, blocks[g].pf,       blocks[g].cell_start,
+            d[g] = ForceBlockDesc{blocks[g].pos,  blocks[g].vel, blocks[g].h,        blocks[g].cell_start,
                                   blocks[g].hmax, blocks[g].x0,  blocks[g].nx,       blocks[g].x_origin,
                                   0};
         force_cells_blocks(d.data(), nblocks, n, perm, n_home, lo_yz, cell, nx_global, ny, nz, reach, a_out, du_out,

@@ -9,9 +9,10 @@
 // index, so the result is deterministic).  The pass
 //
 //   k_pack        applies the sort permutation once and packs each particle
-//                 as a float4 (x, y, z, h) plus its mass (fp16/bf16 stream
+//                 as a float4 (x, y, z, m) plus its h (fp16/bf16 stream
 //                 values widen exactly), and finds the h range (largest and
-//                 smallest h: equal ends select the uniform-h pair loop);
+//                 smallest h: equal ends select the uniform-h pair loop, which
+//                 reads one float4 per candidate and nothing else);
 //   k_pairs_c     one thread per home particle of the own x-layers (a
 //                 contiguous range of the sorted order): for each of the
 //                 (2R+1)^2 (dx, dy) neighbour columns the cells of one
@@ -70,13 +71,13 @@ __device__ __forceinline__ void h_range(float hmax, float hmin, unsigned* __rest
 template <int P>
 __global__ void k_pack(const void* __restrict__ x, const void* __restrict__ m, const void* __restrict__ h,
                        const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ pos,
-                       float* __restrict__ mass, unsigned* __restrict__ hmax_bits) {
+                       float* __restrict__ hs, unsigned* __restrict__ hmax_bits) {
     float hmax = 0.0f, hmin = __int_as_float(0x7f800000);
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = perm ? uint64_t(perm[k]) : k;
         const float hi = ldf<P>(h, i);
-        pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), hi);
-        mass[k] = ldf<P>(m, i);
+        pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), ldf<P>(m, i));
+        hs[k] = hi;
         hmax = fmaxf(hmax, hi);
         hmin = fminf(hmin, hi);
     }
@@ -125,29 +126,30 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // same instructions: no support test, no branch, one MUFU.RCP and one
 // MUFU.SQRT (approximate forms; the sum stays within rel 1e-5 of the binary64
 // oracle, tests/test_gpu_parity.py).  hh_i = h_i / 2.
-__device__ __forceinline__ float pair_term(const float4 pi, float hh_i, const float4 pj, float mj) {
+// pj = (x, y, z, m) of the candidate, hj its smoothing length.
+__device__ __forceinline__ float pair_term(const float4 pi, float hh_i, const float4 pj, float hj) {
     const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
+    const float inv_h = rcp_approx(fmaf(0.5f, hj, hh_i));
     const float q = sqrt_approx(r2) * inv_h;
     const float t = fmaxf(2.0f - q, 0.0f);
     const float u = fmaxf(1.0f - q, 0.0f);
     const float w = fmaf(t * t, t, (u * u) * (-4.0f * u));
-    return (mj * (inv_h * inv_h * inv_h)) * w;
+    return (pj.w * (inv_h * inv_h * inv_h)) * w;
 }
 
-// pair_term when every candidate has the home's h (uniform smoothing length,
-// detected per launch from the blocks' h range): h_ij = h, so 1/h_ij and its
-// cube are per-home constants.  The same float operations in the same order
-// as pair_term with h_j = h_i, so the result is bit-identical.
-__device__ __forceinline__ float pair_term_u(const float4 pi, float inv_h, float ih3, const float4 pj, float mj) {
+// The spline factor alone when every candidate has the home's h (uniform
+// smoothing length, detected per launch from the blocks' h range): h_ij = h,
+// so 1/h_ij and its cube are per-home constants — the caller accumulates
+// m_j w with one FFMA and scales by 1/h^3 once per home.  The candidate is
+// one float4 (x, y, z, m): one load, no other array.
+__device__ __forceinline__ float pair_w_u(const float4 pi, float inv_h, const float4 pj) {
     const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float q = sqrt_approx(r2) * inv_h;
     const float t = fmaxf(2.0f - q, 0.0f);
     const float u = fmaxf(1.0f - q, 0.0f);
-    const float w = fmaf(t * t, t, (u * u) * (-4.0f * u));
-    return (mj * ih3) * w;
+    return fmaf(t * t, t, (u * u) * (-4.0f * u));
 }
 
 // The smoothing-length range of the candidate blocks: hmax word [0] = bits of
@@ -182,8 +184,8 @@ __device__ __forceinline__ bool uniform_h(const BS& B, float* hmax) {
 // place over NVLink through peer pointers, no ghost copy).  Each block covers
 // global x-layers [x0, x0 + nx) of one grid (shared origin, cell, ny, nz).
 struct CellBlock {
-    const float4* pos;
-    const float* mass;
+    const float4* pos;  // (x, y, z, m)
+    const float* h;
     const int32_t* cs;
     const unsigned* hmax;
     int x0, nx;
@@ -204,24 +206,21 @@ __device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __r
     const int64_t i_home = perm ? perm[k] : k;
     if (i_home >= G.n_home) return;  // ghosts: neighbours only
     const float4 pi = hpos[k];
+    const float h_i = B.b[0].h[k];
     // the binning formula of the own block (same origin, same rounding), then global layers
     const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell, fz = (pi.z - G.loz) * G.inv_cell;
     const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
     const float fx = fxl + float(hx0);
     const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
     const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
-    const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
+    const float rc = (h_i + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
     const float rc2 = rc * rc;
-    const float hh_i = 0.5f * pi.w;
-    const float inv_hu = rcp_approx(fmaf(0.5f, pi.w, hh_i));  // UNI: 1/h_ij for every candidate
+    const float hh_i = 0.5f * h_i;
+    const float inv_hu = rcp_approx(fmaf(0.5f, h_i, hh_i));  // UNI: 1/h_ij for every candidate
     const float ih3 = inv_hu * inv_hu * inv_hu;
     const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
     const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
     float acc = 0.0f;
-    auto term = [&](const float4 pj, float mj) {
-        if constexpr (UNI) return pair_term_u(pi, inv_hu, ih3, pj, mj);
-        else return pair_term(pi, hh_i, pj, mj);
-    };
 #pragma unroll 1
     for (int dxi = -R; dxi <= R; ++dxi) {
         const int jx = ix + dxi;
@@ -230,7 +229,7 @@ __device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __r
         while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
         if (g == B.nb) continue;  // layer held by no block
         const float4* __restrict__ pos = B.b[g].pos;
-        const float* __restrict__ mass = B.b[g].mass;
+        const float* __restrict__ hs = B.b[g].h;
         const int32_t* __restrict__ cell_start = B.b[g].cs;
         // faces of the global grid extend to infinity (binning clamps)
         const float ddx =
@@ -255,15 +254,24 @@ __device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __r
         for (int t = 0; t < W; ++t) {
             int j = b[t];
             for (; j + 1 < e[t]; j += 2) {
-                const float4 p0 = (pos[j]), p1 = (pos[j + 1]);
-                const float m0 = __ldg(mass + j), m1 = __ldg(mass + j + 1);
-                acc += term(p0, m0);
-                acc += term(p1, m1);
+                const float4 p0 = pos[j], p1 = pos[j + 1];
+                if constexpr (UNI) {
+                    acc = fmaf(p0.w, pair_w_u(pi, inv_hu, p0), acc);
+                    acc = fmaf(p1.w, pair_w_u(pi, inv_hu, p1), acc);
+                } else {
+                    acc += pair_term(pi, hh_i, p0, __ldg(hs + j));
+                    acc += pair_term(pi, hh_i, p1, __ldg(hs + j + 1));
+                }
             }
-            if (j < e[t]) acc += term((pos[j]), __ldg(mass + j));
+            if (j < e[t]) {
+                const float4 p0 = pos[j];
+                if constexpr (UNI) acc = fmaf(p0.w, pair_w_u(pi, inv_hu, p0), acc);
+                else acc += pair_term(pi, hh_i, p0, __ldg(hs + j));
+            }
         }
     }
-    rho[i_home] = acc * 0.079577471545947668f;  // 1 / (4 pi)
+    constexpr float k4pi = 0.079577471545947668f;  // 1 / (4 pi)
+    rho[i_home] = UNI ? acc * (ih3 * k4pi) : acc * k4pi;
 }
 
 template <int R>
@@ -299,32 +307,32 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
     if (sp < 0) throw std::invalid_argument("density_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
     float4* pos = nullptr;
-    float* mass = nullptr;
+    float* hs = nullptr;
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pos), 16 * n, st), "cudaMallocAsync");
-    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&mass), 4 * n + 16, st), "cudaMallocAsync");
-    unsigned* hmax = reinterpret_cast<unsigned*>(mass + n);
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&hs), 4 * n + 16, st), "cudaMallocAsync");
+    unsigned* hmax = reinterpret_cast<unsigned*>(hs + n);
     check_cuda(cudaMemsetAsync(hmax, 0, 2 * sizeof(unsigned), st), "memset");
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
     const int64_t nn = int64_t(n);
-    if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
-    else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
-    else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, mass, hmax);
+    if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, hs, hmax);
+    else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, hs, hmax);
+    else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, pos, hs, hmax);
     BlockSet B{};
-    B.b[0] = CellBlock{pos, mass, cell_start, hmax, 0, nx, lo[0]};
+    B.b[0] = CellBlock{pos, hs, cell_start, hmax, 0, nx, lo[0]};
     B.nb = 1;
     B.NX = nx;
     launch_pairs(B, perm, G, nn, reach, rho, st);
     check_cuda(cudaGetLastError(), "density_cells launch");
     count_launches(2);
     check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
-    check_cuda(cudaFreeAsync(mass, st), "cudaFreeAsync");
+    check_cuda(cudaFreeAsync(hs, st), "cudaFreeAsync");
 }
 
 // Pack for the block API: caller-owned, persistent outputs (so that other
 // ranks can read them in place through peer pointers).
 void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm, void* pos,
-                float* mass, unsigned* hmax, cudaStream_t st) {
+                float* hs, unsigned* hmax, cudaStream_t st) {
     require_device();
     if (n >= (1ull << 31)) throw std::invalid_argument("cells_pack: n must be < 2^31 per device");
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
@@ -334,9 +342,9 @@ void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t 
     if (reinterpret_cast<uintptr_t>(pos) & 15) throw std::invalid_argument("pos must be 16-byte aligned");
     float4* p4 = static_cast<float4*>(pos);
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, mass, hmax);
-    else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, mass, hmax);
-    else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, mass, hmax);
+    if (sp == SP_F32) k_pack<SP_F32><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, hs, hmax);
+    else if (sp == SP_F16) k_pack<SP_F16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, hs, hmax);
+    else k_pack<SP_BF16><<<blocks, 256, 0, st>>>(x, m, h, perm, n, p4, hs, hmax);
     check_cuda(cudaGetLastError(), "cells_pack launch");
     count_launches(1);
 }
@@ -353,10 +361,10 @@ void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const
     B.NX = NX;
     for (int g = 0; g < nb; ++g) {
         const CellBlockDesc& d = blocks[g];
-        if (!d.pos || !d.mass || !d.cell_start || !d.hmax) throw std::invalid_argument("null block pointer");
+        if (!d.pos || !d.h || !d.cell_start || !d.hmax) throw std::invalid_argument("null block pointer");
         if (d.nx <= 0 || d.x0 < 0 || d.x0 + d.nx > NX || int64_t(d.nx) * ny * nz >= (1ll << 31))
             throw std::invalid_argument("block layers outside the grid");
-        B.b[g] = CellBlock{static_cast<const float4*>(d.pos), d.mass, d.cell_start, d.hmax, d.x0, d.nx, d.x_origin};
+        B.b[g] = CellBlock{static_cast<const float4*>(d.pos), d.h, d.cell_start, d.hmax, d.x0, d.nx, d.x_origin};
     }
     if (n == 0) return;
     CellGrid G{blocks[0].x_origin, lo_yz[0], lo_yz[1], 1.0f / cell, NX, ny, nz, reach, int64_t(n_home)};
@@ -368,7 +376,7 @@ void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const
 // ------------------------------------------------------------------ force
 // Cell-linked force (sph.cpp:201-245 restated over cell neighbours; the
 // reference evaluates it inside 64-particle buffers).  k_pack_force packs per
-// sorted particle (x, y, z, h), (vx, vy, vz, m) and P/rho^2, flags rho == 0
+// sorted particle (x, y, z, m), (vx, vy, vz, P/rho^2) and h, flags rho == 0
 // (the reference's domain_error) and reduces h_max; k_force_c sweeps the same
 // culled column runs as k_pairs_c and accumulates, per home particle i,
 //   a_i  = -sum_j m_j (P_i/rho_i^2 + P_j/rho_j^2) dW/dr(r, h_ij) dx/r
@@ -383,16 +391,16 @@ template <int P>
 __global__ void k_pack_force(const void* __restrict__ x, const void* __restrict__ v, const void* __restrict__ m,
                              const void* __restrict__ h, const void* __restrict__ rho, const void* __restrict__ pr,
                              const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ pos,
-                             float4* __restrict__ vel, float* __restrict__ pf, unsigned* __restrict__ hmax_bits,
+                             float4* __restrict__ vel, float* __restrict__ hs, unsigned* __restrict__ hmax_bits,
                              unsigned* __restrict__ degenerate) {
     float hmax = 0.0f, hmin = __int_as_float(0x7f800000);
     bool zero = false;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = perm ? uint64_t(perm[k]) : k;
         const float hi = ldf<P>(h, i), ri = ldf<P>(rho, i);
-        pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), hi);
-        vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(m, i));
-        pf[k] = ldf<P>(pr, i) / (ri * ri);
+        pos[k] = make_float4(ldf<P>(x, 3 * i), ldf<P>(x, 3 * i + 1), ldf<P>(x, 3 * i + 2), ldf<P>(m, i));
+        vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(pr, i) / (ri * ri));
+        hs[k] = hi;
         hmax = fmaxf(hmax, hi);
         hmin = fminf(hmin, hi);
         zero |= ri == 0.0f;
@@ -407,12 +415,12 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     return r;
 }
 
-// Candidate blocks of the force: a density block's (x,y,z,h) plus the same
-// particles' (v, m) and P/rho^2, all in the block's cell-sorted order.
+// Candidate blocks of the force: a density block's (x,y,z,m) and h plus the
+// same particles' (v, P/rho^2), all in the block's cell-sorted order.
 struct ForceBlock {
-    const float4* pos;
-    const float4* vel;
-    const float* pf;
+    const float4* pos;  // (x, y, z, m)
+    const float4* vel;  // (vx, vy, vz, P/rho^2)
+    const float* h;
     const int32_t* cs;
     const unsigned* hmax;
     int x0, nx;
@@ -433,6 +441,7 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
     const int64_t i_home = perm ? perm[k] : k;
     if (i_home >= G.n_home) return;  // ghosts: neighbours only
     const float4 pi = B.b[0].pos[k];
+    const float h_i = B.b[0].h[k];
     const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell,
                 fz = (pi.z - G.loz) * G.inv_cell;
     const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
@@ -440,11 +449,11 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
     const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
     const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
     const float4 vi = B.b[0].vel[k];
-    const float pfi = B.b[0].pf[k];
-    const float rc = (pi.w + hmax) * G.inv_cell * 1.00001f;
+    const float pfi = vi.w;
+    const float rc = (h_i + hmax) * G.inv_cell * 1.00001f;
     const float rc2 = rc * rc;
-    const float hh_i = 0.5f * pi.w;
-    const float inv_hu = rcp_approx(fmaf(0.5f, pi.w, hh_i));  // UNI: 1/h_ij for every candidate
+    const float hh_i = 0.5f * h_i;
+    const float inv_hu = rcp_approx(fmaf(0.5f, h_i, hh_i));  // UNI: 1/h_ij for every candidate
     const float ih4u = (inv_hu * inv_hu) * (inv_hu * inv_hu);
     const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
     const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
@@ -458,11 +467,11 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
         if (g == B.nb) continue;  // layer held by no block
         const float4* __restrict__ pos = B.b[g].pos;
         const float4* __restrict__ vel = B.b[g].vel;
-        const float* __restrict__ pf = B.b[g].pf;
+        const float* __restrict__ hs = B.b[g].h;
         const int32_t* __restrict__ cell_start = B.b[g].cs;
         auto pair = [&](int j) {
-            const float4 pj = pos[j];
-            const float4 vj = vel[j];
+            const float4 pj = pos[j];  // (x, y, z, m)
+            const float4 vj = vel[j];  // (v, P/rho^2)
             const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
             const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
             const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
@@ -470,7 +479,7 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
             if constexpr (UNI) {
                 inv_h = inv_hu, ih4 = ih4u;
             } else {
-                inv_h = rcp_approx(fmaf(0.5f, pj.w, hh_i));
+                inv_h = rcp_approx(fmaf(0.5f, __ldg(hs + j), hh_i));
                 const float ih2 = inv_h * inv_h;
                 ih4 = ih2 * ih2;
             }
@@ -478,12 +487,13 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
             const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
             const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
             const float sc = dw * ih4 * inv_r;                    // pi dW/dr / r
-            const float f = vj.w * (pfi + __ldg(pf + j)) * sc;
+            const float msc = pj.w * sc;
+            const float f = msc * (pfi + vj.w);
             ax = fmaf(f, dx, ax);
             ay = fmaf(f, dy, ay);
             az = fmaf(f, dz, az);
             const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
-            cp = fmaf(vj.w * sc, dvx, cp);
+            cp = fmaf(msc, dvx, cp);
         };
         const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
                                 0.0f);
@@ -542,17 +552,16 @@ static void launch_force(const ForceBlockSet& B, const int32_t* perm, const Cell
     else k_force_c<4, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
 }
 
-// (v, m) and P/rho^2 of a packed block, in its cell-sorted order; rho == 0 sets *zero
+// (v, P/rho^2) of a packed block, in its cell-sorted order; rho == 0 sets *zero
 template <int P>
-__global__ void k_pack_vel(const void* __restrict__ v, const void* __restrict__ m, const void* __restrict__ rho,
-                           const void* __restrict__ pr, const int32_t* __restrict__ perm, uint64_t n,
-                           float4* __restrict__ vel, float* __restrict__ pf, unsigned* __restrict__ zero) {
+__global__ void k_pack_vel(const void* __restrict__ v, const void* __restrict__ rho, const void* __restrict__ pr,
+                           const int32_t* __restrict__ perm, uint64_t n, float4* __restrict__ vel,
+                           unsigned* __restrict__ zero) {
     bool z = false;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = perm ? uint64_t(perm[k]) : k;
         const float ri = ldf<P>(rho, i);
-        vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(m, i));
-        pf[k] = ldf<P>(pr, i) / (ri * ri);
+        vel[k] = make_float4(ldf<P>(v, 3 * i), ldf<P>(v, 3 * i + 1), ldf<P>(v, 3 * i + 2), ldf<P>(pr, i) / (ri * ri));
         z |= ri == 0.0f;
     }
     if (__any_sync(0xffffffffu, z) && (threadIdx.x & 31) == 0) atomicOr(zero, 1u);
@@ -570,39 +579,39 @@ void force_cells(const void* x, const void* v, const void* m, const void* h, con
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
     if (sp < 0) throw std::invalid_argument("force_cells precision must be SF_PREC_NATIVE (fp32), 16 or SF_PREC_BF16");
     float4 *pos = nullptr, *vel = nullptr;
-    float* pf = nullptr;
+    float* hs = nullptr;
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pos), 32 * n, st), "cudaMallocAsync");
-    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pf), 4 * n + 16, st), "cudaMallocAsync");
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&hs), 4 * n + 16, st), "cudaMallocAsync");
     vel = pos + n;
-    unsigned* words = reinterpret_cast<unsigned*>(pf + n);  // [0], [1] h range (h_range), [2] rho == 0 flag
+    unsigned* words = reinterpret_cast<unsigned*>(hs + n);  // [0], [1] h range (h_range), [2] rho == 0 flag
     check_cuda(cudaMemsetAsync(words, 0, 3 * sizeof(unsigned), st), "memset");
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    if (sp == SP_F32) k_pack_force<SP_F32><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 2);
-    else if (sp == SP_F16) k_pack_force<SP_F16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 2);
-    else k_pack_force<SP_BF16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, pf, words, words + 2);
+    if (sp == SP_F32) k_pack_force<SP_F32><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, hs, words, words + 2);
+    else if (sp == SP_F16) k_pack_force<SP_F16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, hs, words, words + 2);
+    else k_pack_force<SP_BF16><<<blocks, 256, 0, st>>>(x, v, m, h, rho, pr, perm, n, pos, vel, hs, words, words + 2);
     unsigned flag = 0;
     check_cuda(cudaMemcpyAsync(&flag, words + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
     check_cuda(cudaStreamSynchronize(st), "sync");
     if (flag) {
         cudaFreeAsync(pos, st);
-        cudaFreeAsync(pf, st);
+        cudaFreeAsync(hs, st);
         throw std::domain_error("force: degenerate state, rho == 0");
     }
     CellGrid G{lo[0], lo[1], lo[2], 1.0f / cell, nx, ny, nz, reach, int64_t(n_home)};
     ForceBlockSet B{};
-    B.b[0] = ForceBlock{pos, vel, pf, cell_start, words, 0, nx, lo[0]};
+    B.b[0] = ForceBlock{pos, vel, hs, cell_start, words, 0, nx, lo[0]};
     B.nb = 1;
     B.NX = nx;
     launch_force(B, perm, G, int64_t(n), reach, a, du, st);
     check_cuda(cudaGetLastError(), "force_cells launch");
     count_launches(2);
     check_cuda(cudaFreeAsync(pos, st), "cudaFreeAsync");
-    check_cuda(cudaFreeAsync(pf, st), "cudaFreeAsync");
+    check_cuda(cudaFreeAsync(hs, st), "cudaFreeAsync");
 }
 
 // (v, m) and P/rho^2 into a block, stream-ordered: rho == 0 anywhere sets *zero (no host sync)
-void force_pack_async(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
-                      const int32_t* perm, void* vel, float* pf, unsigned* zero, cudaStream_t st) {
+void force_pack_async(const void* v, const void* rho, const void* pr, int prec, uint64_t n, const int32_t* perm,
+                      void* vel, unsigned* zero, cudaStream_t st) {
     require_device();
     if (n >= (1ull << 31)) throw std::invalid_argument("force_pack: n must be < 2^31 per device");
     const int sp = (prec == 1 || prec == 32) ? SP_F32 : prec == 16 ? SP_F16 : prec == 100 ? SP_BF16 : -1;
@@ -611,21 +620,21 @@ void force_pack_async(const void* v, const void* m, const void* rho, const void*
     if (reinterpret_cast<uintptr_t>(vel) & 15) throw std::invalid_argument("vel must be 16-byte aligned");
     float4* v4 = static_cast<float4*>(vel);
     const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
-    if (sp == SP_F32) k_pack_vel<SP_F32><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
-    else if (sp == SP_F16) k_pack_vel<SP_F16><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
-    else k_pack_vel<SP_BF16><<<blocks, 256, 0, st>>>(v, m, rho, pr, perm, n, v4, pf, zero);
+    if (sp == SP_F32) k_pack_vel<SP_F32><<<blocks, 256, 0, st>>>(v, rho, pr, perm, n, v4, zero);
+    else if (sp == SP_F16) k_pack_vel<SP_F16><<<blocks, 256, 0, st>>>(v, rho, pr, perm, n, v4, zero);
+    else k_pack_vel<SP_BF16><<<blocks, 256, 0, st>>>(v, rho, pr, perm, n, v4, zero);
     check_cuda(cudaGetLastError(), "force_pack launch");
     count_launches(1);
 }
 
-void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
-                const int32_t* perm, void* vel, float* pf, cudaStream_t st) {
+void force_pack(const void* v, const void* rho, const void* pr, int prec, uint64_t n, const int32_t* perm, void* vel,
+                cudaStream_t st) {
     require_device();
     if (n == 0) return;
     unsigned* zero = nullptr;
     check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&zero), sizeof(unsigned), st), "cudaMallocAsync");
     check_cuda(cudaMemsetAsync(zero, 0, sizeof(unsigned), st), "memset");
-    force_pack_async(v, m, rho, pr, prec, n, perm, vel, pf, zero, st);
+    force_pack_async(v, rho, pr, prec, n, perm, vel, zero, st);
     unsigned flag = 0;
     check_cuda(cudaMemcpyAsync(&flag, zero, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
     check_cuda(cudaFreeAsync(zero, st), "cudaFreeAsync");
@@ -645,10 +654,10 @@ void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const 
     B.NX = NX;
     for (int g = 0; g < nb; ++g) {
         const ForceBlockDesc& d = blocks[g];
-        if (!d.pos || !d.vel || !d.pf || !d.cell_start || !d.hmax) throw std::invalid_argument("null block pointer");
+        if (!d.pos || !d.vel || !d.h || !d.cell_start || !d.hmax) throw std::invalid_argument("null block pointer");
         if (d.nx <= 0 || d.x0 < 0 || d.x0 + d.nx > NX || int64_t(d.nx) * ny * nz >= (1ll << 31))
             throw std::invalid_argument("block layers outside the grid");
-        B.b[g] = ForceBlock{static_cast<const float4*>(d.pos), static_cast<const float4*>(d.vel), d.pf, d.cell_start,
+        B.b[g] = ForceBlock{static_cast<const float4*>(d.pos), static_cast<const float4*>(d.vel), d.h, d.cell_start,
                             d.hmax, d.x0, d.nx, d.x_origin};
     }
     if (n == 0) return;

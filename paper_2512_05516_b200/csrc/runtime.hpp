@@ -49,8 +49,8 @@ void density_cells(const void* x, const void* m, const void* h, int prec, uint64
                    uint64_t n_home, float* rho, cudaStream_t st);
 // one block of the multi-block density (sf_cell_block)
 struct CellBlockDesc {
-    const void* pos;
-    const float* mass;
+    const void* pos;   // float4 (x, y, z, m)
+    const float* h;
     const int32_t* cell_start;
     const unsigned* hmax;
     int32_t x0, nx;
@@ -58,24 +58,24 @@ struct CellBlockDesc {
     int32_t reserved;
 };
 void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm, void* pos,
-                float* mass, unsigned* hmax, cudaStream_t st);
+                float* hs, unsigned* hmax, cudaStream_t st);
 void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                           const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* rho,
                           cudaStream_t st);
 struct ForceBlockDesc {
-    const void* pos;
-    const void* vel;
-    const float* pf;
+    const void* pos;   // float4 (x, y, z, m): the density block's
+    const void* vel;   // float4 (vx, vy, vz, P/rho^2)
+    const float* h;
     const int32_t* cell_start;
     const unsigned* hmax;
     int32_t x0, nx;
     float x_origin;
     int32_t reserved;
 };
-void force_pack_async(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
-                      const int32_t* perm, void* vel, float* pf, unsigned* zero, cudaStream_t st);
-void force_pack(const void* v, const void* m, const void* rho, const void* pr, int prec, uint64_t n,
-                const int32_t* perm, void* vel, float* pf, cudaStream_t st);
+void force_pack_async(const void* v, const void* rho, const void* pr, int prec, uint64_t n, const int32_t* perm,
+                      void* vel, unsigned* zero, cudaStream_t st);
+void force_pack(const void* v, const void* rho, const void* pr, int prec, uint64_t n, const int32_t* perm, void* vel,
+                cudaStream_t st);
 void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                         const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* a, float* du,
                         cudaStream_t st);

@@ -7,8 +7,8 @@
 // map through CUDA IPC (same node: NVLink / NVSwitch peers, or processes
 // sharing a GPU):
 //
-//   [header | epochs | cell_start | pos (x,y,z,h) | mass | h range |
-//    vel (v, m) | P/rho^2 | outbox to the left | outbox to the right]
+//   [header | epochs | cell_start | pos (x,y,z,m) | h | h range |
+//    vel (v, P/rho^2) | outbox to the left | outbox to the right]
 //
 // * Halo: the density and force kernels read the neighbours' packed cell
 //   blocks in place through the peer pointers (no ghost copy, no send/recv).
@@ -72,17 +72,16 @@ static_assert(sizeof(Header) == 192, "header layout");
 uint64_t al256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
 
 struct ShardLayout {
-    uint64_t cs, pos, mass, hmax, vel, pf, out[2], total;
+    uint64_t cs, pos, h, hmax, vel, out[2], total;
 };
 ShardLayout layout_of(uint64_t ncell, uint64_t cap, uint64_t cap_m) {
     ShardLayout L{};
     L.cs = 256;
     L.pos = al256(L.cs + 4 * (ncell + 1));
-    L.mass = al256(L.pos + 16 * cap);
-    L.hmax = al256(L.mass + 4 * cap);
+    L.h = al256(L.pos + 16 * cap);
+    L.hmax = al256(L.h + 4 * cap);
     L.vel = al256(L.hmax + 16);
-    L.pf = al256(L.vel + 16 * cap);
-    L.out[0] = al256(L.pf + 4 * cap);
+    L.out[0] = al256(L.vel + 16 * cap);
     L.out[1] = al256(L.out[0] + 16 + uint64_t(kRowBytes) * cap_m);
     L.total = al256(L.out[1] + 16 + uint64_t(kRowBytes) * cap_m);
     return L;
@@ -390,13 +389,13 @@ void wait_peers(Shard* S, int e, uint64_t value, cudaStream_t st) {
 }
 
 CellBlockDesc density_block(const uint8_t* base, const ShardLayout& L, int x0, int nx, float x_origin) {
-    return CellBlockDesc{base + L.pos, reinterpret_cast<const float*>(base + L.mass),
+    return CellBlockDesc{base + L.pos, reinterpret_cast<const float*>(base + L.h),
                          reinterpret_cast<const int32_t*>(base + L.cs), reinterpret_cast<const unsigned*>(base + L.hmax),
                          x0, nx, x_origin, 0};
 }
 
 ForceBlockDesc force_block(const uint8_t* base, const ShardLayout& L, int x0, int nx, float x_origin) {
-    return ForceBlockDesc{base + L.pos, base + L.vel, reinterpret_cast<const float*>(base + L.pf),
+    return ForceBlockDesc{base + L.pos, base + L.vel, reinterpret_cast<const float*>(base + L.h),
                           reinterpret_cast<const int32_t*>(base + L.cs),
                           reinterpret_cast<const unsigned*>(base + L.hmax), x0, nx, x_origin, 0};
 }
@@ -431,7 +430,7 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
         bin_particles(x, S->n, lo, S->fine, S->fnx, S->NF, S->NF, reinterpret_cast<int32_t*>(base + S->L.cs), perm,
                       S->scratch->p, S->bin_bytes, st);
         cells_pack(x, S->field(c, F_M), S->field(c, F_H), 1, S->n, perm, base + S->L.pos,
-                   reinterpret_cast<float*>(base + S->L.mass), reinterpret_cast<unsigned*>(base + S->L.hmax), st);
+                   reinterpret_cast<float*>(base + S->L.h), reinterpret_cast<unsigned*>(base + S->L.hmax), st);
         signal(S, E_PACKED, st);
         wait_peers(S, E_PACKED, s, st);
         binned = true;
@@ -464,10 +463,10 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
             density_cells_blocks(dblocks.data(), int(dblocks.size()), S->n, perm, S->n, lo_yz, S->fine, S->NF, S->NF,
                                  S->NF, S->refine, reinterpret_cast<float*>(S->field(c, F_RHO)), st);
         } else if (k == "force") {
-            // the neighbours finished reading this block's (v, m, P/rho^2) in the previous step (E_READ_DONE,
+            // the neighbours finished reading this block's (v, P/rho^2) in the previous step (E_READ_DONE,
             // waited in bin_and_pack); rho == 0 -> *rho_zero, checked at the end of the step
-            force_pack_async(S->field(c, F_V), S->field(c, F_M), S->field(c, F_RHO), S->field(c, F_P), 1, S->n, perm,
-                             base + S->L.vel, reinterpret_cast<float*>(base + S->L.pf), rho_zero, st);
+            force_pack_async(S->field(c, F_V), S->field(c, F_RHO), S->field(c, F_P), 1, S->n, perm, base + S->L.vel,
+                             rho_zero, st);
             signal(S, E_PACKED_FORCE, st);
             wait_peers(S, E_PACKED_FORCE, s, st);
             force_cells_blocks(fblocks.data(), int(fblocks.size()), S->n, perm, S->n, lo_yz, S->fine, S->NF, S->NF,

@@ -253,7 +253,7 @@ def test_block_and_ipc_entry_points_fail_loudly_without_device():
     lo = (C.c_float * 2)(0, 0)
     arr = (L.SfCellBlock * 1)(blk)
     assert lib.sf_b200_density_cells_blocks(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 1, p(f), None) == L.SF_ERROR
-    assert lib.sf_b200_force_pack(p(f), p(f), p(f), p(f), 1, n, p(i32), p(f), p(f), None) == L.SF_ERROR
+    assert lib.sf_b200_force_pack(p(f), p(f), p(f), 1, n, p(i32), p(f), None) == L.SF_ERROR
     out = C.c_void_p()
     assert lib.sf_b200_dev_alloc(1024, C.byref(out)) == L.SF_ERROR
     assert "no CUDA device" in lib.sf_last_error().decode()
