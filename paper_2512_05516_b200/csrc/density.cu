@@ -275,7 +275,7 @@ __device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __r
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+__global__ void __launch_bounds__(256, 5) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
                                                  int64_t n, float* __restrict__ rho) {
     float hmax;
     const bool uni = uniform_h(B, &hmax);
