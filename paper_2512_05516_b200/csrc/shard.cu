@@ -94,7 +94,19 @@ __global__ void k_signal(uint64_t* epoch, uint64_t value) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(epoch), "l"(value) : "memory");
 }
 
-__global__ void k_wait_epochs(const uint64_t* a, const uint64_t* b, uint64_t value) {
+// One thread spins (acquire, system scope) until both neighbours' epoch words
+// reach `value`.  Bounded: after kWaitNs without progress it raises *timeout
+// and returns, so a neighbour that failed (or never started the step) turns
+// into an SF_ERROR at this step's end instead of a hung stream.
+constexpr uint64_t kWaitNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_wait_epochs(const uint64_t* a, const uint64_t* b, uint64_t value, int* timeout) {
+    const uint64_t t0 = global_ns();
     for (const uint64_t* p : {a, b}) {
         if (!p) continue;
         uint64_t v = 0;
@@ -102,6 +114,10 @@ __global__ void k_wait_epochs(const uint64_t* a, const uint64_t* b, uint64_t val
         for (;;) {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
             if (v >= value) break;
+            if (global_ns() - t0 > kWaitNs) {
+                atomicOr(timeout, 4);
+                return;
+            }
             __nanosleep(ns);
             ns = ns < 4096 ? ns * 2 : ns;
         }
@@ -384,7 +400,7 @@ void signal(Shard* S, int e, cudaStream_t st) {
 
 void wait_peers(Shard* S, int e, uint64_t value, cudaStream_t st) {
     if (S->world == 1 || value == 0) return;
-    k_wait_epochs<<<1, 1, 0, st>>>(S->peer_epoch(0, e), S->peer_epoch(1, e), value);
+    k_wait_epochs<<<1, 1, 0, st>>>(S->peer_epoch(0, e), S->peer_epoch(1, e), value, S->misc->as<int>(16));
     count_launches(1);
 }
 
@@ -541,6 +557,9 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
         check_cuda(cudaStreamSynchronize(st), "sync");  // the one host synchronisation of the step
         if (flags[0]) {
             check_cuda(cudaMemset(overflow, 0, 4), "memset");
+            if (flags[0] & 4)
+                throw std::runtime_error("shard_step: a neighbour did not reach this step within 20 s "
+                                         "(failed or not stepping); the shard's state is undefined");
             throw std::runtime_error("shard_step: migration overflowed the outbox or the shard capacity");
         }
         if (flags[1] && force_ran) {

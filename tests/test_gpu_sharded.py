@@ -378,7 +378,8 @@ def test_bench_under_torchrun_two_ranks_one_device(workload, tmp_path):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    extra = ["--no-e2e", "--no-cpu", "--no-extras"] if workload == "c2" else \
+    # c2 with extras: at 2 ranks the only extra is the sharded C5 timestep (small here), in the same line
+    extra = ["--no-e2e", "--no-cpu", "--c5-n", str(1 << 20)] if workload == "c2" else \
         ["--workload", "c5", "--c5-n", str(1 << 20), "--no-cpu"]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(29600 + (workload == "c5")), os.path.join(root, "bench.py"), "--gpus", "2",
@@ -390,3 +391,8 @@ def test_bench_under_torchrun_two_ranks_one_device(workload, tmp_path):
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    if workload == "c2":
+        c5 = d["sharded_c5"]
+        assert "unavailable" not in c5, c5
+        assert c5["n_gpus"] == 2 and c5["value"] > 0 and c5["particles_total"] == 1 << 20
+        assert c5["phases_ms_max_over_ranks"]["force"] > 0
