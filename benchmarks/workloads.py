@@ -3,7 +3,7 @@
   c1  kick / drift on 1M particles, AoS full-precision storage, in place
       (92 MB < L2: L2 flushed between timed launches, each launch timed alone)
   c3  SPH density, cell-linked, 4M uniform particles, SoA fp32 vs fp16 vs bf16
-  c4  64M host-resident particles: streamed (narrowed 2-D DMA) vs managed vs
+  c4  64M host-resident particles: streamed (zero copy, narrowed lanes) vs managed vs
       in-place (whole records), one drift and one kick+drift step each
   c5  128M particles, density + kick/drift sharded by cell (peer-block halo)
 

@@ -269,11 +269,12 @@ SF_API uint64_t sf_b200_bin_scratch_bytes(uint64_t n, int nx, int ny, int nz);
  * records of `src` (full field set, AoS).  One step = gather + `kernels`
  * (comma list of kick,drift) in the dst view's precision + scatter-back of
  * every write set into the AoS, for every record.
- *   mode 0 STREAMED: pinned host memory; per chunk only the contiguous field
- *                    span the kernels touch crosses PCIe (one 2-D DMA, pitch =
- *                    record) — the reference's narrowed streaming transfers;
- *   mode 1 MANAGED:  host_aos is cudaMallocManaged; prefetch/advise hints and
- *                    in-place conversion on the migrated pages;
+ *   mode 0 STREAMED: pinned host memory, zero copy: the gather reads only the
+ *                    SoA view's lanes of the host records over PCIe and the
+ *                    scatter-back stores only the write set's lanes into them
+ *                    (the reference's narrowed streaming transfers);
+ *   mode 1 MANAGED:  host_aos is cudaMallocManaged; prefetch to the GPU, kernels
+ *                    on the migrated pages, prefetch back (no placement hints);
  *   mode 2 INPLACE:  pinned host memory, whole records each way (the
  *                    reference's in-place round trip).
  *   mode 3 MANAGED_MAPPED: managed memory kept on the host and never

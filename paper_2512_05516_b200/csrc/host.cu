@@ -3,12 +3,14 @@
 // PCIe-attached B200.  Three modes, all chunked over 3 rotating streams so
 // the two copy engines and the SMs overlap (H2D k+1 ∥ compute k ∥ D2H k-1):
 //
-//   STREAMED (0) pinned host AoS; per chunk only the contiguous field span
-//                the kernels touch crosses PCIe, as one 2-D DMA (pitch =
-//                record, width = span): the reference's run_dev_streaming
-//                ships narrowed records (streamed_bytes_one_way,
-//                pipelines.cpp:434-441) — here the narrowing is the DMA's
-//                own stride, no host-side gather.
+//   STREAMED (0) pinned host AoS, zero copy: the gather kernel reads only
+//                the fields of the SoA view straight from the host records
+//                over PCIe (per-lane typed loads of the mapped pinned
+//                memory, no whole-record tiles) and the scatter-back writes
+//                only the write set's lanes into them — the reference's
+//                run_dev_streaming ships just the narrowed records
+//                (streamed_bytes_one_way, pipelines.cpp:434-441).  (Round 1
+//                narrowed with 2-D DMA rows of the field span: 2.3 GB/s.)
 //   MANAGED  (1) cudaMallocManaged AoS, no placement hints; per chunk
 //                cudaMemPrefetchAsync to the GPU, kernels run in place on the
 //                migrated pages, prefetch back.
@@ -55,18 +57,6 @@ View with_count(const View& v, uint64_t count) {
     return c;
 }
 
-// AoS view over the contiguous run of fields [lo, hi] (declaration order).
-View span_view(const View& full, int lo, int hi) {
-    View v = full;
-    v.subset.clear();
-    v.fmt.clear();
-    for (int f = lo; f <= hi; ++f) {
-        v.subset.push_back(f);
-        v.fmt.push_back(full.fmt[full.pos_of(f)]);
-    }
-    return v;
-}
-
 }  // namespace
 
 void run_host(const View& src, void* host, const View& dst, const std::string& kernels, double dt, int math, int mode,
@@ -86,20 +76,24 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
     const uint64_t n = src.count;
     const uint64_t rb = src.record_bits();
 
-    // the contiguous span of fields the kernels (and the SoA view) touch
-    int lo = int(src.schema->fields.size()), hi = -1;
-    for (int f : dst.subset) lo = std::min(lo, f), hi = std::max(hi, f);
-    for (const auto& k : ks) {
-        const KernelSet* set = src.schema->kernel(k);
-        if (!set) throw std::invalid_argument("no access set declared for kernel '" + k + "'");
-        for (size_t f = 0; f < src.schema->fields.size(); ++f)
-            if (set->touches(src.schema->fields[f].name)) lo = std::min(lo, int(f)), hi = std::max(hi, int(f));
+    for (const auto& k : ks)
+        if (!src.schema->kernel(k)) throw std::invalid_argument("no access set declared for kernel '" + k + "'");
+    const View& dev_view = src;  // layout of the AoS chunk the kernels address (device slot, or the host records)
+    if (mode == 0 && (!src.byte_aligned() || (rb & 7)))
+        throw std::invalid_argument("streamed mode needs byte-aligned lanes (use INPLACE for bit-packed AoS)");
+    // streamed: the bytes the kernels touch per record, both ways (stored widths)
+    uint64_t read_bits = 0, write_bits = 0;
+    for (size_t f = 0; f < src.schema->fields.size(); ++f) {
+        const FieldDecl& d = src.schema->fields[f];
+        const uint64_t w = uint64_t(d.arity) * src.width(src.pos_of(int(f)));
+        bool rd = std::find(dst.subset.begin(), dst.subset.end(), int(f)) != dst.subset.end(), wr = false;
+        for (const auto& k : ks) {
+            const KernelSet* set = src.schema->kernel(k);
+            wr |= std::find(set->writes.begin(), set->writes.end(), d.name) != set->writes.end();
+        }
+        read_bits += rd ? w : 0;
+        write_bits += wr ? w : 0;
     }
-    const View dev_view = mode == 0 ? span_view(src, lo, hi) : src;  // layout of the device-side AoS chunk
-    const uint64_t span_off_bits = src.lane_base(lo);
-    const uint64_t span_bits = dev_view.record_bits();
-    if (mode == 0 && ((span_off_bits | span_bits | rb) & 7))
-        throw std::invalid_argument("streamed mode needs a byte-aligned field span (use INPLACE for bit-packed AoS)");
 
     cudaPointerAttributes attr{};
     check_cuda(cudaPointerGetAttributes(&attr, host), "pointer attributes");
@@ -163,7 +157,6 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
 
     uint64_t h2d = 0, d2h = 0, nchunks = 0;
     const uint64_t launches0 = launch_count();
-    const size_t rbytes = size_t(rb / 8), sbytes = size_t(span_bits / 8), soff = size_t(span_off_bits / 8);
     for (uint64_t r0 = 0; r0 < n; r0 += chunk, ++nchunks) {
         const int s = int(nchunks % slots);
         cudaStream_t st = pool->streams[s];
@@ -171,11 +164,10 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
         const size_t off = size_t(r0 * rb / 8);
         const size_t bytes = size_t((cnt * rb + 7) / 8);
         uint8_t* hchunk = static_cast<uint8_t*>(host) + off;
-        void* aos = managed ? static_cast<void*>(hchunk) : pool->aos[s];
+        void* aos = (managed || mode == 0) ? static_cast<void*>(hchunk) : pool->aos[s];
+        const bool zero_copy = mode == 0;
         if (mode == 0) {
-            check_cuda(cudaMemcpy2DAsync(aos, sbytes, hchunk + soff, rbytes, sbytes, cnt, cudaMemcpyHostToDevice, st),
-                       "H2D 2D");
-            h2d += sbytes * cnt;
+            h2d += read_bits * cnt / 8;  // the kernels read these lanes in place over PCIe
         } else if (mode == 2) {
             check_cuda(cudaMemcpyAsync(aos, hchunk, bytes, cudaMemcpyHostToDevice, st), "H2D");
             h2d += bytes;
@@ -186,7 +178,7 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
             h2d += bytes;  // MANAGED_MAPPED: no migration, the kernels read the host pages over PCIe
         }
         const View sv = with_count(dev_view, cnt), dv = with_count(dst, cnt);
-        gather(sv, aos, dv, pool->soa[s], ks[0].c_str(), dt, math, st);
+        gather(sv, aos, dv, pool->soa[s], ks[0].c_str(), dt, math, st, zero_copy);
         for (size_t k = 1; k < ks.size(); ++k) run_kernel(dv, pool->soa[s], ks[k], dt, 1, 0, math, st);
         if (host_soa) {
             // SoA result straight to host: one D2H per stream of the chunk
@@ -201,11 +193,9 @@ void run_host(const View& src, void* host, const View& dst, const std::string& k
             }
             if (mode == 1) check_cuda(cudaMemPrefetchAsync(hchunk, bytes, cudaCpuDeviceId, st), "prefetch");
         } else {
-            for (const auto& k : ks) scatter_merge(dv, pool->soa[s], sv, aos, k, st);
+            for (const auto& k : ks) scatter_merge(dv, pool->soa[s], sv, aos, k, st, zero_copy);
             if (mode == 0) {
-                check_cuda(cudaMemcpy2DAsync(hchunk + soff, rbytes, aos, sbytes, sbytes, cnt, cudaMemcpyDeviceToHost, st),
-                           "D2H 2D");
-                d2h += sbytes * cnt;
+                d2h += write_bits * cnt / 8;  // the write set's lanes, stored in place over PCIe
             } else if (mode == 2) {
                 check_cuda(cudaMemcpyAsync(hchunk, aos, bytes, cudaMemcpyDeviceToHost, st), "D2H");
                 d2h += bytes;

@@ -433,10 +433,11 @@ static void launch_convert_ieee_t(const CStream& c, uint64_t n, const uint8_t* s
 
 template <int SB>
 static void launch_convert_ieee_s(const CStream& c, uint64_t n, const uint8_t* src, uint8_t* dst, cudaStream_t st,
-                                  int blocks) {
-    // sector read-patch-write for 8-B lanes in wide records (neighbouring records' sectors disjoint)
+                                  int blocks, bool zero_copy) {
+    // sector read-patch-write for 8-B lanes in wide records (neighbouring records' sectors disjoint); not for
+    // a zero-copy destination in host memory, where it would read every written sector back over PCIe
     const uint64_t span = uint64_t(c.dst.arity) * 8;
-    if (ieee_code(c.dst.fmt) == B_F64 && c.dst.arity <= 3 && c.dst.stride / 8 >= span + 64 &&
+    if (!zero_copy && ieee_code(c.dst.fmt) == B_F64 && c.dst.arity <= 3 && c.dst.stride / 8 >= span + 64 &&
         (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
         const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
         if (c.dst.arity == 3)
@@ -1358,10 +1359,11 @@ __global__ void k_force_buffer(const __grid_constant__ ForcePlan P, uint8_t* buf
 
 // ----------------------------------------------------------------- launchers
 
-cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st) {
+cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st, bool zero_copy) {
     if (p.count == 0 || p.n == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
-    if (launch_scatter_tile(p, src, dst, st, &err)) return err;  // into AoS records: one staged pass
+    // into AoS records: one staged pass (it reads the whole records: not for a zero-copy host destination)
+    if (!zero_copy && launch_scatter_tile(p, src, dst, st, &err)) return err;
     bool typed = true;
     for (uint32_t i = 0; i < p.n && typed; ++i) typed = convert_ieee_ok(p.s[i], src, dst);
     if (typed && src != dst) {  // per stream; in place (src == dst) keeps the one-pass generic kernel
@@ -1372,10 +1374,10 @@ cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cud
             const uint8_t* s8 = static_cast<const uint8_t*>(src);
             uint8_t* d8 = static_cast<uint8_t*>(dst);
             switch (ieee_code(c.src.fmt)) {
-                case B_F16: launch_convert_ieee_s<B_F16>(c, p.count, s8, d8, st, blocks); break;
-                case B_BF16: launch_convert_ieee_s<B_BF16>(c, p.count, s8, d8, st, blocks); break;
-                case B_F32: launch_convert_ieee_s<B_F32>(c, p.count, s8, d8, st, blocks); break;
-                default: launch_convert_ieee_s<B_F64>(c, p.count, s8, d8, st, blocks); break;
+                case B_F16: launch_convert_ieee_s<B_F16>(c, p.count, s8, d8, st, blocks, zero_copy); break;
+                case B_BF16: launch_convert_ieee_s<B_BF16>(c, p.count, s8, d8, st, blocks, zero_copy); break;
+                case B_F32: launch_convert_ieee_s<B_F32>(c, p.count, s8, d8, st, blocks, zero_copy); break;
+                default: launch_convert_ieee_s<B_F64>(c, p.count, s8, d8, st, blocks, zero_copy); break;
             }
         }
         count_launches(p.n - 1);  // the caller counts one
@@ -1393,7 +1395,7 @@ static size_t gather_warp_bytes(const GatherPlan& p) {
 
 
 cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
-                          int /*ctas_per_sm*/) {
+                          bool zero_copy) {
     if (plan.count == 0 || plan.n == 0) return cudaSuccess;
     GatherPlan p = plan;
     p.stages = uint8_t(kWStages);
@@ -1414,7 +1416,9 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
         return cudaGetLastError();
     };
     const bool xv_plan = p.proc == PROC_XV_F16 || p.proc == PROC_XV_BF16 || p.proc == PROC_XV_F32;
-    if (xv_plan && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+    // zero_copy (source in pinned host memory, read over PCIe): no whole-record tile copies, per-lane typed
+    // loads of just the plan's fields (k_gather_multi<direct>)
+    if (!zero_copy && xv_plan && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(dst) & 7) == 0 && p.record_bits / 8 <= kRecTileMaxStride) {
         const size_t xsm = 128 + 256 * size_t(p.record_bits / 8);
         const unsigned g = unsigned((p.count + 255) / 256);
@@ -1439,7 +1443,8 @@ cudaError_t launch_gather(const GatherPlan& plan, const void* src, uint64_t src_
             // one thread per record, uncapped grid: CTAs in flight cover one compact record range
             const int mb = int((p.count + 255) / 256);
             const size_t rbytes = p.record_bits / 8, smem = 128 + 256 * rbytes;
-            if (p.record_bits % 8 == 0 && rbytes <= kRecTileMaxStride && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            if (!zero_copy && p.record_bits % 8 == 0 && rbytes <= kRecTileMaxStride &&
+                (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
                 cudaError_t e = cudaFuncSetAttribute(k_gather_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      int(smem));
                 if (e != cudaSuccess) return e;

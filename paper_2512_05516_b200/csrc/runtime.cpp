@@ -75,7 +75,7 @@ static void fuse_ops(ConvertPlan& p, const View& src, const View& dst, const std
 }
 
 void gather(const View& src, const void* sp, const View& dst, void* dp, const char* kernel, double dt, int math,
-            cudaStream_t st) {
+            cudaStream_t st, bool zero_copy) {
     require_device();
     check_ptr(sp, "source buffer");
     check_ptr(dp, "destination buffer");
@@ -85,13 +85,13 @@ void gather(const View& src, const void* sp, const View& dst, void* dp, const ch
                 dst.lane_base(int(q)) % 8 == 0;
     if (tiled) {
         const GatherPlan g = kernel ? plan_gather_fused(src, dst, kernel, dt, math) : plan_gather(src, dst);
-        check_cuda(launch_gather(g, sp, src.total_bytes(), dp, st, 0), "gather launch");
+        check_cuda(launch_gather(g, sp, src.total_bytes(), dp, st, zero_copy), "gather launch");
         count_launches(1);
         return;
     }
     ConvertPlan p = plan_convert(src, dst, dst.subset);
     if (kernel) fuse_ops(p, src, dst, kernel, dt, math);
-    check_cuda(launch_convert(p, sp, dp, st), "convert launch");
+    check_cuda(launch_convert(p, sp, dp, st, zero_copy), "convert launch");
     count_launches(1);
 }
 
@@ -100,7 +100,7 @@ void convert(const View& src, const void* sp, const View& dst, void* dp, cudaStr
 }
 
 void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, const std::string& kernel,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool zero_copy) {
     require_device();
     check_ptr(sp, "source buffer");
     check_ptr(dp, "destination buffer");
@@ -113,7 +113,7 @@ void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, c
         fields.push_back(f);
     }
     const ConvertPlan p = plan_convert(src, dst, fields);
-    check_cuda(launch_convert(p, sp, dp, st), "scatter launch");
+    check_cuda(launch_convert(p, sp, dp, st, zero_copy), "scatter launch");
     count_launches(1);
 }
 

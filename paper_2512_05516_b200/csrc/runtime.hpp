@@ -13,9 +13,11 @@
 namespace sfb {
 
 // kernels.cu / density.cu launchers
-cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st);
+// zero_copy: the host-memory side of the conversion is read / written in place over PCIe (pinned memory
+// mapped into the device's address space): only the plan's lanes are touched, never whole records
+cudaError_t launch_convert(const ConvertPlan& p, const void* src, void* dst, cudaStream_t st, bool zero_copy = false);
 cudaError_t launch_gather(const GatherPlan& p, const void* src, uint64_t src_bytes, void* dst, cudaStream_t st,
-                          int ctas_per_sm);
+                          bool zero_copy = false);
 cudaError_t launch_density_buffer(const DensityPlan& p, void* buf, cudaStream_t st);
 cudaError_t launch_update_rec(int xb, int yb, int arity, void* buf, uint64_t n, uint32_t stride, uint32_t xoff,
                               uint32_t yoff, double dt, uint8_t op, uint8_t math, cudaStream_t st);
@@ -36,10 +38,10 @@ void count_launches(uint64_t n);
 uint64_t launch_count();
 
 void gather(const View& src, const void* sp, const View& dst, void* dp, const char* kernel, double dt, int math,
-            cudaStream_t st);
+            cudaStream_t st, bool zero_copy = false);
 void convert(const View& src, const void* sp, const View& dst, void* dp, cudaStream_t st);
 void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, const std::string& kernel,
-                   cudaStream_t st);
+                   cudaStream_t st, bool zero_copy = false);
 void run_kernel(const View& v, void* p, const std::string& kernel, double dt, uint64_t bs, int per_access, int math,
                 cudaStream_t st);
 

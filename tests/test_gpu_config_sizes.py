@@ -230,7 +230,8 @@ def test_c4_64m_run_host_sampled_vs_oracle(mode):
     rows = hb.numpy()[: v.nbytes].reshape(n, 88)[sample].copy()
     dst = api.View(P, n, "soa", None, 16)
     m = api.run_host(v, hb, dst, "kick,drift", 1e-3, chunk=1 << 21, mode=mode)
-    assert m["h2d_bytes"] == v.nbytes == m["d2h_bytes"]
+    assert m["h2d_bytes"] == v.nbytes
+    assert m["d2h_bytes"] == (n * 40 if mode == 0 else v.nbytes)  # streamed: x, v, u written back in place
     # oracle on the sampled records (the step is record-local)
     ob = _oracle_aos(rows.reshape(-1).copy(), k)
     S = ob.schema
