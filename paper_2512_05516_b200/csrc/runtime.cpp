@@ -117,6 +117,16 @@ void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, c
     count_launches(1);
 }
 
+void convert_fields(const View& src, const void* sp, const View& dst, void* dp, const std::vector<int>& fields,
+                    cudaStream_t st, bool zero_copy) {
+    require_device();
+    check_ptr(sp, "source buffer");
+    check_ptr(dp, "destination buffer");
+    const ConvertPlan p = plan_convert(src, dst, fields);
+    check_cuda(launch_convert(p, sp, dp, st, zero_copy), "convert launch");
+    count_launches(1);
+}
+
 namespace {
 // plain IEEE x/y lanes of one op, naturally aligned inside every record
 bool rec_op_ok(const View& v, const CStream& c, const void* p) {

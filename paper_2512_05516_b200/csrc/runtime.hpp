@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "plans.cuh"
 #include "view.hpp"
@@ -44,6 +45,9 @@ void scatter_merge(const View& src, const void* sp, const View& dst, void* dp, c
                    cudaStream_t st, bool zero_copy = false);
 void run_kernel(const View& v, void* p, const std::string& kernel, double dt, uint64_t bs, int per_access, int math,
                 cudaStream_t st);
+// the listed schema fields from src into dst (both views must hold them), nothing else
+void convert_fields(const View& src, const void* sp, const View& dst, void* dp, const std::vector<int>& fields,
+                    cudaStream_t st, bool zero_copy = false);
 
 // density.cu
 void density_cells(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm,
