@@ -669,7 +669,7 @@ def other_arm(args):
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f64" if
                 args.workload in ("c1", "c4") else "f32", "data": "synthetic (uniform random, device RNG)",
-                "config": res["config"], "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": None,
+                "config": res["config"], "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res.get("e2e"),
                 "gpu_launches": launches, "clocks": clocks, "impl": "b200", "workload": args.workload}
         for k in ("kernels", "phases_ms", "particles_local"):
             if k in res:

@@ -93,9 +93,9 @@ def c1(args, peak, peak_kind):
     # rotation set: 6 copies (554 MB > 126 MB L2), so every launch finds its buffer cold
     rot = [api.convert(src, api.View(P, n, "aos", None, api.SF_PREC_NATIVE)) for _ in range(6)]
     flush = L2Flush()
-    kern = {"kick": "k_update_rec_multi (in-place kick, AoS f32 lanes)",
-            "drift": "k_update_rec (in-place drift, AoS f64 x / f32 v)",
-            "kick,drift": "k_update_rec_seq (kick then drift in one pass over the records)"}
+    kern = {"kick": "k_update_rec_tile<128> (in-place kick on the AoS records, TMA-staged)",
+            "drift": "k_update_rec_tile<128> (in-place drift on the AoS records, TMA-staged)",
+            "kick,drift": "k_update_rec_tile<128> (kick then drift in one pass over the records)"}
     out = {}
     # algorithmic bytes: kick reads v,a,u,du (32 B) writes v,u (16 B); drift reads x,v (36 B) writes x (24 B);
     # the one-pass sequence reads x,v,a,u,du (56 B) and writes x,v,u (40 B)
@@ -121,7 +121,23 @@ def c1(args, peak, peak_kind):
         out[k] = {"ms": ms, "ms_flushed_each": ms_f, "ms_rotating_cold": ms_r, "value": n / (ms * 1e-3),
                   "roofline": roofline(bpp, n, ms, peak, peak_kind, kern[k])}
     ms = out["kick,drift"]["ms"]
-    return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": out["kick,drift"]["roofline"],
+    # end to end: the 1M records in pinned host memory, whole records H2D, gather to the full-precision SoA +
+    # kick + drift + scatter-back, whole records D2H (sf_b200_run_host in place, 3-stream chunk ring)
+    hb = api.HostBuffer(v.nbytes, 0)
+    torch.from_numpy(hb.numpy()).copy_(src.data[: v.nbytes])
+    torch.cuda.synchronize()
+    dst = api.View(P, n, "soa", None, api.SF_PREC_NATIVE)
+    api.run_host(v, hb, dst, "kick,drift", 1e-3, chunk=1 << 18, mode=2)
+    secs = []
+    for _ in range(max(3, min(args.steps, 10))):
+        m = api.run_host(v, hb, dst, "kick,drift", 1e-3, chunk=1 << 18, mode=2)
+        secs.append(m["seconds"])
+    hb.free()
+    e2e_s = sum(secs) / len(secs)
+    e2e = {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": m["h2d_bytes"], "d2h_bytes_per_step": m["d2h_bytes"],
+           "ms": e2e_s * 1e3, "path": "sf_b200_run_host(mode 2): pinned host AoS, whole records H2D || gather to the "
+                                      "full-precision SoA + kick + drift + scatter-back || whole records D2H"}
+    return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": out["kick,drift"]["roofline"], "e2e": e2e,
             "config": {"workload": "C1 (BASELINE configs[0]): kick then drift in place on 1M particles, AoS "
                                    "full-precision storage (default 88-B schema), one pass over the records "
                                    "(run_kernel('kick,drift'); the per-kernel launches are under 'kernels')", "particles": n,
