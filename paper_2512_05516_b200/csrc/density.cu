@@ -98,15 +98,6 @@ struct CellGrid {
     int64_t n_home;  // particles [0, n_home) (particle order) are homes; the rest neighbours only
 };
 
-// The home kernels run one thread per home over a grid of ceil(n/256) CTAs
-// (not a capped grid-stride loop): the block scheduler hands out CTAs in
-// index order, so the CTAs in flight always cover one compact range of the
-// cell-sorted homes and their candidate columns stay in L2.  With the grid
-// capped at 16 CTAs/SM, each resident CTA strode through the whole range,
-// the in-flight set scattered across it and the L2 hit rate of k_pairs_c
-// at C5 (128M) fell to 46% (91% uncapped; 54 -> 46 ms).
-static unsigned home_grid(uint64_t n) { return unsigned((n + 255) / 256); }
-
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -118,38 +109,87 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
-// Branch-free M4 pair term (sph.cpp:17-24 with h_ij = (h_i + h_j)/2):
-//   pi h_ij^3 w(q) = (max(2-q,0)^3 - 4 max(1-q,0)^3) / 4
-// (for q < 1 the difference expands to 1 - 1.5 q^2 + 0.75 q^3, sph.cpp:20;
-// for 1 <= q < 2 only the first term is left, sph.cpp:22; beyond 2 both are
-// 0); the 1/(4 pi) is applied once per particle.  Every candidate runs the
-// same instructions: no support test, no branch, one MUFU.RCP and one
-// MUFU.SQRT (approximate forms; the sum stays within rel 1e-5 of the binary64
-// oracle, tests/test_gpu_parity.py).  hh_i = h_i / 2.
-// pj = (x, y, z, m) of the candidate, hj its smoothing length.
-__device__ __forceinline__ float pair_term(const float4 pi, float hh_i, const float4 pj, float hj) {
-    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float inv_h = rcp_approx(fmaf(0.5f, hj, hh_i));
-    const float q = sqrt_approx(r2) * inv_h;
-    const float t = fmaxf(2.0f - q, 0.0f);
-    const float u = fmaxf(1.0f - q, 0.0f);
-    const float w = fmaf(t * t, t, (u * u) * (-4.0f * u));
-    return (pj.w * (inv_h * inv_h * inv_h)) * w;
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
-// The spline factor alone when every candidate has the home's h (uniform
-// smoothing length, detected per launch from the blocks' h range): h_ij = h,
-// so 1/h_ij and its cube are per-home constants — the caller accumulates
-// m_j w with one FFMA and scales by 1/h^3 once per home.  The candidate is
-// one float4 (x, y, z, m): one load, no other array.
-__device__ __forceinline__ float pair_w_u(const float4 pi, float inv_h, const float4 pj) {
-    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float q = sqrt_approx(r2) * inv_h;
-    const float t = fmaxf(2.0f - q, 0.0f);
-    const float u = fmaxf(1.0f - q, 0.0f);
-    return fmaf(t * t, t, (u * u) * (-4.0f * u));
+// Packed binary32 pairs (sm_100 f32x2: one FADD2 / FMUL2 / FFMA2 issues two
+// IEEE binary32 operations, round to nearest, no flush).  A thread evaluates
+// one candidate against TWO homes per instruction: the homes' coordinates
+// are the pair, the candidate's scalars are broadcast operands.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float lo2(f32x2 a) {
+    float l, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(a));
+    (void)h;
+    return l;
+}
+__device__ __forceinline__ float hi2(f32x2 a) {
+    float l, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(a));
+    (void)l;
+    return h;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// A pair held in one aligned register pair for a whole loop (one FADD2 of +0:
+// ptxas keeps the result instead of re-packing the two scalars at every use;
+// -0 becomes +0, which no difference or product here can see).
+__device__ __forceinline__ f32x2 hold2(float lo, float hi) { return add2(pk2(lo, hi), 0ull); }
+
+// Branch-free M4 spline (sph.cpp:17-24), up to the factor 8 / (4 pi h^3):
+//   pi h^3 w(q) / 8 = t^3 - u^3,  t = sat(1 - q/2),  u = sat(c (1 - q)),  c = 2^(-1/3)
+// ((2 - q)^3 - 4 (1 - q)^3 = pi h^3 w for q < 1, sph.cpp:20; (2 - q)^3 alone
+// for 1 <= q < 2, sph.cpp:22; 0 beyond): saturating FMAs straight from r
+// (t = sat(1 + r (-1/2h)), u = sat(c + r (-c/h))), no branch and no support
+// test: every candidate runs the same instructions (approximate MUFU forms;
+// the sums stay within rel 1e-5 of the binary64 oracle,
+// tests/test_gpu_parity.py).  c carries the factor 1/2 of the u^3 term (c^3 =
+// 1/2 up to one rounding of c: relative 1e-7 on that term).
+constexpr float kC3 = 0.79370052598409974f;  // 2^(-1/3)
+
+__device__ __forceinline__ float spline_w8(float r, float inv_h) {
+    const float t = __saturatef(fmaf(-0.5f * inv_h, r, 1.0f));
+    const float u = __saturatef(fmaf(-kC3 * inv_h, r, kC3));
+    return fmaf(t * t, t, -(u * u) * u);
+}
+
+// Two homes (X, Y, Z packed) against one candidate pj: acc += m_j (t^3 - u^3).
+// A = -1/(2h), Bc = -c/h of the uniform h.
+__device__ __forceinline__ f32x2 density_pair2(f32x2 X, f32x2 Y, f32x2 Z, const float4 pj, float A, float Bc,
+                                               f32x2 acc) {
+    const f32x2 dx = sub2(X, pk2(pj.x, pj.x)), dy = sub2(Y, pk2(pj.y, pj.y)), dz = sub2(Z, pk2(pj.z, pj.z));
+    const f32x2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    const float r0 = sqrt_approx(lo2(r2)), r1 = sqrt_approx(hi2(r2));
+    const f32x2 t = pk2(__saturatef(fmaf(A, r0, 1.0f)), __saturatef(fmaf(A, r1, 1.0f)));
+    const f32x2 u = pk2(__saturatef(fmaf(Bc, r0, kC3)), __saturatef(fmaf(Bc, r1, kC3)));
+    const f32x2 w = sub2(mul2(mul2(t, t), t), mul2(mul2(u, u), u));
+    return fma2(w, pk2(pj.w, pj.w), acc);
 }
 
 // The smoothing-length range of the candidate blocks: hmax word [0] = bits of
@@ -168,17 +208,6 @@ __device__ __forceinline__ bool uniform_h(const BS& B, float* hmax) {
     return lo == hi && hi > 0.0f;
 }
 
-// Per-particle culled candidate runs.  As k_pairs_r (one thread per home
-// particle, the (2R+1)^2 neighbour columns swept in lockstep so neighbouring
-// lanes share candidate lines in L1), but every column's z-window is cut to
-// the cells that can hold a particle inside the support sphere of radius
-// h_i + h_max around the home particle (h_max from k_pack), and columns the
-// sphere misses are skipped.  For uniform particles with cells of side ~h at
-// reach 2 this evaluates ~84 of the 125 cells.  Cells on the grid faces
-// extend to infinity (binning clamps), so their distance is measured only on
-// their inner side.  Culling removes only candidates at q >= 2 (w = 0; a
-// 1e-5 radius margin covers rounding), and every candidate runs the
-// branch-free pair_term.
 // Candidate blocks: the homes' own cell-sorted block [0] plus up to two
 // neighbouring slabs' blocks [1], [2] (multi-GPU: their packed arrays read in
 // place over NVLink through peer pointers, no ghost copy).  Each block covers
@@ -196,31 +225,65 @@ struct BlockSet {
     int nb, NX;  // blocks in use; global x-layers (faces at 0 and NX)
 };
 
-template <int R, bool UNI>
-__device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __restrict__ perm, const CellGrid& G,
-                                           int64_t k, float hmax, float* __restrict__ rho) {
-    constexpr int W = 2 * R + 1;
-    const float4* __restrict__ hpos = B.b[0].pos;
-    const int hx0 = B.b[0].x0, hnx = B.b[0].nx;
-    const float hlox = B.b[0].lox;
-    const int64_t i_home = perm ? perm[k] : k;
-    if (i_home >= G.n_home) return;  // ghosts: neighbours only
-    const float4 pi = hpos[k];
-    const float h_i = B.b[0].h[k];
+// Two consecutive homes of the cell-sorted order per thread (almost always
+// the same cell column, usually the same cell): they share one pass over the
+// neighbour columns, each window cut to the support bound around the pair's
+// box, and every candidate is evaluated against both homes at once with the
+// packed-fp32 pair terms above.  A pair straddling a column boundary takes
+// one pass per home.  Homes past n or at/after n_home (ghosts) are not
+// written.
+struct HomePair {
+    float4 p0, p1;  // (x, y, z, m)
+    float h0, h1;
+    float fx0, fy0, fz0, fx1, fy1, fz1;  // cell coordinates (global x layers)
+    int ix0, iy0, ix1, iy1;
+    int64_t i0, i1;  // particle indices (i >= n_home: not a home)
+};
+
+template <class Blk>
+__device__ __forceinline__ HomePair load_pair(const Blk& b0, const int32_t* __restrict__ perm, const CellGrid& G,
+                                              int64_t k0, int64_t n) {
+    HomePair H;
+    const int64_t k1 = k0 + 1 < n ? k0 + 1 : k0;
+    H.i0 = perm ? int64_t(perm[k0]) : k0;
+    H.i1 = k0 + 1 < n ? (perm ? int64_t(perm[k1]) : k1) : G.n_home;
+    H.p0 = b0.pos[k0], H.p1 = b0.pos[k1];
+    H.h0 = b0.h[k0], H.h1 = b0.h[k1];
     // the binning formula of the own block (same origin, same rounding), then global layers
-    const float fxl = (pi.x - hlox) * G.inv_cell, fy = (pi.y - G.loy) * G.inv_cell, fz = (pi.z - G.loz) * G.inv_cell;
-    const int ix = min(max(int(floorf(fxl)), 0), hnx - 1) + hx0;
-    const float fx = fxl + float(hx0);
-    const int iy = min(max(int(floorf(fy)), 0), G.ny - 1);
-    const int iz = min(max(int(floorf(fz)), 0), G.nz - 1);
-    const float rc = (h_i + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
-    const float rc2 = rc * rc;
-    const float hh_i = 0.5f * h_i;
-    const float inv_hu = rcp_approx(fmaf(0.5f, h_i, hh_i));  // UNI: 1/h_ij for every candidate
-    const float ih3 = inv_hu * inv_hu * inv_hu;
-    const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
-    const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
-    float acc = 0.0f;
+    const float fxl0 = (H.p0.x - b0.lox) * G.inv_cell, fxl1 = (H.p1.x - b0.lox) * G.inv_cell;
+    H.fy0 = (H.p0.y - G.loy) * G.inv_cell, H.fy1 = (H.p1.y - G.loy) * G.inv_cell;
+    H.fz0 = (H.p0.z - G.loz) * G.inv_cell, H.fz1 = (H.p1.z - G.loz) * G.inv_cell;
+    H.ix0 = min(max(int(floorf(fxl0)), 0), b0.nx - 1) + b0.x0;
+    H.ix1 = min(max(int(floorf(fxl1)), 0), b0.nx - 1) + b0.x0;
+    H.fx0 = fxl0 + float(b0.x0), H.fx1 = fxl1 + float(b0.x0);
+    H.iy0 = min(max(int(floorf(H.fy0)), 0), G.ny - 1);
+    H.iy1 = min(max(int(floorf(H.fy1)), 0), G.ny - 1);
+    return H;
+}
+
+// The candidate runs of one pass (members m0 / m1 of the pair): for each of
+// the (2R+1)^2 neighbour columns the cells of one z-window are one contiguous
+// run [b, e) of a block (own, or a neighbouring slab's read in place), cut to
+// the support bound rc (cell units, squared) around the members' box;
+// columns the bound misses are skipped.  Cells on the grid faces extend to
+// infinity (binning clamps), so their distance is measured only on their
+// inner side.  Culling removes only candidates at q >= 2 (w = 0; the radius
+// margin covers rounding).  Neighbouring threads sweep the same runs in
+// lockstep (their homes are neighbours in the sorted order), so candidate
+// lines are shared through L1.
+template <int R, class BS, class Visit>
+__device__ __forceinline__ void pass_runs(const BS& B, const CellGrid& G, const HomePair& H, bool m0, bool m1,
+                                          float rc2, Visit&& visit) {
+    constexpr int W = 2 * R + 1;
+    const float fxlo = m0 ? (m1 ? fminf(H.fx0, H.fx1) : H.fx0) : H.fx1;
+    const float fxhi = m0 ? (m1 ? fmaxf(H.fx0, H.fx1) : H.fx0) : H.fx1;
+    const float fylo = m0 ? (m1 ? fminf(H.fy0, H.fy1) : H.fy0) : H.fy1;
+    const float fyhi = m0 ? (m1 ? fmaxf(H.fy0, H.fy1) : H.fy0) : H.fy1;
+    const float fzlo = fminf(fmaxf(m0 ? (m1 ? fminf(H.fz0, H.fz1) : H.fz0) : H.fz1, -1e6f), 1e6f);
+    const float fzhi = fminf(fmaxf(m0 ? (m1 ? fmaxf(H.fz0, H.fz1) : H.fz0) : H.fz1, -1e6f), 1e6f);
+    const int ix = m0 ? H.ix0 : H.ix1, iy = m0 ? H.iy0 : H.iy1;
+    const int izl = min(max(int(floorf(fzlo)), 0), G.nz - 1), izh = min(max(int(floorf(fzhi)), 0), G.nz - 1);
+    const int zmin = max(izl - R, 0), zmax = min(izh + R, G.nz - 1);
 #pragma unroll 1
     for (int dxi = -R; dxi <= R; ++dxi) {
         const int jx = ix + dxi;
@@ -228,66 +291,110 @@ __device__ __forceinline__ void pairs_home(const BlockSet& B, const int32_t* __r
         int g = 0;
         while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
         if (g == B.nb) continue;  // layer held by no block
-        const float4* __restrict__ pos = B.b[g].pos;
-        const float* __restrict__ hs = B.b[g].h;
         const int32_t* __restrict__ cell_start = B.b[g].cs;
-        // faces of the global grid extend to infinity (binning clamps)
         const float ddx =
-            fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f), 0.0f);
-        int b[W], e[W];
+            fmaxf(fmaxf(jx > 0 ? float(jx) - fxhi : 0.0f, jx < B.NX - 1 ? fxlo - float(jx + 1) : 0.0f), 0.0f);
         const int cx = (jx - B.b[g].x0) * G.ny;  // cell ids fit in int32 (checked on the host)
-#pragma unroll
+#pragma unroll 1
         for (int t = 0; t < W; ++t) {
             const int jy = iy - R + t;
             const float ddy =
-                fmaxf(fmaxf(jy > 0 ? float(jy) - fy : 0.0f, jy < G.ny - 1 ? fy - float(jy + 1) : 0.0f), 0.0f);
+                fmaxf(fmaxf(jy > 0 ? float(jy) - fyhi : 0.0f, jy < G.ny - 1 ? fylo - float(jy + 1) : 0.0f), 0.0f);
             const float d2 = fmaf(ddx, ddx, ddy * ddy);
             const float dz = sqrt_approx(fmaxf(rc2 - d2, 0.0f));  // rel err ~1e-7, inside the margin
-            const int zlo = min(max(int(floorf(fzc - dz)), zmin), G.nz - 1);
-            const int zhi = max(min(int(floorf(fzc + dz)), zmax), 0);
-            const bool ok = jy >= 0 && jy < G.ny && d2 < rc2 && zlo <= zhi;
-            const int c0 = (cx + (ok ? jy : 0)) * G.nz;
-            b[t] = ok ? __ldg(cell_start + c0 + zlo) : 0;
-            e[t] = ok ? __ldg(cell_start + c0 + zhi + 1) : 0;
-        }
-#pragma unroll
-        for (int t = 0; t < W; ++t) {
-            int j = b[t];
-            for (; j + 1 < e[t]; j += 2) {
-                const float4 p0 = pos[j], p1 = pos[j + 1];
-                if constexpr (UNI) {
-                    acc = fmaf(p0.w, pair_w_u(pi, inv_hu, p0), acc);
-                    acc = fmaf(p1.w, pair_w_u(pi, inv_hu, p1), acc);
-                } else {
-                    acc += pair_term(pi, hh_i, p0, __ldg(hs + j));
-                    acc += pair_term(pi, hh_i, p1, __ldg(hs + j + 1));
-                }
-            }
-            if (j < e[t]) {
-                const float4 p0 = pos[j];
-                if constexpr (UNI) acc = fmaf(p0.w, pair_w_u(pi, inv_hu, p0), acc);
-                else acc += pair_term(pi, hh_i, p0, __ldg(hs + j));
-            }
+            const int zlo = min(max(int(floorf(fzlo - dz)), zmin), G.nz - 1);
+            const int zhi = max(min(int(floorf(fzhi + dz)), zmax), 0);
+            if (jy < 0 || jy >= G.ny || !(d2 < rc2) || zlo > zhi) continue;
+            const int c0 = (cx + jy) * G.nz;
+            visit(g, __ldg(cell_start + c0 + zlo), __ldg(cell_start + c0 + zhi + 1));
         }
     }
-    constexpr float k4pi = 0.079577471545947668f;  // 1 / (4 pi)
-    rho[i_home] = UNI ? acc * (ih3 * k4pi) : acc * k4pi;
 }
 
+template <int R, bool UNI>
+__device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __restrict__ perm, const CellGrid& G,
+                                            int64_t k0, int64_t n, float hmax, float* __restrict__ rho) {
+    const HomePair H = load_pair(B.b[0], perm, G, k0, n);
+    const bool live0 = H.i0 < G.n_home, live1 = H.i1 < G.n_home;
+    if (!live0 && !live1) return;  // ghosts: neighbours only
+    constexpr float k2InvPi = 0.63661977236758134f;  // 8 / (4 pi): spline_w8 carries w / 8
+    if constexpr (UNI) {
+        const bool same = H.ix0 == H.ix1 && H.iy0 == H.iy1;
+        const float inv_h = rcp_approx(hmax);  // h_ij = h for every pair
+        const float A = -0.5f * inv_h, Bc = -kC3 * inv_h;
+        const float rc = 2.0f * hmax * G.inv_cell * 1.00001f;  // support bound, cell units
+        const f32x2 X = hold2(H.p0.x, H.p1.x), Y = hold2(H.p0.y, H.p1.y), Z = hold2(H.p0.z, H.p1.z);
+        float res0 = 0.0f, res1 = 0.0f;
+#pragma unroll 1
+        for (int pass = 0; pass < (same ? 1 : 2); ++pass) {
+            const bool m0 = same || pass == 0, m1 = same || pass == 1;
+            f32x2 acc = 0ull, acc2 = 0ull;  // +0.0f pairs; two chains for ILP
+            pass_runs<R>(B, G, H, m0, m1, rc * rc, [&](int g, int b, int e) {
+                const float4* __restrict__ pos = B.b[g].pos;
+                int j = b;
+#pragma unroll 1
+                for (; j + 1 < e; j += 2) {
+                    const float4 p = pos[j], q = pos[j + 1];
+                    acc = density_pair2(X, Y, Z, p, A, Bc, acc);
+                    acc2 = density_pair2(X, Y, Z, q, A, Bc, acc2);
+                }
+                if (j < e) acc = density_pair2(X, Y, Z, pos[j], A, Bc, acc);
+            });
+            acc = add2(acc, acc2);
+            if (m0) res0 = lo2(acc);
+            if (m1) res1 = hi2(acc);
+        }
+        const float scale = (inv_h * inv_h) * inv_h * k2InvPi;
+        if (live0) rho[H.i0] = res0 * scale;
+        if (live1) rho[H.i1] = res1 * scale;
+    } else {
+        // spread h: one home at a time, h_ij = (h_i + h_j) / 2 per pair
+#pragma unroll 1
+        for (int m = 0; m < 2; ++m) {
+            if (!(m ? live1 : live0)) continue;
+            const float4 pi = m ? H.p1 : H.p0;
+            const float hh = 0.5f * (m ? H.h1 : H.h0);
+            const float rc = (2.0f * hh + hmax) * G.inv_cell * 1.00001f;
+            float acc = 0.0f;
+            pass_runs<R>(B, G, H, m == 0, m == 1, rc * rc, [&](int g, int b, int e) {
+                const float4* __restrict__ pos = B.b[g].pos;
+                const float* __restrict__ hs = B.b[g].h;
+#pragma unroll 1
+                for (int j = b; j < e; ++j) {
+                    const float4 pj = pos[j];
+                    const float ih = rcp_approx(fmaf(0.5f, __ldg(hs + j), hh));
+                    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+                    const float r = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    acc = fmaf(pj.w * ((ih * ih) * ih), spline_w8(r, ih), acc);
+                }
+            });
+            rho[m ? H.i1 : H.i0] = acc * k2InvPi;
+        }
+    }
+}
+
+// One thread per pair of homes over a grid of ceil(n/512) CTAs (not a capped
+// grid-stride loop): the block scheduler hands out CTAs in index order, so
+// the CTAs in flight always cover one compact range of the cell-sorted homes
+// and their candidate columns stay in L2 (with the grid capped at 16 CTAs/SM
+// the resident CTAs strode through the whole range and the L2 hit rate at C5
+// fell from 91% to 46%).
+static unsigned pair_grid(uint64_t n) { return unsigned(((n + 1) / 2 + 255) / 256); }
+
 template <int R>
-__global__ void __launch_bounds__(256, 5) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+__global__ void __launch_bounds__(256, 4) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
                                                  int64_t n, float* __restrict__ rho) {
     float hmax;
     const bool uni = uniform_h(B, &hmax);
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
-        if (uni) pairs_home<R, true>(B, perm, G, k, hmax, rho);
-        else pairs_home<R, false>(B, perm, G, k, hmax, rho);
-    }
+    const int64_t k0 = 2 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
+    if (k0 >= n) return;
+    if (uni) pairs_home2<R, true>(B, perm, G, k0, n, hmax, rho);
+    else pairs_home2<R, false>(B, perm, G, k0, n, hmax, rho);
 }
 
 static void launch_pairs(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach, float* rho,
                          cudaStream_t st) {
-    const unsigned grid = home_grid(uint64_t(n));
+    const unsigned grid = pair_grid(uint64_t(n));
     if (reach == 1) k_pairs_c<1><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
     else if (reach == 2) k_pairs_c<2><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
     else if (reach == 3) k_pairs_c<3><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
@@ -407,12 +514,6 @@ __global__ void k_pack_force(const void* __restrict__ x, const void* __restrict_
     }
     h_range(hmax, hmin, hmax_bits);
     if (__any_sync(0xffffffffu, zero) && (threadIdx.x & 31) == 0) atomicOr(degenerate, 1u);
-}
-
-__device__ __forceinline__ float rsqrt_approx(float x) {
-    float r;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
 }
 
 // Candidate blocks of the force: a density block's (x,y,z,m) and h plus the
@@ -545,7 +646,7 @@ __global__ void __launch_bounds__(256) k_force_c(const ForceBlockSet B, const in
 
 static void launch_force(const ForceBlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
                          float* a, float* du, cudaStream_t st) {
-    const unsigned grid = home_grid(uint64_t(n));
+    const unsigned grid = unsigned((uint64_t(n) + 255) / 256);  // one thread per home, in index order
     if (reach == 1) k_force_c<1, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
     else if (reach == 2) k_force_c<2, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
     else if (reach == 3) k_force_c<3, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);

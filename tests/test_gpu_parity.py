@@ -289,6 +289,25 @@ def test_density_cells_vs_oracle(prec, refine):
         assert np.all(np.diff(perm_h[cs_h[c]:cs_h[c + 1]]) > 0)
 
 
+@pytest.mark.parametrize("refine", [3, 4])
+def test_cells_reach_3_and_4_vs_oracle(refine):
+    """Reach 3 / 4 (49 / 81 neighbour columns: more than one 32-column batch
+    per warp group), spread h (the general pair term), density and force."""
+    n = 1 << 14
+    ts, (xd, vd, md, hd, rd, Pd) = _force_case(n, 40 + refine, api.SF_PREC_NATIVE)
+    nc = int(np.floor(1.0 / float(2 * ts[3].max())))
+    cell = 1.0 / nc / refine
+    dims = (nc * refine,) * 3
+    cs, perm = api.bin_particles(ts[0].contiguous(), (0, 0, 0), cell, dims)
+    rho = api.density_cells(ts[0], ts[2], ts[3], cs, perm, (0, 0, 0), cell, dims, reach=refine)
+    want = O.density_cells(xd.reshape(-1), md, hd, 0.0, 1.0, 1.0 / nc)
+    np.testing.assert_allclose(rho.double().cpu().numpy(), want, rtol=1e-5, atol=0)
+    a, du = api.force_cells(*ts, cs, perm, (0, 0, 0), cell, dims, reach=refine)
+    want_a, want_du, sa, sd = O.force_cells(xd.reshape(-1), vd.reshape(-1), md, hd, rd, Pd, 0.0, 1.0, 1.0 / nc)
+    assert np.all(np.linalg.norm(a.double().cpu().numpy() - want_a, axis=1) <= FORCE_TOL * sa)
+    assert np.all(np.abs(du.double().cpu().numpy() - want_du) <= FORCE_TOL * sd + 1e-30)
+
+
 def test_density_cells_homes_and_ghosts():
     """Only the first n_home particles are computed; the rest (ghosts) feed
     their neighbours only and keep rho untouched."""
