@@ -216,9 +216,8 @@ def c3(args, peak, peak_kind):
         rl["useful_TFLOPs"] = rl["pairs_per_s"] * 24 / 1e12  # ~24 flops per in-support pair
         rl["fp32_peak_TFLOPs"] = peak_tf
         rl["useful_flop_frac"] = rl["useful_TFLOPs"] / peak_tf
-        rl["note"] = ("issue-bound: ncu smsp__issue_active ~82% with ~56% SIMD efficiency and ~2.75 evaluated "
-                      "candidates per in-support pair (profiles/r01_pairs_ncu_summary.txt); frac is on HBM bytes, "
-                      "which are not the limiter")
+        rl["note"] = ("FP32-issue-bound pair loop: see the ncu issue activity, SIMD efficiency and FMA-pipe use "
+                      "under roofline.ncu (profiles/kernel_metrics.json)")
     return {"value": n / (ms * 1e-3), "ms_per_step": ms, "roofline": rl,
             "config": {"workload": "C3 (BASELINE configs[2]): SPH density, cell-linked, 4M uniform particles, "
                                    "SoA fp32 vs fp16 vs bf16", "particles": n, "h": h, "cells_per_side": nc,

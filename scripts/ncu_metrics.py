@@ -50,4 +50,9 @@ def metrics(rep):
 
 
 if __name__ == "__main__":
-    print(json.dumps({sys.argv[2]: metrics(sys.argv[1])[0]}))
+    # ncu_metrics.py <report> <key>                    first kernel of the report
+    # ncu_metrics.py <report> <key> <kernel-substring>  first kernel whose name contains the substring
+    ms = metrics(sys.argv[1])
+    if len(sys.argv) > 3:
+        ms = [m for m in ms if sys.argv[3] in m["kernel"]]
+    print(json.dumps({sys.argv[2]: ms[0]}))
