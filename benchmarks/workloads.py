@@ -506,6 +506,7 @@ def timestep_pipeline(args, n: int = 1 << 20) -> dict:
                     speed["%s/%s_vs_aos_inplace32" % (mode, prec)] = base["total_s"] / t["total_s"]
     return {"particles": n, "rows": res, "soa_speedup_vs_aos": speed,
             "paper": "In-place / Streaming vs AoS baseline: 2.6x / ~2x GH200, 1.9x / 1.4x H100 (PAPER.md:554)",
-            "note": "moves are measured pinned cudaMemcpy (whole records in place; narrowed fields as "
-                    "byte columns, one 2-D DMA per run of adjacent fields, when streaming); phases run one "
-                    "after another as in the reference's Run (not overlapped)"}
+            "note": "moves are measured over PCIe: in place = pinned cudaMemcpy of the whole compressed records "
+                    "each way; streaming = the conversion kernels read / store only the kernel's narrowed lanes "
+                    "of the pinned host records in place (zero copy); phases run one after another as in the "
+                    "reference's Run (not overlapped)"}

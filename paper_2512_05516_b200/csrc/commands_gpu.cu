@@ -345,11 +345,6 @@ struct VariantResult {
     uint64_t checksum = 0;
 };
 
-#ifndef SFB_STREAM_ZERO_COPY
-#define SFB_STREAM_ZERO_COPY 1
-#endif
-constexpr bool kStreamZeroCopy = SFB_STREAM_ZERO_COPY;
-
 struct PinnedBuf {
     void* p = nullptr;
     explicit PinnedBuf(size_t bytes) { check_cuda(cudaHostAlloc(&p, bytes + 16, cudaHostAllocDefault), "cudaHostAlloc"); }
@@ -357,48 +352,15 @@ struct PinnedBuf {
     ~PinnedBuf() { cudaFreeHost(p); }
 };
 
-// The narrowed record N(set) as byte columns of the full record: one 2-D DMA
-// per run of fields adjacent in both records (pitch = record), so exactly
-// the narrowed bytes cross PCIe (streamed_bytes_one_way, pipelines.cpp:
-// 434-441) and the copy engine does the narrowing.
-struct Column {
-    size_t full_off, narrow_off, bytes;
-};
-std::vector<Column> narrowed_columns(const View& full, const View& nv) {
-    std::vector<Column> cols;
-    for (size_t p = 0; p < nv.subset.size(); ++p) {
-        const size_t fo = size_t(full.lane_base(full.pos_of(nv.subset[p])) / 8), no = size_t(nv.lane_base(int(p)) / 8);
-        const size_t w = size_t(uint64_t(nv.arity(int(p))) * nv.width(int(p)) / 8);
-        if (!cols.empty() && cols.back().full_off + cols.back().bytes == fo && cols.back().narrow_off + cols.back().bytes == no)
-            cols.back().bytes += w;
-        else
-            cols.push_back({fo, no, w});
-    }
-    return cols;
-}
-
-void copy_columns(const std::vector<Column>& cols, void* narrow, size_t narrow_pitch, void* full, size_t full_pitch,
-                  uint64_t n, bool to_device) {
-    for (const Column& c : cols) {
-        uint8_t* nb = static_cast<uint8_t*>(narrow) + c.narrow_off;
-        uint8_t* fb = static_cast<uint8_t*>(full) + c.full_off;
-        if (to_device)
-            check_cuda(cudaMemcpy2DAsync(nb, narrow_pitch, fb, full_pitch, c.bytes, n, cudaMemcpyHostToDevice, nullptr),
-                       "H2D columns");
-        else
-            check_cuda(cudaMemcpy2DAsync(fb, full_pitch, nb, narrow_pitch, c.bytes, n, cudaMemcpyDeviceToHost, nullptr),
-                       "D2H columns");
-    }
-}
-
 // pipelines::run_variant (pipelines.cpp:378-405) on the GPU, over real PCIe.
 // The state lives in pinned host memory.  dev-* variants: in-place moves the
 // whole compressed AoS to the device once, runs every kernel there (through
 // the variant's conversions) and moves it back (run_dev_inplace,
 // pipelines.cpp:231-249); streaming moves, per kernel, only the narrowed
 // fields each way — read from / stored into the host records in place by the
-// conversion kernels (zero copy; 1.6x faster than byte-column 2-D DMA, which
-// SFB_STREAM_ZERO_COPY=0 builds) — and converts on the device
+// conversion kernels (zero copy: only the narrowed lanes cross PCIe; 1.6x
+// faster than moving them as byte columns with 2-D DMA, measured in round 2)
+// — and converts on the device
 // (run_dev_streaming, :251-296).  move_s is the measured transfer time and bytes_to_device /
 // bytes_to_host the bytes actually copied (= the reference ledger).
 // cpu-* variants run on the device with no transfer (their state is where
@@ -434,7 +396,6 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
                 check_cuda(cudaMemcpyAsync(state.p, hstate->p, abytes, cudaMemcpyHostToDevice, nullptr), "H2D");
             });
     }
-    const size_t rec_bytes = size_t(aos.record_bits() / 8);
     for (const auto& k : c.kernels) {
         const KernelSet* set = pop.schema->kernel(k);
         if (!set) throw std::invalid_argument("no access set declared for kernel '" + k + "'");
@@ -445,16 +406,12 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
             DevBuf nb(nv.total_bytes());
             const bool cols = aos.byte_aligned() && nv.byte_aligned() && aos.record_bits() % 8 == 0 &&
                               nv.record_bits() % 8 == 0;
-            const std::vector<Column> colv = cols ? narrowed_columns(aos, nv) : std::vector<Column>{};
-            const size_t nrec = size_t(nv.record_bits() / 8);
             res.to_dev += nv.total_bytes();
             res.to_host += nv.total_bytes();
             res.transfers += 2;
             res.move_s += gpu_seconds([&] {
-                if (kStreamZeroCopy && cols) {  // the device reads the narrowed lanes of the host records in place
+                if (cols) {  // the device reads the narrowed lanes of the host records in place
                     gather(aos, hstate->p, nv, nb.p, nullptr, 0.0, 0, nullptr, true);
-                } else if (cols) {
-                    copy_columns(colv, nb.p, nrec, hstate->p, rec_bytes, n, true);
                 } else {  // bit-packed records: whole records over PCIe, narrowed on the device
                     check_cuda(cudaMemcpyAsync(state.p, hstate->p, abytes, cudaMemcpyHostToDevice, nullptr), "H2D");
                     convert(aos, state.p, nv, nb.p, nullptr);
@@ -477,10 +434,8 @@ VariantResult run_variant_gpu(const RunConfig& c, const Population& pop, const s
             }
             // N^T: the narrowed fields back into the host records (read-only fields come back bit-identical)
             res.move_s += gpu_seconds([&] {
-                if (kStreamZeroCopy && cols) {  // ... and stores them back in place
+                if (cols) {  // ... and stores them back in place
                     convert_fields(nv, nb.p, aos, hstate->p, nv.subset, nullptr, true);
-                } else if (cols) {
-                    copy_columns(colv, nb.p, nrec, hstate->p, rec_bytes, n, false);
                 } else {
                     scatter_merge(nv, nb.p, aos, state.p, k, nullptr);
                     check_cuda(cudaMemcpyAsync(hstate->p, state.p, abytes, cudaMemcpyDeviceToHost, nullptr), "D2H");
