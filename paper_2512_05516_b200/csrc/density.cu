@@ -13,15 +13,16 @@
 //                 values widen exactly), and finds the h range (largest and
 //                 smallest h: equal ends select the uniform-h pair loop, which
 //                 reads one float4 per candidate and nothing else);
-//   k_pairs_c     one thread per home particle of the own x-layers (a
-//                 contiguous range of the sorted order): for each of the
-//                 (2R+1)^2 (dx, dy) neighbour columns the cells of one
-//                 z-window are one contiguous run of the packed array, read
-//                 through L1/L2 (neighbouring lanes sweep the same runs in
-//                 lockstep); each window is culled to the support sphere
-//                 h_i + h_max; every candidate runs the same branch-free pair
-//                 term (1/h_ij hoisted per home when h is uniform).  rho is
-//                 stored back in particle (unsorted) order.
+//   k_pairs_c     one thread per PAIR of consecutive homes of the own
+//                 x-layers (a contiguous range of the sorted order; the two
+//                 usually share a cell): for each of the (2R+1)^2 (dx, dy)
+//                 neighbour columns the cells of one z-window are one
+//                 contiguous run of the packed array, read through L1/L2
+//                 (neighbouring lanes sweep the same runs in lockstep); each
+//                 window is culled to the support bound around the pair's box;
+//                 every candidate runs the same branch-free pair term against
+//                 both homes at once (packed fp32, 1/h_ij hoisted when h is
+//                 uniform).  rho is stored back in particle (unsorted) order.
 //
 // With cells of side >= 2h use reach 1 (27 cells); with cells of side >= h
 // reach 2 (125 smaller cells, ~84 after culling).  Pair formula: the
