@@ -181,17 +181,37 @@ __device__ __forceinline__ float spline_w8(float r, float inv_h) {
 }
 
 // Two homes (X, Y, Z packed) against one candidate pj: acc += m_j (t^3 - u^3).
-// A = -1/(2h), Bc = -c/h of the uniform h.
+// A = -1/(2h), Bc = -c/h of the uniform h.  in0 / in1: the candidate lies
+// inside the support of home 0 / 1 (t > 0, i.e. r < 2h).
 __device__ __forceinline__ f32x2 density_pair2(f32x2 X, f32x2 Y, f32x2 Z, const float4 pj, float A, float Bc,
-                                               f32x2 acc) {
+                                               f32x2 acc, bool& in0, bool& in1) {
     const f32x2 dx = sub2(X, pk2(pj.x, pj.x)), dy = sub2(Y, pk2(pj.y, pj.y)), dz = sub2(Z, pk2(pj.z, pj.z));
     const f32x2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
     const float r0 = sqrt_approx(lo2(r2)), r1 = sqrt_approx(hi2(r2));
-    const f32x2 t = pk2(__saturatef(fmaf(A, r0, 1.0f)), __saturatef(fmaf(A, r1, 1.0f)));
+    const float t0 = __saturatef(fmaf(A, r0, 1.0f)), t1 = __saturatef(fmaf(A, r1, 1.0f));
+    in0 = t0 > 0.0f, in1 = t1 > 0.0f;
+    const f32x2 t = pk2(t0, t1);
     const f32x2 u = pk2(__saturatef(fmaf(Bc, r0, kC3)), __saturatef(fmaf(Bc, r1, kC3)));
     const f32x2 w = sub2(mul2(mul2(t, t), t), mul2(mul2(u, u), u));
     return fma2(w, pk2(pj.w, pj.w), acc);
 }
+
+// The density's in-support bit masks for the force of the same step (which
+// needs every rho first, then exactly the same pairs).  For window w (the
+// neighbour columns in (dx, dy) row-major order, reach <= 2: 25 windows) of
+// the home at sorted position k: occ[k] bit w = the window holds an
+// in-support candidate, and then win[w * stride + k] = ((block << 30) | the
+// window's first candidate, bits) with bit i set when candidate first + i
+// lies inside the home's support; occ[k] bit 31: a window held more than 32
+// candidates (that home's force sweeps its windows instead).  Neighbouring
+// homes write neighbouring 8-byte words of a window (coalesced); empty
+// windows are neither written nor read.
+struct WindowMasks {
+    int2* win;
+    uint32_t* occ;
+    int64_t stride;
+};
+constexpr uint32_t kOccOverflow = 1u << 31;
 
 // The smoothing-length range of the candidate blocks: hmax word [0] = bits of
 // the largest h, word [1] = ~bits of the smallest (0 = unknown: not uniform).
@@ -271,7 +291,8 @@ __device__ __forceinline__ HomePair load_pair(const Blk& b0, const int32_t* __re
 // inner side.  Culling removes only candidates at q >= 2 (w = 0; the radius
 // margin covers rounding).  Neighbouring threads sweep the same runs in
 // lockstep (their homes are neighbours in the sorted order), so candidate
-// lines are shared through L1.
+// lines are shared through L1.  visit(w, g, b, e) is called for every window
+// w of the (2R+1)^2 (row-major in (dx, dy)); empty ones with b == e.
 template <int R, class BS, class Visit>
 __device__ __forceinline__ void pass_runs(const BS& B, const CellGrid& G, const HomePair& H, bool m0, bool m1,
                                           float rc2, Visit&& visit) {
@@ -288,10 +309,14 @@ __device__ __forceinline__ void pass_runs(const BS& B, const CellGrid& G, const 
 #pragma unroll 1
     for (int dxi = -R; dxi <= R; ++dxi) {
         const int jx = ix + dxi;
-        if (jx < 0 || jx >= B.NX) continue;
+        const int w0 = (dxi + R) * W;  // window index of the row's first column
         int g = 0;
-        while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
-        if (g == B.nb) continue;  // layer held by no block
+        if (jx >= 0 && jx < B.NX)
+            while (g < B.nb && (jx < B.b[g].x0 || jx >= B.b[g].x0 + B.b[g].nx)) ++g;
+        if (jx < 0 || jx >= B.NX || g == B.nb) {  // outside the grid, or a layer held by no block
+            for (int t = 0; t < W; ++t) visit(w0 + t, 0, 0, 0);
+            continue;
+        }
         const int32_t* __restrict__ cell_start = B.b[g].cs;
         const float ddx =
             fmaxf(fmaxf(jx > 0 ? float(jx) - fxhi : 0.0f, jx < B.NX - 1 ? fxlo - float(jx + 1) : 0.0f), 0.0f);
@@ -305,20 +330,36 @@ __device__ __forceinline__ void pass_runs(const BS& B, const CellGrid& G, const 
             const float dz = sqrt_approx(fmaxf(rc2 - d2, 0.0f));  // rel err ~1e-7, inside the margin
             const int zlo = min(max(int(floorf(fzlo - dz)), zmin), G.nz - 1);
             const int zhi = max(min(int(floorf(fzhi + dz)), zmax), 0);
-            if (jy < 0 || jy >= G.ny || !(d2 < rc2) || zlo > zhi) continue;
+            if (jy < 0 || jy >= G.ny || !(d2 < rc2) || zlo > zhi) {
+                visit(w0 + t, g, 0, 0);
+                continue;
+            }
             const int c0 = (cx + jy) * G.nz;
-            visit(g, __ldg(cell_start + c0 + zlo), __ldg(cell_start + c0 + zhi + 1));
+            visit(w0 + t, g, __ldg(cell_start + c0 + zlo), __ldg(cell_start + c0 + zhi + 1));
         }
     }
 }
 
-template <int R, bool UNI>
+template <int R, bool UNI, bool LIST>
 __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __restrict__ perm, const CellGrid& G,
-                                            int64_t k0, int64_t n, float hmax, float* __restrict__ rho) {
+                                            int64_t k0, int64_t n, float hmax, float* __restrict__ rho,
+                                            const WindowMasks& M) {
     const HomePair H = load_pair(B.b[0], perm, G, k0, n);
     const bool live0 = H.i0 < G.n_home, live1 = H.i1 < G.n_home;
     if (!live0 && !live1) return;  // ghosts: neighbours only
     constexpr float k2InvPi = 0.63661977236758134f;  // 8 / (4 pi): spline_w8 carries w / 8
+    uint32_t occ0 = 0, occ1 = 0;                     // LIST: windows with in-support candidates, overflow
+    // LIST: a home's window (base, in-support bits) for the force, when it holds any
+    auto put = [&](bool home, int w, int g, int b, uint32_t bits, bool fit) {
+        uint32_t& occ = home ? occ1 : occ0;
+        if (!fit) occ |= kOccOverflow;
+        if (bits == 0) return;
+        occ |= 1u << w;
+        // streaming store (evict-first): the masks are read once, by the force, and must not push the
+        // candidate lines out of L2
+        __stcs(M.win + int64_t(w) * M.stride + k0 + (home ? 1 : 0),
+               make_int2(int(uint32_t(g) << 30 | uint32_t(b)), int(bits)));
+    };
     if constexpr (UNI) {
         const bool same = H.ix0 == H.ix1 && H.iy0 == H.iy1;
         const float inv_h = rcp_approx(hmax);  // h_ij = h for every pair
@@ -330,16 +371,37 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
         for (int pass = 0; pass < (same ? 1 : 2); ++pass) {
             const bool m0 = same || pass == 0, m1 = same || pass == 1;
             f32x2 acc = 0ull, acc2 = 0ull;  // +0.0f pairs; two chains for ILP
-            pass_runs<R>(B, G, H, m0, m1, rc * rc, [&](int g, int b, int e) {
+            pass_runs<R>(B, G, H, m0, m1, rc * rc, [&](int w, int g, int b, int e) {
                 const float4* __restrict__ pos = B.b[g].pos;
+                uint32_t mk0 = 0, mk1 = 0, bit = 1;  // LIST: bit of candidate j (0 past 32: no mask)
+                const bool fit = e - b <= 32;
                 int j = b;
 #pragma unroll 1
                 for (; j + 1 < e; j += 2) {
                     const float4 p = pos[j], q = pos[j + 1];
-                    acc = density_pair2(X, Y, Z, p, A, Bc, acc);
-                    acc2 = density_pair2(X, Y, Z, q, A, Bc, acc2);
+                    bool a0, a1, b0, b1;
+                    acc = density_pair2(X, Y, Z, p, A, Bc, acc, a0, a1);
+                    acc2 = density_pair2(X, Y, Z, q, A, Bc, acc2, b0, b1);
+                    if constexpr (LIST) {
+                        if (a0) mk0 |= bit;
+                        if (a1) mk1 |= bit;
+                        if (b0) mk0 |= bit << 1;
+                        if (b1) mk1 |= bit << 1;
+                        bit <<= 2;
+                    }
                 }
-                if (j < e) acc = density_pair2(X, Y, Z, pos[j], A, Bc, acc);
+                if (j < e) {
+                    bool a0, a1;
+                    acc = density_pair2(X, Y, Z, pos[j], A, Bc, acc, a0, a1);
+                    if constexpr (LIST) {
+                        if (a0) mk0 |= bit;
+                        if (a1) mk1 |= bit;
+                    }
+                }
+                if constexpr (LIST) {
+                    if (m0 && live0) put(false, w, g, b, mk0, fit);
+                    if (m1 && live1) put(true, w, g, b, mk1, fit);
+                }
             });
             acc = add2(acc, acc2);
             if (m0) res0 = lo2(acc);
@@ -357,9 +419,11 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
             const float hh = 0.5f * (m ? H.h1 : H.h0);
             const float rc = (2.0f * hh + hmax) * G.inv_cell * 1.00001f;
             float acc = 0.0f;
-            pass_runs<R>(B, G, H, m == 0, m == 1, rc * rc, [&](int g, int b, int e) {
+            pass_runs<R>(B, G, H, m == 0, m == 1, rc * rc, [&](int w, int g, int b, int e) {
                 const float4* __restrict__ pos = B.b[g].pos;
                 const float* __restrict__ hs = B.b[g].h;
+                const bool fit = e - b <= 32;
+                uint32_t mk = 0;
 #pragma unroll 1
                 for (int j = b; j < e; ++j) {
                     const float4 pj = pos[j];
@@ -367,10 +431,16 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
                     const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
                     const float r = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                     acc = fmaf(pj.w * ((ih * ih) * ih), spline_w8(r, ih), acc);
+                    if (LIST && fit) mk |= uint32_t(fmaf(-0.5f * ih, r, 1.0f) > 0.0f) << (j - b);
                 }
+                if constexpr (LIST) put(m == 1, w, g, b, mk, fit);
             });
             rho[m ? H.i1 : H.i0] = acc * k2InvPi;
         }
+    }
+    if constexpr (LIST) {
+        if (live0) M.occ[k0] = occ0;
+        if (live1) M.occ[k0 + 1] = occ1;
     }
 }
 
@@ -382,24 +452,33 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
 // fell from 91% to 46%).
 static unsigned pair_grid(uint64_t n) { return unsigned(((n + 1) / 2 + 255) / 256); }
 
-template <int R>
+template <int R, bool LIST>
 __global__ void __launch_bounds__(256, 4) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
-                                                 int64_t n, float* __restrict__ rho) {
+                                                 int64_t n, float* __restrict__ rho, const WindowMasks M) {
     float hmax;
     const bool uni = uniform_h(B, &hmax);
     const int64_t k0 = 2 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
     if (k0 >= n) return;
-    if (uni) pairs_home2<R, true>(B, perm, G, k0, n, hmax, rho);
-    else pairs_home2<R, false>(B, perm, G, k0, n, hmax, rho);
+    if (uni) pairs_home2<R, true, LIST>(B, perm, G, k0, n, hmax, rho, M);
+    else pairs_home2<R, false, LIST>(B, perm, G, k0, n, hmax, rho, M);
+}
+
+template <bool LIST>
+static void launch_pairs_t(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
+                           float* rho, const WindowMasks& M, cudaStream_t st) {
+    const unsigned grid = pair_grid(uint64_t(n));
+    if (reach == 1) k_pairs_c<1, LIST><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
+    else if (reach == 2) k_pairs_c<2, LIST><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
+    else if constexpr (!LIST) {  // window masks: 25 windows at most (reach <= 2)
+        if (reach == 3) k_pairs_c<3, false><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
+        else k_pairs_c<4, false><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
+    }
 }
 
 static void launch_pairs(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach, float* rho,
-                         cudaStream_t st) {
-    const unsigned grid = pair_grid(uint64_t(n));
-    if (reach == 1) k_pairs_c<1><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
-    else if (reach == 2) k_pairs_c<2><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
-    else if (reach == 3) k_pairs_c<3><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
-    else k_pairs_c<4><<<grid, 256, 0, st>>>(B, perm, G, n, rho);
+                         cudaStream_t st, const WindowMasks* M = nullptr) {
+    if (M) launch_pairs_t<true>(B, perm, G, n, reach, rho, *M, st);
+    else launch_pairs_t<false>(B, perm, G, n, reach, rho, WindowMasks{nullptr, nullptr, 0}, st);
 }
 
 
@@ -459,7 +538,7 @@ void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t 
 
 void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                           const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* rho,
-                          cudaStream_t st) {
+                          cudaStream_t st, int32_t* win) {
     require_device();
     if (nb < 1 || nb > 3 || NX <= 0 || ny <= 0 || nz <= 0 || n_home > n || reach < 1 || reach > 4 || !(cell > 0))
         throw std::invalid_argument("bad cell grid");
@@ -476,7 +555,14 @@ void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const
     }
     if (n == 0) return;
     CellGrid G{blocks[0].x_origin, lo_yz[0], lo_yz[1], 1.0f / cell, NX, ny, nz, reach, int64_t(n_home)};
-    launch_pairs(B, perm, G, int64_t(n), reach, rho, st);
+    if (win && reach <= 2) {  // window bases are tagged (block << 30): every block must hold < 2^30 particles
+        if (n >= (1ull << 30)) throw std::invalid_argument("window masks need fewer than 2^30 particles per block");
+        const WindowMasks M{reinterpret_cast<int2*>(win), reinterpret_cast<uint32_t*>(win) + window_mask_words(n, reach) - n,
+                            int64_t(n)};
+        launch_pairs(B, perm, G, int64_t(n), reach, rho, st, &M);
+    } else {
+        launch_pairs(B, perm, G, int64_t(n), reach, rho, st);
+    }
     check_cuda(cudaGetLastError(), "density_cells_blocks launch");
     count_launches(1);
 }
@@ -533,6 +619,41 @@ struct ForceBlockSet {
     int nb, NX;
 };
 
+// One force term (sph.cpp:201-245) of candidate (pj = (x, m), vj = (v, P/rho^2))
+// on home (pi, vi), accumulated into s:
+//   (ax, ay, az) += m_j (P_i/rho_i^2 + P_j/rho_j^2) pi h_ij^4 dW/dr / r * dx
+//   cp           += m_j pi h_ij^4 dW/dr / r * (v_i - v_j) . dx
+// with pi h^4 dW/dr = 3 max(1-q,0)^2 - 0.75 max(2-q,0)^2 (q < 1: -3q + 2.25q^2,
+// sph.cpp:30; 1 <= q < 2: -0.75 (2-q)^2, sph.cpp:32), exactly 0 at r = 0, so
+// the self term vanishes as in grad_w (sph.cpp:35-40) without a j != i test.
+struct ForceSums {
+    float ax, ay, az, cp;
+};
+__device__ __forceinline__ void force_term(const float4 pi, const float4 vi, float inv_h, float ih4, const float4 pj,
+                                           const float4 vj, ForceSums& s) {
+    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
+    const float q = (r2 * inv_r) * inv_h;
+    const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
+    const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
+    const float msc = pj.w * (dw * ih4 * inv_r);           // m_j pi dW/dr / r
+    const float f = msc * (vi.w + vj.w);
+    s.ax = fmaf(f, dx, s.ax);
+    s.ay = fmaf(f, dy, s.ay);
+    s.az = fmaf(f, dz, s.az);
+    s.cp = fmaf(msc, fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x))), s.cp);
+}
+
+__device__ __forceinline__ void store_force(const ForceSums& s, float pfi, int64_t i, float* __restrict__ a_out,
+                                            float* __restrict__ du_out) {
+    constexpr float kInvPi = 0.31830988618379067f;
+    a_out[3 * i] = -kInvPi * s.ax;
+    a_out[3 * i + 1] = -kInvPi * s.ay;
+    a_out[3 * i + 2] = -kInvPi * s.az;
+    du_out[i] = pfi * (kInvPi * s.cp);
+}
+
 template <int R, int U, bool UNI>
 __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t* __restrict__ perm, const CellGrid& G,
                                            int64_t k, float hmax, float* __restrict__ a_out,
@@ -559,7 +680,7 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
     const float ih4u = (inv_hu * inv_hu) * (inv_hu * inv_hu);
     const float fzc = fminf(fmaxf(fz, -1e6f), 1e6f);
     const int zmin = max(iz - R, 0), zmax = min(iz + R, G.nz - 1);
-    float ax = 0.0f, ay = 0.0f, az = 0.0f, cp = 0.0f;
+    ForceSums S{0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll 1
     for (int dxi = -R; dxi <= R; ++dxi) {
         const int jx = ix + dxi;
@@ -572,30 +693,13 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
         const float* __restrict__ hs = B.b[g].h;
         const int32_t* __restrict__ cell_start = B.b[g].cs;
         auto pair = [&](int j) {
-            const float4 pj = pos[j];  // (x, y, z, m)
-            const float4 vj = vel[j];  // (v, P/rho^2)
-            const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            const float inv_r = rsqrt_approx(fmaxf(r2, 1e-30f));
-            float inv_h, ih4;
             if constexpr (UNI) {
-                inv_h = inv_hu, ih4 = ih4u;
+                force_term(pi, vi, inv_hu, ih4u, pos[j], vel[j], S);
             } else {
-                inv_h = rcp_approx(fmaf(0.5f, __ldg(hs + j), hh_i));
+                const float inv_h = rcp_approx(fmaf(0.5f, __ldg(hs + j), hh_i));
                 const float ih2 = inv_h * inv_h;
-                ih4 = ih2 * ih2;
+                force_term(pi, vi, inv_h, ih2 * ih2, pos[j], vel[j], S);
             }
-            const float q = (r2 * inv_r) * inv_h;
-            const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
-            const float dw = fmaf(-0.75f * t, t, 3.0f * u * u);  // pi h^4 dW/dr
-            const float sc = dw * ih4 * inv_r;                    // pi dW/dr / r
-            const float msc = pj.w * sc;
-            const float f = msc * (pfi + vj.w);
-            ax = fmaf(f, dx, ax);
-            ay = fmaf(f, dy, ay);
-            az = fmaf(f, dz, az);
-            const float dvx = fmaf(dz, vi.z - vj.z, fmaf(dy, vi.y - vj.y, dx * (vi.x - vj.x)));
-            cp = fmaf(msc, dvx, cp);
         };
         const float ddx = fmaxf(fmaxf(jx > 0 ? float(jx) - fx : 0.0f, jx < B.NX - 1 ? fx - float(jx + 1) : 0.0f),
                                 0.0f);
@@ -627,11 +731,74 @@ __device__ __forceinline__ void force_home(const ForceBlockSet& B, const int32_t
             for (; j < e[t]; ++j) pair(j);
         }
     }
-    constexpr float kInvPi = 0.31830988618379067f;
-    a_out[3 * i_home] = -kInvPi * ax;
-    a_out[3 * i_home + 1] = -kInvPi * ay;
-    a_out[3 * i_home + 2] = -kInvPi * az;
-    du_out[i_home] = pfi * (kInvPi * cp);
+    store_force(S, pfi, i_home, a_out, du_out);
+}
+
+// The force of one home from the in-support bit masks the density of the
+// same step wrote (exactly the in-support pairs, no culling arithmetic): one
+// flattened loop over the home's windows, refilling (base, bits) when the
+// current mask is spent, so a lane's iterations are its ~65 pairs plus the
+// (2R+1)^2 refills rather than the sum over windows of the warp's longest
+// run.  A home with an over-long window falls back to the window sweep.
+template <int R, bool UNI>
+__device__ __forceinline__ void force_masked_home(const ForceBlockSet& B, const int32_t* __restrict__ perm,
+                                                  const CellGrid& G, int64_t k, float hmax, const WindowMasks& M,
+                                                  float* __restrict__ a_out, float* __restrict__ du_out) {
+    const int64_t i_home = perm ? perm[k] : k;
+    if (i_home >= G.n_home) return;  // ghosts: neighbours only
+    uint32_t occ = M.occ[k];
+    if (occ & kOccOverflow) {
+        force_home<R, 2, UNI>(B, perm, G, k, hmax, a_out, du_out);
+        return;
+    }
+    const float4 pi = B.b[0].pos[k], vi = B.b[0].vel[k];
+    const float h_i = B.b[0].h[k], hh_i = 0.5f * h_i;
+    const float inv_hu = rcp_approx(h_i);
+    const float ih4u = (inv_hu * inv_hu) * (inv_hu * inv_hu);
+    ForceSums S{0.0f, 0.0f, 0.0f, 0.0f};
+    const int2* __restrict__ win = M.win + k;
+    int g = 0, base = 0;
+    uint32_t bits = 0;
+    const float4* __restrict__ pos = B.b[0].pos;
+    const float4* __restrict__ vel = B.b[0].vel;
+    const float* __restrict__ hs = B.b[0].h;
+    auto term = [&](int j, bool real) {
+        float4 pj = pos[j];
+        if (!real) pj.w = 0.0f;  // padding lane of a pair: zero mass, zero contribution
+        if constexpr (UNI) {
+            force_term(pi, vi, inv_hu, ih4u, pj, vel[j], S);
+        } else {
+            const float inv_h = rcp_approx(fmaf(0.5f, __ldg(hs + j), hh_i));
+            const float ih2 = inv_h * inv_h;
+            force_term(pi, vi, inv_h, ih2 * ih2, pj, vel[j], S);
+        }
+    };
+#pragma unroll 1
+    for (;;) {
+        if (bits == 0) {  // next occupied window (a block switch is rare: only at slab faces)
+            if (occ == 0) break;
+            const int w = __ffs(occ) - 1;
+            occ &= occ - 1;
+            const int2 t = __ldg(win + int64_t(w) * M.stride);
+            bits = uint32_t(t.y);
+            base = int(uint32_t(t.x) & 0x3fffffffu);
+            const int gn = int(uint32_t(t.x) >> 30);
+            if (gn != g) {
+                g = gn;
+                pos = B.b[g].pos, vel = B.b[g].vel, hs = B.b[g].h;
+            }
+            continue;
+        }
+        // two in-support candidates per iteration (independent loads and terms)
+        const int j0 = base + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const bool two = bits != 0;
+        const int j1 = two ? base + __ffs(bits) - 1 : j0;
+        if (two) bits &= bits - 1;
+        term(j0, true);
+        term(j1, two);
+    }
+    store_force(S, vi.w, i_home, a_out, du_out);
 }
 
 template <int R, int U>
@@ -652,6 +819,25 @@ static void launch_force(const ForceBlockSet& B, const int32_t* perm, const Cell
     else if (reach == 2) k_force_c<2, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
     else if (reach == 3) k_force_c<3, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
     else k_force_c<4, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_force_masked(const ForceBlockSet B, const int32_t* __restrict__ perm,
+                                                      CellGrid G, int64_t n, const WindowMasks M,
+                                                      float* __restrict__ a_out, float* __restrict__ du_out) {
+    float hmax;
+    const bool uni = uniform_h(B, &hmax);
+    const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    if (uni) force_masked_home<R, true>(B, perm, G, k, hmax, M, a_out, du_out);
+    else force_masked_home<R, false>(B, perm, G, k, hmax, M, a_out, du_out);
+}
+
+static void launch_force_masked(const ForceBlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
+                                const WindowMasks& M, float* a, float* du, cudaStream_t st) {
+    const unsigned grid = unsigned((uint64_t(n) + 255) / 256);
+    if (reach == 1) k_force_masked<1><<<grid, 256, 0, st>>>(B, perm, G, n, M, a, du);
+    else k_force_masked<2><<<grid, 256, 0, st>>>(B, perm, G, n, M, a, du);
 }
 
 // (v, P/rho^2) of a packed block, in its cell-sorted order; rho == 0 sets *zero
@@ -746,7 +932,7 @@ void force_pack(const void* v, const void* rho, const void* pr, int prec, uint64
 
 void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                         const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* a, float* du,
-                        cudaStream_t st) {
+                        cudaStream_t st, const int32_t* win) {
     require_device();
     if (nb < 1 || nb > 3 || NX <= 0 || ny <= 0 || nz <= 0 || n_home > n || reach < 1 || reach > 4 || !(cell > 0))
         throw std::invalid_argument("bad cell grid");
@@ -764,7 +950,15 @@ void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const 
     }
     if (n == 0) return;
     CellGrid G{blocks[0].x_origin, lo_yz[0], lo_yz[1], 1.0f / cell, NX, ny, nz, reach, int64_t(n_home)};
-    launch_force(B, perm, G, int64_t(n), reach, a, du, st);
+    if (win && reach <= 2) {  // the window masks the density of this step wrote for the same blocks
+        if (n >= (1ull << 30)) throw std::invalid_argument("window masks need fewer than 2^30 particles per block");
+        int32_t* w = const_cast<int32_t*>(win);
+        const WindowMasks M{reinterpret_cast<int2*>(w), reinterpret_cast<uint32_t*>(w) + window_mask_words(n, reach) - n,
+                            int64_t(n)};
+        launch_force_masked(B, perm, G, int64_t(n), reach, M, a, du, st);
+    } else {
+        launch_force(B, perm, G, int64_t(n), reach, a, du, st);
+    }
     check_cuda(cudaGetLastError(), "force_cells_blocks launch");
     count_launches(1);
 }

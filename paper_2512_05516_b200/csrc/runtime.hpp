@@ -65,9 +65,15 @@ struct CellBlockDesc {
 };
 void cells_pack(const void* x, const void* m, const void* h, int prec, uint64_t n, const int32_t* perm, void* pos,
                 float* hs, unsigned* hmax, cudaStream_t st);
+// win (optional, window_mask_words(n, reach) 32-bit words, 8-byte aligned): every home's per-window
+// in-support bit masks, written by the density for the force of the same step (force_cells_blocks(..., win)
+// then sweeps exactly those pairs); used for reach <= 2, ignored above
 void density_cells_blocks(const CellBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                           const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* rho,
-                          cudaStream_t st);
+                          cudaStream_t st, int32_t* win = nullptr);
+inline uint64_t window_mask_words(uint64_t n, int reach) {
+    return (2 * uint64_t(2 * reach + 1) * (2 * reach + 1) + 1) * n;  // (base, bits) per window + occupancy
+}
 struct ForceBlockDesc {
     const void* pos;   // float4 (x, y, z, m): the density block's
     const void* vel;   // float4 (vx, vy, vz, P/rho^2)
@@ -84,7 +90,7 @@ void force_pack(const void* v, const void* rho, const void* pr, int prec, uint64
                 cudaStream_t st);
 void force_cells_blocks(const ForceBlockDesc* blocks, int nb, uint64_t n, const int32_t* perm, uint64_t n_home,
                         const float* lo_yz, float cell, int NX, int ny, int nz, int reach, float* a, float* du,
-                        cudaStream_t st);
+                        cudaStream_t st, const int32_t* win = nullptr);
 void force_cells(const void* x, const void* v, const void* m, const void* h, const void* rho, const void* pr,
                  int prec, uint64_t n, const int32_t* perm, const int32_t* cell_start, const float* lo, float cell,
                  int nx, int ny, int nz, int reach, uint64_t n_home, float* a, float* du, cudaStream_t st);

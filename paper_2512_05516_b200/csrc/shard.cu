@@ -253,6 +253,8 @@ struct Shard {
     uint64_t ncell = 0;
     ShardLayout L{};
     std::unique_ptr<DevMem> shared, state[2], scratch, perm, classes, misc;
+    std::unique_ptr<DevMem> wmask;  // the density's per-window in-support masks for the force
+    uint64_t wmask_n = 0;           // homes they hold
     int cur = 0;
     uint64_t bin_bytes = 0, scan_bytes = 0;
     struct Peer {
@@ -468,6 +470,22 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
         }
     };
     bool force_ran = false;
+    // density then force in one step: the density writes every home's per-window in-support masks and the
+    // force sweeps exactly those pairs (no culling arithmetic, no out-of-support candidates)
+    int32_t* win = nullptr;
+    bool win_ready = false;
+    {
+        const auto di = std::find(kernels.begin(), kernels.end(), "density");
+        const auto fi = std::find(kernels.begin(), kernels.end(), "force");
+        if (di != kernels.end() && fi != kernels.end() && di < fi && S->n > 0 && S->n < (1ull << 30)) {
+            if (!S->wmask || S->wmask_n < S->n) {
+                S->wmask.reset();
+                S->wmask_n = S->n + S->n / 8 + 1024;
+                S->wmask.reset(new DevMem(window_mask_words(S->wmask_n, S->refine) * 4));
+            }
+            win = S->wmask->as<int32_t>();
+        }
+    }
     for (size_t ki = 0; ki < kernels.size(); ++ki) {
         const std::string& k = kernels[ki];
         mark(int(2 * ki));
@@ -477,7 +495,8 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
         }
         if (k == "density") {
             density_cells_blocks(dblocks.data(), int(dblocks.size()), S->n, perm, S->n, lo_yz, S->fine, S->NF, S->NF,
-                                 S->NF, S->refine, reinterpret_cast<float*>(S->field(c, F_RHO)), st);
+                                 S->NF, S->refine, reinterpret_cast<float*>(S->field(c, F_RHO)), st, win);
+            win_ready = win != nullptr;
         } else if (k == "force") {
             // the neighbours finished reading this block's (v, P/rho^2) in the previous step (E_READ_DONE,
             // waited in bin_and_pack); rho == 0 -> *rho_zero, checked at the end of the step
@@ -487,7 +506,7 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
             wait_peers(S, E_PACKED_FORCE, s, st);
             force_cells_blocks(fblocks.data(), int(fblocks.size()), S->n, perm, S->n, lo_yz, S->fine, S->NF, S->NF,
                                S->NF, S->refine, reinterpret_cast<float*>(S->field(c, F_A)),
-                               reinterpret_cast<float*>(S->field(c, F_DU)), st);
+                               reinterpret_cast<float*>(S->field(c, F_DU)), st, win_ready ? win : nullptr);
             force_ran = true;
         } else if (k == "kick") {
             // sph.cpp:247-256: v += a dt; u = max(0, u + du dt) in binary64, stored binary32
