@@ -773,23 +773,31 @@ __device__ __forceinline__ void force_masked_home(const ForceBlockSet& B, const 
             force_term(pi, vi, inv_h, ih2 * ih2, pj, vel[j], S);
         }
     };
+    // software pipeline: the next occupied window's (base, bits) is loaded while the current one is swept;
+    // an exhausted window is replaced by it with register moves only, in the same iteration as the next two
+    // terms, so lanes that switch windows do not stall the others
+    auto fetch = [&](uint32_t& o) {
+        int2 t = make_int2(0, 0);
+        if (o) {
+            t = __ldg(win + int64_t(__ffs(o) - 1) * M.stride);
+            o &= o - 1;
+        }
+        return t;
+    };
+    int2 nxt = fetch(occ);
 #pragma unroll 1
-    for (;;) {
+    while (bits | uint32_t(nxt.y)) {
         if (bits == 0) {  // next occupied window (a block switch is rare: only at slab faces)
-            if (occ == 0) break;
-            const int w = __ffs(occ) - 1;
-            occ &= occ - 1;
-            const int2 t = __ldg(win + int64_t(w) * M.stride);
-            bits = uint32_t(t.y);
-            base = int(uint32_t(t.x) & 0x3fffffffu);
-            const int gn = int(uint32_t(t.x) >> 30);
+            bits = uint32_t(nxt.y);
+            base = int(uint32_t(nxt.x) & 0x3fffffffu);
+            const int gn = int(uint32_t(nxt.x) >> 30);
             if (gn != g) {
                 g = gn;
                 pos = B.b[g].pos, vel = B.b[g].vel, hs = B.b[g].h;
             }
-            continue;
+            nxt = fetch(occ);
         }
-        // two in-support candidates per iteration (independent loads and terms)
+        // two in-support candidates of the window per iteration (independent loads and terms)
         const int j0 = base + __ffs(bits) - 1;
         bits &= bits - 1;
         const bool two = bits != 0;
