@@ -598,9 +598,9 @@ def sharded_c5(args, world, rank, peak, peak_kind):
     # compute rooflines of the two pair kernels (uniform particles: 64 in-support neighbours by construction)
     pairs = 64.0 * n / world
     if phases.get("force"):
-        out["roofline"] = compute_roofline("k_force_c (fp32, per rank)", pairs, 40, phases["force"], "force_c5")
+        out["roofline"] = compute_roofline("pack + k_force_masked (fp32, per rank: the in-support pairs the density marked)", pairs, 40, phases["force"], "force_c5")
     if phases.get("density"):
-        out["roofline_density"] = compute_roofline("bin + pack + k_pairs_c (fp32, per rank)", pairs, 24,
+        out["roofline_density"] = compute_roofline("bin + pack + k_pairs_c with window masks (fp32, per rank)", pairs, 24,
                                                    phases["density"], "pairs_c5")
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
