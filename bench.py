@@ -533,6 +533,10 @@ def run_extras(args, world, rank, peak, peak_kind):
                                              k["fp32"]["density_ms"], "pairs_c3_fp32")
             r["roofline_force"] = compute_roofline("k_force_c (fp32)", pairs, 40, k["force_fp32"]["force_ms"],
                                                    "force_c3_fp32")
+            if "step_fp32" in k:
+                r["roofline_force_masked"] = compute_roofline(
+                    "k_force_masked (fp32, after a density that marked the in-support pairs)", pairs, 40,
+                    k["step_fp32"]["force_masked_ms"], "force_masked_c3_fp32")
             r["hbm_frac_fp32"] = k["fp32"]["hbm_GBps_algorithmic"] / peak
             if not args.no_cpu:
                 rate, secs = cpu_reference_kernels_rate(1 << 20, ["density"], threads, T=32, layout="soa")

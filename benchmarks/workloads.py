@@ -204,6 +204,40 @@ def c3(args, peak, peak_kind):
                                  "pairs_in_support_per_s": pairs / (msf * 1e-3),
                                  "note": "pack (x,h | v,m | P/rho^2) + k_force_c; includes the rho == 0 check "
                                          "(one stream sync)"}
+            if refine <= 2:
+                # one SPH step's density then force sharing the pair search (block API, window masks): the
+                # density marks every home's in-support pairs, the force evaluates exactly those
+                pos = torch.empty(n, 4, device="cuda")
+                hsb = torch.empty(n, device="cuda")
+                hmx = torch.zeros(4, dtype=torch.int32, device="cuda")
+                api.cells_pack(xs, ms_, hs, perm, pos, hsb, hmx, prec=prec)
+                blk = api.cell_block(pos, hsb, cs, hmx, 0, dims[0], 0.0)
+                mk = api.window_masks(n, refine)
+                geo = (n, perm, (0.0, 0.0), fine, dims[0], dims[1], dims[2])
+                rho2 = torch.empty(n, device="cuda")
+                fdm = lambda: api.density_cells_blocks([blk], *geo, reach=refine, rho=rho2, masks=mk)  # noqa: E731
+                fdp = lambda: api.density_cells_blocks([blk], *geo, reach=refine, rho=rho2)  # noqa: E731
+                for _ in range(args.warmup):
+                    fdp()
+                    fdm()
+                tdp = timed_each(fdp, max(3, args.steps // 5))
+                tdm = timed_each(fdm, max(3, args.steps // 5))
+                velb = torch.empty(n, 4, device="cuda")
+                api.force_pack(vel, rho2, rho2 * (2.0 / 3.0), perm, velb)
+                fbk = api.force_block(pos, velb, hsb, cs, hmx, 0, dims[0], 0.0)
+                a2, du2 = torch.empty(n, 3, device="cuda"), torch.empty(n, device="cuda")
+                ffm = lambda: api.force_cells_blocks([fbk], *geo, reach=refine, a=a2, du=du2, masks=mk)  # noqa: E731
+                for _ in range(args.warmup):
+                    ffm()
+                tfm = timed_each(ffm, max(3, args.steps // 5))
+                mdp, mdm, mfm = (sum(t_) / len(t_) for t_ in (tdp, tdm, tfm))
+                out["step_fp32"] = {
+                    "density_pairs_ms": mdp, "density_pairs_masked_ms": mdm, "force_masked_ms": mfm,
+                    "density_then_force_ms": mdm + mfm,
+                    "pairs_in_support_per_s_force": pairs / (mfm * 1e-3),
+                    "note": "pair kernels only (the block API: bin and pack done once outside): k_pairs_c, "
+                            "k_pairs_c writing window masks, then k_force_masked over the marked pairs; "
+                            "compare density_pairs_ms + the window-sweep force"}
     ms = out["fp32"]["density_ms"]
     rl = {"bound": "issue (FP32 + MUFU)", "achieved": out["fp32"]["hbm_GBps_algorithmic"], "peak": peak,
           "unit": "GB/s", "frac": out["fp32"]["hbm_GBps_algorithmic"] / peak, "peak_kind": peak_kind,

@@ -196,6 +196,23 @@ SF_API sf_status sf_b200_force_cells_blocks(const sf_force_block* blocks, int nb
                                             const int32_t* perm, uint64_t n_home, const float* lo_yz,
                                             float cell, int nx_global, int ny, int nz, int reach,
                                             float* a_out, float* du_out, void* stream);
+/* One SPH step's density then force over the same blocks, sharing the pair
+ * search: the density also writes `masks` (caller-owned device memory of
+ * sf_b200_window_mask_bytes(n, reach), 8-B aligned) — for every home and
+ * neighbour-column window, the window's first candidate and a bit per
+ * in-support candidate — and the force then evaluates exactly those pairs
+ * (no culling, no out-of-support candidates; a home with a window of more
+ * than 32 candidates falls back to the window sweep).  The masks are valid
+ * for the force of the same blocks, perm and grid only.  reach <= 2. */
+SF_API uint64_t sf_b200_window_mask_bytes(uint64_t n, int reach);
+SF_API sf_status sf_b200_density_cells_blocks_masked(const sf_cell_block* blocks, int nblocks, uint64_t n,
+                                                     const int32_t* perm, uint64_t n_home, const float* lo_yz,
+                                                     float cell, int nx_global, int ny, int nz, int reach,
+                                                     float* rho_out, void* masks, void* stream);
+SF_API sf_status sf_b200_force_cells_blocks_masked(const sf_force_block* blocks, int nblocks, uint64_t n,
+                                                   const int32_t* perm, uint64_t n_home, const float* lo_yz,
+                                                   float cell, int nx_global, int ny, int nz, int reach,
+                                                   float* a_out, float* du_out, const void* masks, void* stream);
 /* Device memory that another process can map (cudaMalloc base), and CUDA IPC
  * handles for it (same node; NVLink/NVSwitch peers or the same device). */
 SF_API sf_status sf_b200_dev_alloc(uint64_t bytes, void** ptr);

@@ -96,6 +96,10 @@ SYMBOLS = [
     ("sf_b200_density_cells_blocks", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P]),
     ("sf_b200_force_pack", i32, [P, P, P, i32, u64, P, P, P]),
     ("sf_b200_force_cells_blocks", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P, P]),
+    ("sf_b200_window_mask_bytes", u64, [u64, i32]),
+    ("sf_b200_density_cells_blocks_masked", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P, P]),
+    ("sf_b200_force_cells_blocks_masked", i32, [P, i32, u64, P, u64, P, C.c_float, i32, i32, i32, i32, P, P, P,
+                                                P]),
     ("sf_b200_dev_alloc", i32, [u64, PP]),
     ("sf_b200_dev_free", i32, [P]),
     ("sf_b200_ipc_handle", i32, [P, P]),

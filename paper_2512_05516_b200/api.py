@@ -362,20 +362,34 @@ def cell_block(pos, hs, cell_start, hmax, x0: int, nx: int, x_origin: float) -> 
     return L.SfCellBlock(addr(pos), addr(hs), addr(cell_start), addr(hmax), x0, nx, float(x_origin), 0)
 
 
+def window_masks(n: int, reach: int):
+    """Device buffer for the window masks one density hands to the force of
+    the same step (reach 1 or 2)."""
+    import torch
+    nbytes = int(lib().sf_b200_window_mask_bytes(n, reach))
+    if nbytes == 0:
+        raise L.SfInvalidArg("window masks need reach 1 or 2")
+    return torch.empty(nbytes // 8, dtype=torch.int64, device="cuda")
+
+
 def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,
-                         reach: int = 1, rho=None):
+                         reach: int = 1, rho=None, masks=None):
     """Cell-linked density of blocks[0]'s first n_home particles with
-    candidates from every block (own slab + neighbouring slabs in place)."""
+    candidates from every block (own slab + neighbouring slabs in place).
+    masks (window_masks(n, reach)): also record every home's in-support
+    pairs for force_cells_blocks(..., masks=) of the same step."""
     import torch
     n_home = n if n_home is None else n_home
     alloc = torch.empty if n_home == n else torch.zeros  # entries past n_home are not written
     rho = rho if rho is not None else alloc(max(n, 1), dtype=torch.float32, device="cuda")
     arr = (L.SfCellBlock * len(blocks))(*blocks)
     lo_arr = (C.c_float * 2)(*[float(t) for t in lo_yz])
-    check(lib().sf_b200_density_cells_blocks(C.cast(arr, C.c_void_p), len(blocks), n,
-                                             _ptr(perm) if perm is not None else None, n_home,
-                                             C.cast(lo_arr, C.c_void_p), float(cell), nx_global, ny, nz, reach,
-                                             _ptr(rho), _stream()))
+    args = (C.cast(arr, C.c_void_p), len(blocks), n, _ptr(perm) if perm is not None else None, n_home,
+            C.cast(lo_arr, C.c_void_p), float(cell), nx_global, ny, nz, reach, _ptr(rho))
+    if masks is None:
+        check(lib().sf_b200_density_cells_blocks(*args, _stream()))
+    else:
+        check(lib().sf_b200_density_cells_blocks_masked(*args, _ptr(masks), _stream()))
     return rho
 
 
@@ -396,9 +410,11 @@ def force_block(pos, vel, hs, cell_start, hmax, x0: int, nx: int, x_origin: floa
 
 
 def force_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,
-                       reach: int = 1, a=None, du=None):
+                       reach: int = 1, a=None, du=None, masks=None):
     """Cell-linked force of blocks[0]'s first n_home particles with
-    candidates from every block; returns (a (n,3), du (n,))."""
+    candidates from every block; returns (a (n,3), du (n,)).  masks: the
+    window masks density_cells_blocks(..., masks=) wrote for these blocks
+    (the force then evaluates exactly the in-support pairs)."""
     import torch
     n_home = n if n_home is None else n_home
     alloc = torch.empty if n_home == n else torch.zeros  # entries past n_home are not written
@@ -406,10 +422,12 @@ def force_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int,
     du = du if du is not None else alloc(max(n, 1), dtype=torch.float32, device="cuda")
     arr = (L.SfForceBlock * len(blocks))(*blocks)
     lo_arr = (C.c_float * 2)(*[float(t) for t in lo_yz])
-    check(lib().sf_b200_force_cells_blocks(C.cast(arr, C.c_void_p), len(blocks), n,
-                                           _ptr(perm) if perm is not None else None, n_home,
-                                           C.cast(lo_arr, C.c_void_p), float(cell), nx_global, ny, nz, reach,
-                                           _ptr(a), _ptr(du), _stream()))
+    args = (C.cast(arr, C.c_void_p), len(blocks), n, _ptr(perm) if perm is not None else None, n_home,
+            C.cast(lo_arr, C.c_void_p), float(cell), nx_global, ny, nz, reach, _ptr(a), _ptr(du))
+    if masks is None:
+        check(lib().sf_b200_force_cells_blocks(*args, _stream()))
+    else:
+        check(lib().sf_b200_force_cells_blocks_masked(*args, _ptr(masks), _stream()))
     return a, du
 
 

@@ -341,6 +341,47 @@ sf_status sf_b200_force_cells_blocks(const sf_force_block* blocks, int nblocks, 
     });
 }
 
+uint64_t sf_b200_window_mask_bytes(uint64_t n, int reach) {
+    return reach >= 1 && reach <= 2 ? 4 * window_mask_words(n, reach) : 0;
+}
+
+sf_status sf_b200_density_cells_blocks_masked(const sf_cell_block* blocks, int nblocks, uint64_t n,
+                                              const int32_t* perm, uint64_t n_home, const float* lo_yz, float cell,
+                                              int nx_global, int ny, int nz, int reach, float* rho_out, void* masks,
+                                              void* stream) {
+    if (!blocks || !lo_yz || (n && (!rho_out || !masks))) return fail(SF_INVALID_ARG, "null argument");
+    if (reach < 1 || reach > 2) return fail(SF_INVALID_ARG, "window masks need reach 1 or 2");
+    if (reinterpret_cast<uintptr_t>(masks) & 7) return fail(SF_INVALID_ARG, "masks must be 8-byte aligned");
+    return guarded([&] {
+        std::vector<CellBlockDesc> d(size_t(std::max(nblocks, 0)));
+        for (int g = 0; g < nblocks; ++g)
+            d[g] = CellBlockDesc{blocks[g].pos,    blocks[g].h,        blocks[g].cell_start, blocks[g].hmax,
+                                 blocks[g].x0,     blocks[g].nx,       blocks[g].x_origin,   0};
+        density_cells_blocks(d.data(), nblocks, n, perm, n_home, lo_yz, cell, nx_global, ny, nz, reach, rho_out,
+                             static_cast<cudaStream_t>(stream), static_cast<int32_t*>(masks));
+        return SF_OK;
+    });
+}
+
+sf_status sf_b200_force_cells_blocks_masked(const sf_force_block* blocks, int nblocks, uint64_t n,
+                                            const int32_t* perm, uint64_t n_home, const float* lo_yz, float cell,
+                                            int nx_global, int ny, int nz, int reach, float* a_out, float* du_out,
+                                            const void* masks, void* stream) {
+    if (!blocks || !lo_yz || (n && (!a_out || !du_out || !masks))) return fail(SF_INVALID_ARG, "null argument");
+    if (reach < 1 || reach > 2) return fail(SF_INVALID_ARG, "window masks need reach 1 or 2");
+    if (reinterpret_cast<uintptr_t>(masks) & 7) return fail(SF_INVALID_ARG, "masks must be 8-byte aligned");
+    return guarded([&] {
+        std::vector<ForceBlockDesc> d(size_t(std::max(nblocks, 0)));
+        for (int g = 0; g < nblocks; ++g)
+            d[g] = ForceBlockDesc{blocks[g].pos,  blocks[g].vel, blocks[g].h,        blocks[g].cell_start,
+                                  blocks[g].hmax, blocks[g].x0,  blocks[g].nx,       blocks[g].x_origin,
+                                  0};
+        force_cells_blocks(d.data(), nblocks, n, perm, n_home, lo_yz, cell, nx_global, ny, nz, reach, a_out, du_out,
+                           static_cast<cudaStream_t>(stream), static_cast<const int32_t*>(masks));
+        return SF_OK;
+    });
+}
+
 sf_status sf_b200_dev_alloc(uint64_t bytes, void** out) {
     if (!out) return fail(SF_INVALID_ARG, "null argument");
     return guarded([&] {

@@ -396,3 +396,61 @@ def test_bench_under_torchrun_two_ranks_one_device(workload, tmp_path):
         assert "unavailable" not in c5, c5
         assert c5["n_gpus"] == 2 and c5["value"] > 0 and c5["particles_total"] == 1 << 20
         assert c5["phases_ms_max_over_ranks"]["force"] > 0
+
+
+@pytest.mark.parametrize("world,refine,spread,clustered", [(1, 2, False, False), (3, 2, True, False),
+                                                          (2, 1, False, False), (2, 2, False, True)])
+def test_masked_force_after_density_matches_oracle(world, refine, spread, clustered):
+    """One step's density writes window masks (sf_b200_density_cells_blocks_masked)
+    and the force sweeps exactly the marked pairs (..._force_cells_blocks_masked):
+    same rho, and a / du within the force tolerance of the oracle, across
+    slabs (peer blocks), with spread h (general pair term) and with clustered
+    particles whose dense windows exceed 32 candidates (those homes fall back
+    to the window sweep)."""
+    n = 1 << 14
+    rng = np.random.default_rng(31 + world + refine)
+    x = rng.random((n, 3))
+    if clustered:  # a tight clump: windows far beyond 32 candidates
+        k = n // 8
+        x[:k] = np.clip(0.5 + rng.normal(0, 0.004, (k, 3)), 0, 1 - 1e-9)
+    h, nc, cell = grid_for(n)
+    hh = np.full(n, h) * (rng.uniform(0.85, 1.0, n) if spread else 1.0)
+    m = rng.uniform(0.5, 1.5, n) / n
+    v = rng.uniform(-1, 1, (n, 3))
+    P = rng.uniform(0.2, 1.2, n)
+    dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
+    S = _slab_blocks(x, m, hh, nc, cell, world, refine)
+    rho_all = np.zeros(n)
+    masks, vels = [], []
+    grid = lambda r: (S[r]["n"], S[r]["perm"], (0.0, 0.0), cell / refine, nc * refine, nc * refine,  # noqa: E731
+                      nc * refine)
+    for r in range(world):
+        blocks = [S[r]["block"]] + [S[q]["block"] for q in (r - 1, r + 1) if 0 <= q < world]
+        mk = api.window_masks(S[r]["n"], refine)
+        plain = api.density_cells_blocks(blocks, *grid(r), reach=refine).clone()
+        rho = api.density_cells_blocks(blocks, *grid(r), reach=refine, masks=mk)
+        torch.testing.assert_close(rho, plain, rtol=0, atol=0)  # the masks do not change rho
+        rho_all[S[r]["own"]] = rho[:S[r]["n"]].double().cpu().numpy()
+        masks.append(mk)
+    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+    for r in range(world):
+        own = S[r]["own"]
+        vel = torch.empty(S[r]["n"], 4, device="cuda")
+        api.force_pack(t(v[own]), t(rho_all[own]), t(P[own]), S[r]["perm"], vel)
+        vels.append(vel)
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(hh),
+                                    dec(rho_all), dec(P), 0.0, 1.0, cell)
+    FORCE_TOL = 2e-5
+    for r in range(world):
+        fb = lambda q: api.force_block(S[q]["keep"][4], vels[q], S[q]["keep"][5], S[q]["keep"][3],  # noqa: E731
+                                       S[q]["keep"][6], S[q]["block"].x0, S[q]["block"].nx,
+                                       S[q]["block"].x_origin)
+        blocks = [fb(r)] + [fb(q) for q in (r - 1, r + 1) if 0 <= q < world]
+        a, du = api.force_cells_blocks(blocks, *grid(r), reach=refine, masks=masks[r])
+        pa, pdu = api.force_cells_blocks(blocks, *grid(r), reach=refine)
+        own = S[r]["own"]
+        a_np, du_np = a[:S[r]["n"]].double().cpu().numpy(), du[:S[r]["n"]].double().cpu().numpy()
+        assert np.all(np.linalg.norm(a_np - wa[own], axis=1) <= FORCE_TOL * sa[own])
+        assert np.all(np.abs(du_np - wdu[own]) <= FORCE_TOL * sd[own] + 1e-30)
+        # the masked and the window sweep agree to summation rounding
+        torch.testing.assert_close(a, pa, rtol=1e-4, atol=2e-5 * float(pa.abs().max()))
