@@ -453,7 +453,7 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
 static unsigned pair_grid(uint64_t n) { return unsigned(((n + 1) / 2 + 255) / 256); }
 
 template <int R, bool LIST>
-__global__ void __launch_bounds__(256, 4) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+__global__ void __launch_bounds__(256, 5) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
                                                  int64_t n, float* __restrict__ rho, const WindowMasks M) {
     float hmax;
     const bool uni = uniform_h(B, &hmax);
