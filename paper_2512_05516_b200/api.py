@@ -369,7 +369,7 @@ def window_masks(n: int, reach: int):
     nbytes = int(lib().sf_b200_window_mask_bytes(n, reach))
     if nbytes == 0:
         raise L.SfInvalidArg("window masks need reach 1 or 2")
-    return torch.empty(nbytes // 8, dtype=torch.int64, device="cuda")
+    return torch.empty((nbytes + 7) // 8, dtype=torch.int64, device="cuda")  # 8-B aligned (int2 windows)
 
 
 def density_cells_blocks(blocks, n: int, perm, lo_yz, cell: float, nx_global: int, ny: int, nz: int, n_home=None,

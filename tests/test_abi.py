@@ -254,6 +254,20 @@ def test_block_and_ipc_entry_points_fail_loudly_without_device():
     arr = (L.SfCellBlock * 1)(blk)
     assert lib.sf_b200_density_cells_blocks(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 1, p(f), None) == L.SF_ERROR
     assert lib.sf_b200_force_pack(p(f), p(f), p(f), 1, n, p(i32), p(f), None) == L.SF_ERROR
+    # window masks (one step's density -> force): size, reach and alignment checked before any device work
+    assert lib.sf_b200_window_mask_bytes(n, 2) == 4 * (2 * 25 + 1) * n
+    assert lib.sf_b200_window_mask_bytes(n, 1) == 4 * (2 * 9 + 1) * n
+    assert lib.sf_b200_window_mask_bytes(n, 3) == 0
+    masks = (C.c_int64 * ((lib.sf_b200_window_mask_bytes(n, 2) + 15) // 8))()
+    assert lib.sf_b200_density_cells_blocks_masked(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 3, p(f), p(masks),
+                                                   None) == L.SF_INVALID_ARG
+    assert lib.sf_b200_density_cells_blocks_masked(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 2, p(f),
+                                                   C.c_void_p(C.cast(masks, C.c_void_p).value + 4), None) \
+        == L.SF_INVALID_ARG
+    assert lib.sf_b200_density_cells_blocks_masked(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 2, p(f), None,
+                                                   None) == L.SF_INVALID_ARG
+    assert lib.sf_b200_density_cells_blocks_masked(p(arr), 1, n, p(i32), n, p(lo), 0.5, 2, 2, 2, 2, p(f), p(masks),
+                                                   None) == L.SF_ERROR  # no device
     out = C.c_void_p()
     assert lib.sf_b200_dev_alloc(1024, C.byref(out)) == L.SF_ERROR
     assert "no CUDA device" in lib.sf_last_error().decode()
