@@ -1,6 +1,8 @@
 """C5 sharded path on one B200: a full N=1 step against the oracle, and the
 per-rank density with ghost layers (simulated 2- and 4-rank splits of one
 population) against the global oracle density."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -454,3 +456,58 @@ def test_masked_force_after_density_matches_oracle(world, refine, spread, cluste
         assert np.all(np.abs(du_np - wdu[own]) <= FORCE_TOL * sd[own] + 1e-30)
         # the masked and the window sweep agree to summation rounding
         torch.testing.assert_close(a, pa, rtol=1e-4, atol=2e-5 * float(pa.abs().max()))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SFB_RANDOM_MASKED", "4"))))
+def test_random_masked_density_force_vs_oracle(seed):
+    """Random cases for the window-mask hand-off: particle count, slabs 1-3,
+    reach 1 / 2, uniform or spread h, a clustered fraction (windows beyond
+    32 candidates); rho with and without masks bit-identical, the masked force
+    within the force tolerance of the binary64 oracle."""
+    rng = np.random.default_rng(9100 + seed)
+    n = int(rng.integers(3000, 24000))
+    world, refine = int(rng.integers(1, 4)), int(rng.integers(1, 3))
+    x = rng.random((n, 3))
+    k = int(n * rng.uniform(0, 0.25))
+    if k:
+        c = rng.random((3, 3)) * 0.8 + 0.1
+        x[:k] = np.clip(c[rng.integers(0, 3, k)] + rng.normal(0, rng.choice([0.003, 0.02]), (k, 3)), 0, 1 - 1e-9)
+    h, nc, cell = grid_for(n)
+    if nc < 2 * world:
+        world = 1
+    hh = np.full(n, h) * (rng.uniform(0.8, 1.0, n) if rng.random() < 0.5 else 1.0)
+    m = rng.uniform(0.5, 1.5, n) / n
+    v, P = rng.uniform(-1, 1, (n, 3)), rng.uniform(0.2, 1.2, n)
+    dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
+    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+    S = _slab_blocks(x, m, hh, nc, cell, world, refine)
+    grid = lambda r: (S[r]["n"], S[r]["perm"], (0.0, 0.0), cell / refine, nc * refine, nc * refine,  # noqa: E731
+                      nc * refine)
+    rho_all, masks = np.zeros(n), []
+    for r in range(world):
+        blocks = [S[r]["block"]] + [S[q]["block"] for q in (r - 1, r + 1) if 0 <= q < world]
+        mk = api.window_masks(S[r]["n"], refine)
+        plain = api.density_cells_blocks(blocks, *grid(r), reach=refine).clone()
+        rho = api.density_cells_blocks(blocks, *grid(r), reach=refine, masks=mk)
+        assert torch.equal(rho, plain)
+        rho_all[S[r]["own"]] = rho[:S[r]["n"]].double().cpu().numpy()
+        masks.append(mk)
+    np.testing.assert_allclose(rho_all, O.density_cells(dec(x).reshape(-1), dec(m), dec(hh), 0.0, 1.0, cell),
+                               rtol=1e-5)
+    vels = []
+    for r in range(world):
+        own = S[r]["own"]
+        vel = torch.empty(S[r]["n"], 4, device="cuda")
+        api.force_pack(t(v[own]), t(rho_all[own]), t(P[own]), S[r]["perm"], vel)
+        vels.append(vel)
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(hh), dec(rho_all), dec(P),
+                                    0.0, 1.0, cell)
+    for r in range(world):
+        fb = lambda q: api.force_block(S[q]["keep"][4], vels[q], S[q]["keep"][5], S[q]["keep"][3],  # noqa: E731
+                                       S[q]["keep"][6], S[q]["block"].x0, S[q]["block"].nx, S[q]["block"].x_origin)
+        blocks = [fb(r)] + [fb(q) for q in (r - 1, r + 1) if 0 <= q < world]
+        a, du = api.force_cells_blocks(blocks, *grid(r), reach=refine, masks=masks[r])
+        own = S[r]["own"]
+        a_np, du_np = a[:S[r]["n"]].double().cpu().numpy(), du[:S[r]["n"]].double().cpu().numpy()
+        assert np.all(np.linalg.norm(a_np - wa[own], axis=1) <= 2e-5 * sa[own])
+        assert np.all(np.abs(du_np - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
