@@ -229,7 +229,9 @@ def kernels_table(particles):
                       "gpu_updates_per_s": particles / gs if gs > 0 else None,
                       "checksum_equal": r["checksum"] == g["checksum"]}
     return {"particles": particles, "cpu_threads": threads, "rows": table,
-            "note": "density = 64-particle buffer mode (reference semantics, binary64); GPU time excludes transfers"}
+            "note": "density = 64-particle buffer mode (reference semantics, binary64); GPU time excludes transfers; "
+                    "at this size (the reference bench command's own scale, ~10 s of CPU) the GPU kick/drift rows are "
+                    "launch-bound: soa_vs_aos holds the 16M-particle layout comparison"}
 
 
 def dist_init():
