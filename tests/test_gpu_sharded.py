@@ -511,3 +511,35 @@ def test_random_masked_density_force_vs_oracle(seed):
         a_np, du_np = a[:S[r]["n"]].double().cpu().numpy(), du[:S[r]["n"]].double().cpu().numpy()
         assert np.all(np.linalg.norm(a_np - wa[own], axis=1) <= 2e-5 * sa[own])
         assert np.all(np.abs(du_np - wdu[own]) <= 2e-5 * sd[own] + 1e-30)
+
+
+def test_masked_density_force_with_ghost_particles():
+    """n_home < n: the masks cover the homes only (ghosts feed their
+    neighbours) and the masked force writes no ghost."""
+    n = 1 << 13
+    rng = np.random.default_rng(77)
+    x = rng.random((n, 3))
+    h, nc, cell = grid_for(n)
+    hh, m = np.full(n, h), rng.uniform(0.5, 1.5, n) / n
+    v, P = rng.uniform(-1, 1, (n, 3)), rng.uniform(0.2, 1.2, n)
+    dec = lambda a: torch.tensor(a, dtype=torch.float32).double().numpy()  # noqa: E731
+    S = _slab_blocks(x, m, hh, nc, cell, 1, 2)[0]
+    n_home = n - 700  # particle indices >= n_home are ghosts
+    geo = (n, S["perm"], (0.0, 0.0), cell / 2, 2 * nc, 2 * nc, 2 * nc)
+    mk = api.window_masks(n, 2)
+    rho = api.density_cells_blocks([S["block"]], *geo, n_home=n_home, reach=2, masks=mk)
+    want = O.density_cells(dec(x).reshape(-1), dec(m), dec(hh), 0.0, 1.0, cell)
+    np.testing.assert_allclose(rho[:n_home].double().cpu().numpy(), want[:n_home], rtol=1e-5)
+    rho_all = want.astype(np.float32)  # ghosts carry the oracle's rho (as a neighbour rank would)
+    t = lambda a: torch.tensor(a, device="cuda", dtype=torch.float32)  # noqa: E731
+    vel = torch.empty(n, 4, device="cuda")
+    api.force_pack(t(v), t(rho_all), t(P), S["perm"], vel)
+    xt, mt, ht, cs, pos, hs, hmax = S["keep"]
+    fb = api.force_block(pos, vel, hs, cs, hmax, 0, 2 * nc, 0.0)
+    a, du = api.force_cells_blocks([fb], *geo, n_home=n_home, reach=2, masks=mk)
+    wa, wdu, sa, sd = O.force_cells(dec(x).reshape(-1), dec(v).reshape(-1), dec(m), dec(hh), dec(rho_all), dec(P),
+                                    0.0, 1.0, cell)
+    a_np, du_np = a.double().cpu().numpy(), du.double().cpu().numpy()
+    assert np.all(np.linalg.norm(a_np[:n_home] - wa[:n_home], axis=1) <= 2e-5 * sa[:n_home])
+    assert np.all(np.abs(du_np[:n_home] - wdu[:n_home]) <= 2e-5 * sd[:n_home] + 1e-30)
+    assert np.all(a_np[n_home:] == 0) and np.all(du_np[n_home:] == 0)
