@@ -196,6 +196,24 @@ __device__ __forceinline__ f32x2 density_pair2(f32x2 X, f32x2 Y, f32x2 Z, const 
     return fma2(w, pk2(pj.w, pj.w), acc);
 }
 
+// The general (spread-h) pair term for two homes: h_ij = (h_i + h_j) / 2 per
+// pair, so 1/h_ij (two MUFU.RCP) and its cube are per pair; HH = (h_0, h_1) / 2.
+// acc += m_j / h_ij^3 (t^3 - u^3), t = sat(1 - q/2), u = sat(c (1 - q)).
+__device__ __forceinline__ f32x2 density_pair2_h(f32x2 X, f32x2 Y, f32x2 Z, float hh0, float hh1, const float4 pj,
+                                                 float hj, f32x2 acc, bool& in0, bool& in1) {
+    const f32x2 dx = sub2(X, pk2(pj.x, pj.x)), dy = sub2(Y, pk2(pj.y, pj.y)), dz = sub2(Z, pk2(pj.z, pj.z));
+    const f32x2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    const f32x2 ih = pk2(rcp_approx(fmaf(0.5f, hj, hh0)), rcp_approx(fmaf(0.5f, hj, hh1)));
+    const f32x2 q = mul2(pk2(sqrt_approx(lo2(r2)), sqrt_approx(hi2(r2))), ih);
+    const float q0 = lo2(q), q1 = hi2(q);
+    const float t0 = __saturatef(fmaf(-0.5f, q0, 1.0f)), t1 = __saturatef(fmaf(-0.5f, q1, 1.0f));
+    in0 = t0 > 0.0f, in1 = t1 > 0.0f;
+    const f32x2 t = pk2(t0, t1);
+    const f32x2 u = pk2(__saturatef(fmaf(-kC3, q0, kC3)), __saturatef(fmaf(-kC3, q1, kC3)));
+    const f32x2 w = sub2(mul2(mul2(t, t), t), mul2(mul2(u, u), u));
+    return fma2(w, mul2(mul2(mul2(ih, ih), ih), pk2(pj.w, pj.w)), acc);
+}
+
 // The density's in-support bit masks for the force of the same step (which
 // needs every rho first, then exactly the same pairs).  For window w (the
 // neighbour columns in (dx, dy) row-major order, reach <= 2: 25 windows) of
@@ -411,32 +429,41 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
         if (live0) rho[H.i0] = res0 * scale;
         if (live1) rho[H.i1] = res1 * scale;
     } else {
-        // spread h: one home at a time, h_ij = (h_i + h_j) / 2 per pair
+        // spread h: h_ij = (h_i + h_j) / 2 per pair, both homes per candidate (packed)
+        const bool same = H.ix0 == H.ix1 && H.iy0 == H.iy1;
+        const float hh0 = 0.5f * H.h0, hh1 = 0.5f * H.h1;
+        const f32x2 X = hold2(H.p0.x, H.p1.x), Y = hold2(H.p0.y, H.p1.y), Z = hold2(H.p0.z, H.p1.z);
+        float res0 = 0.0f, res1 = 0.0f;
 #pragma unroll 1
-        for (int m = 0; m < 2; ++m) {
-            if (!(m ? live1 : live0)) continue;
-            const float4 pi = m ? H.p1 : H.p0;
-            const float hh = 0.5f * (m ? H.h1 : H.h0);
-            const float rc = (2.0f * hh + hmax) * G.inv_cell * 1.00001f;
-            float acc = 0.0f;
-            pass_runs<R>(B, G, H, m == 0, m == 1, rc * rc, [&](int w, int g, int b, int e) {
+        for (int pass = 0; pass < (same ? 1 : 2); ++pass) {
+            const bool m0 = same || pass == 0, m1 = same || pass == 1;
+            const float hm = m0 ? (m1 ? fmaxf(H.h0, H.h1) : H.h0) : H.h1;
+            const float rc = (hm + hmax) * G.inv_cell * 1.00001f;  // support bound, cell units
+            f32x2 acc = 0ull;
+            pass_runs<R>(B, G, H, m0, m1, rc * rc, [&](int w, int g, int b, int e) {
                 const float4* __restrict__ pos = B.b[g].pos;
                 const float* __restrict__ hs = B.b[g].h;
+                uint32_t mk0 = 0, mk1 = 0, bit = 1;
                 const bool fit = e - b <= 32;
-                uint32_t mk = 0;
 #pragma unroll 1
-                for (int j = b; j < e; ++j) {
-                    const float4 pj = pos[j];
-                    const float ih = rcp_approx(fmaf(0.5f, __ldg(hs + j), hh));
-                    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-                    const float r = sqrt_approx(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    acc = fmaf(pj.w * ((ih * ih) * ih), spline_w8(r, ih), acc);
-                    if (LIST && fit) mk |= uint32_t(fmaf(-0.5f * ih, r, 1.0f) > 0.0f) << (j - b);
+                for (int j = b; j < e; ++j, bit <<= 1) {
+                    bool a0, a1;
+                    acc = density_pair2_h(X, Y, Z, hh0, hh1, pos[j], __ldg(hs + j), acc, a0, a1);
+                    if constexpr (LIST) {
+                        if (a0) mk0 |= bit;
+                        if (a1) mk1 |= bit;
+                    }
                 }
-                if constexpr (LIST) put(m == 1, w, g, b, mk, fit);
+                if constexpr (LIST) {
+                    if (m0 && live0) put(false, w, g, b, mk0, fit);
+                    if (m1 && live1) put(true, w, g, b, mk1, fit);
+                }
             });
-            rho[m ? H.i1 : H.i0] = acc * k2InvPi;
+            if (m0) res0 = lo2(acc);
+            if (m1) res1 = hi2(acc);
         }
+        if (live0) rho[H.i0] = res0 * k2InvPi;
+        if (live1) rho[H.i1] = res1 * k2InvPi;
     }
     if constexpr (LIST) {
         if (live0) M.occ[k0] = occ0;
