@@ -23,6 +23,10 @@
 //                 every candidate runs the same branch-free pair term against
 //                 both homes at once (packed fp32, 1/h_ij hoisted when h is
 //                 uniform).  rho is stored back in particle (unsorted) order.
+//                 With window masks (one SPH step's density then force), the
+//                 sweep also records every home's in-support candidates per
+//                 window, and k_force_masked (force section) evaluates exactly
+//                 those pairs.
 //
 // With cells of side >= 2h use reach 1 (27 cells); with cells of side >= h
 // reach 2 (125 smaller cells, ~84 after culling).  Pair formula: the
