@@ -477,7 +477,8 @@ void shard_step(Shard* S, const std::vector<std::string>& kernels, double dt, cu
     {
         const auto di = std::find(kernels.begin(), kernels.end(), "density");
         const auto fi = std::find(kernels.begin(), kernels.end(), "force");
-        if (di != kernels.end() && fi != kernels.end() && di < fi && S->n > 0 && S->n < (1ull << 30)) {
+        if (di != kernels.end() && fi != kernels.end() && di < fi && S->refine <= 2 && S->n > 0 &&
+            S->n < (1ull << 30)) {  // window masks: reach <= 2
             if (!S->wmask || S->wmask_n < S->n) {
                 S->wmask.reset();
                 S->wmask_n = S->n + S->n / 8 + 1024;
