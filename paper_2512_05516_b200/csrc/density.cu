@@ -481,10 +481,11 @@ __device__ __forceinline__ void pairs_home2(const BlockSet& B, const int32_t* __
 // and their candidate columns stay in L2 (with the grid capped at 16 CTAs/SM
 // the resident CTAs strode through the whole range and the L2 hit rate at C5
 // fell from 91% to 46%).
-static unsigned pair_grid(uint64_t n) { return unsigned(((n + 1) / 2 + 255) / 256); }
+constexpr int kPairThreads = 128;
+static unsigned pair_grid(uint64_t n) { return unsigned(((n + 1) / 2 + kPairThreads - 1) / kPairThreads); }
 
 template <int R, bool LIST>
-__global__ void __launch_bounds__(256, 5) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+__global__ void __launch_bounds__(kPairThreads, 10) k_pairs_c(const BlockSet B, const int32_t* __restrict__ perm, CellGrid G,
                                                  int64_t n, float* __restrict__ rho, const WindowMasks M) {
     float hmax;
     const bool uni = uniform_h(B, &hmax);
@@ -498,11 +499,11 @@ template <bool LIST>
 static void launch_pairs_t(const BlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
                            float* rho, const WindowMasks& M, cudaStream_t st) {
     const unsigned grid = pair_grid(uint64_t(n));
-    if (reach == 1) k_pairs_c<1, LIST><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
-    else if (reach == 2) k_pairs_c<2, LIST><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
+    if (reach == 1) k_pairs_c<1, LIST><<<grid, kPairThreads, 0, st>>>(B, perm, G, n, rho, M);
+    else if (reach == 2) k_pairs_c<2, LIST><<<grid, kPairThreads, 0, st>>>(B, perm, G, n, rho, M);
     else if constexpr (!LIST) {  // window masks: 25 windows at most (reach <= 2)
-        if (reach == 3) k_pairs_c<3, false><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
-        else k_pairs_c<4, false><<<grid, 256, 0, st>>>(B, perm, G, n, rho, M);
+        if (reach == 3) k_pairs_c<3, false><<<grid, kPairThreads, 0, st>>>(B, perm, G, n, rho, M);
+        else k_pairs_c<4, false><<<grid, kPairThreads, 0, st>>>(B, perm, G, n, rho, M);
     }
 }
 
