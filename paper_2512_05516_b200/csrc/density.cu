@@ -842,7 +842,7 @@ __device__ __forceinline__ void force_masked_home(const ForceBlockSet& B, const 
 }
 
 template <int R, int U>
-__global__ void __launch_bounds__(256) k_force_c(const ForceBlockSet B, const int32_t* __restrict__ perm, CellGrid G,
+__global__ void __launch_bounds__(128) k_force_c(const ForceBlockSet B, const int32_t* __restrict__ perm, CellGrid G,
                                                  int64_t n, float* __restrict__ a_out, float* __restrict__ du_out) {
     float hmax;
     const bool uni = uniform_h(B, &hmax);
@@ -854,11 +854,12 @@ __global__ void __launch_bounds__(256) k_force_c(const ForceBlockSet B, const in
 
 static void launch_force(const ForceBlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
                          float* a, float* du, cudaStream_t st) {
-    const unsigned grid = unsigned((uint64_t(n) + 255) / 256);  // one thread per home, in index order
-    if (reach == 1) k_force_c<1, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-    else if (reach == 2) k_force_c<2, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-    else if (reach == 3) k_force_c<3, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
-    else k_force_c<4, 2><<<grid, 256, 0, st>>>(B, perm, G, n, a, du);
+    constexpr unsigned T = 128;
+    const unsigned grid = unsigned((uint64_t(n) + T - 1) / T);  // one thread per home, in index order
+    if (reach == 1) k_force_c<1, 2><<<grid, T, 0, st>>>(B, perm, G, n, a, du);
+    else if (reach == 2) k_force_c<2, 2><<<grid, T, 0, st>>>(B, perm, G, n, a, du);
+    else if (reach == 3) k_force_c<3, 2><<<grid, T, 0, st>>>(B, perm, G, n, a, du);
+    else k_force_c<4, 2><<<grid, T, 0, st>>>(B, perm, G, n, a, du);
 }
 
 template <int R>
@@ -875,9 +876,10 @@ __global__ void __launch_bounds__(256) k_force_masked(const ForceBlockSet B, con
 
 static void launch_force_masked(const ForceBlockSet& B, const int32_t* perm, const CellGrid& G, int64_t n, int reach,
                                 const WindowMasks& M, float* a, float* du, cudaStream_t st) {
-    const unsigned grid = unsigned((uint64_t(n) + 255) / 256);
-    if (reach == 1) k_force_masked<1><<<grid, 256, 0, st>>>(B, perm, G, n, M, a, du);
-    else k_force_masked<2><<<grid, 256, 0, st>>>(B, perm, G, n, M, a, du);
+    constexpr unsigned T = 256;
+    const unsigned grid = unsigned((uint64_t(n) + T - 1) / T);
+    if (reach == 1) k_force_masked<1><<<grid, T, 0, st>>>(B, perm, G, n, M, a, du);
+    else k_force_masked<2><<<grid, T, 0, st>>>(B, perm, G, n, M, a, du);
 }
 
 // (v, P/rho^2) of a packed block, in its cell-sorted order; rho == 0 sets *zero
